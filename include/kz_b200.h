@@ -1,0 +1,155 @@
+/*
+ * kz_b200.h -- C-ABI of the B200-native RK / RKA / RKAB iteration loop.
+ *
+ * This is the drop-in boundary between the reference's Python entry points
+ * (kaczbench, /root/reference/pkg/src/kaczbench) and the sm_100a kernels.
+ * A ctypes binding (paper_2401_17474_b200/_native.py, or the stub in
+ * INTEGRATION.md) calls these functions; no torch or C++ types cross it.
+ *
+ * Conventions
+ *   - Every function returns an int status (KZ_OK = 0).  On failure a
+ *     thread-local message is available from kz_last_error().  Status codes
+ *     map onto the reference's exception taxonomy (errors.py:4-58).
+ *   - Pointers suffixed _host are host memory (pageable or pinned); the
+ *     library copies them.  Pointers suffixed _dev are device memory owned
+ *     by the caller.  `stream` is a cudaStream_t (NULL = legacy default).
+ *   - All calls are synchronous with respect to the host on return unless
+ *     stated otherwise ("at most one solve in flight per process",
+ *     SPEC.md:593; the reference solvers are blocking calls).
+ *   - Inputs are never modified (solvers.py:194: the solver owns x).
+ */
+#ifndef KZ_B200_H
+#define KZ_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KZ_API __attribute__((visibility("default")))
+#else
+#define KZ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum kz_status {
+    KZ_OK = 0,
+    KZ_EINVAL = 1,      /* ValueError / DimensionMismatchError (solvers.py:85-101, linalg.py:30-47) */
+    KZ_EDEGENERATE = 2, /* DegenerateRowError (linalg.py:84-86)                                      */
+    KZ_EEMPTYRANGE = 3, /* EmptyRangeError (sampling.py:194-195, 213-218)                            */
+    KZ_ENOMEM = 4,      /* device allocation failed                                                  */
+    KZ_ECUDA = 5,       /* CUDA runtime / launch error                                               */
+    KZ_ENODEV = 6       /* no CUDA device                                                            */
+};
+
+enum kz_variant { KZ_RK = 0, KZ_RKA = 1, KZ_RKAB = 2 };          /* solvers.py:55 VARIANTS        */
+enum kz_scheme { KZ_FULL_ACCESS = 0, KZ_DISTRIBUTED = 1 };        /* solvers.py:57 SAMPLING_SCHEMES */
+enum kz_kernel {                                                  /* engine selection (auto = 0)    */
+    KZ_KERNEL_AUTO = 0,
+    KZ_KERNEL_CHAIN = 1,        /* worker-per-CTA persistent kernel (RK, RKAB)                   */
+    KZ_KERNEL_SYNC_CLUSTER = 2, /* column-sliced kernel, one thread-block cluster, DSMEM reduce  */
+    KZ_KERNEL_SYNC_GRID = 3     /* column-sliced kernel, whole grid, global-memory reduce        */
+};
+
+typedef struct kz_system kz_system;
+
+/* ---- library ---------------------------------------------------------- */
+KZ_API const char* kz_last_error(void);
+KZ_API int32_t kz_version(void);
+/* Kernels this library has launched in this process (all devices). */
+KZ_API int64_t kz_launch_count(void);
+KZ_API int32_t kz_device_count(int32_t* count);
+
+/* ---- system residency ----------------------------------------------------
+ * Replaces the numpy views of LinearSystem (sysgen.py:84-115) that every
+ * solver reads (solvers.py:193).  A is stored row-major with a padded pitch
+ * (kz_system_pitch) so every row starts on a 128-byte boundary.
+ * x_ref is the stopping reference (LinearSystem.x_ref, sysgen.py:110-115). */
+KZ_API int32_t kz_system_create(int32_t device, int64_t m, int64_t n, kz_system** out);
+KZ_API int32_t kz_system_destroy(kz_system* sys);
+KZ_API int64_t kz_system_pitch(const kz_system* sys);
+/* Host -> device copies.  lda >= n.  b_host: m values; xref_host: n values or NULL. */
+KZ_API int32_t kz_system_upload(kz_system* sys, const double* A_host, int64_t lda, const double* b_host,
+                         const double* xref_host, void* stream);
+/* Device -> device copies from caller-owned device arrays (lda >= n). */
+KZ_API int32_t kz_system_upload_device(kz_system* sys, const double* A_dev, int64_t lda, const double* b_dev,
+                                const double* xref_dev, void* stream);
+/* Raw device pointers of the resident arrays (pitched A, b, x_ref), for
+ * in-place generation of large systems. */
+KZ_API int32_t kz_system_device_ptrs(kz_system* sys, double** A_dev, double** b_dev, double** xref_dev);
+/* Replace the stopping reference x_ref (n values, host). */
+KZ_API int32_t kz_system_set_xref(kz_system* sys, const double* xref_host, void* stream);
+/* Invalidate cached row norms / samplers after A was written in place. */
+KZ_API int32_t kz_system_touch(kz_system* sys);
+
+/* ---- row norms: row_norm_cache (linalg.py:80-88) ------------------------
+ * Bit-exact with np.einsum("ij,ij->i") (SSE2 two-lane order).  Cached on
+ * the system.  Returns KZ_EDEGENERATE with *bad_row = first zero row.
+ * sq_host (m values) may be NULL. */
+KZ_API int32_t kz_row_norms(kz_system* sys, double* sq_host, int64_t* bad_row, void* stream);
+
+/* ---- sampler: make_sampler / worker_streams (sampling.py:189-199,
+ * solvers.py:162-171) ------------------------------------------------------
+ * Builds the inclusive CDF(s) for (scheme, q): one CDF over all rows
+ * (full_access) or one per block partition_bounds(m, q, t) (distributed).
+ * cdf_host (m values, concatenated per block) may be NULL. */
+KZ_API int32_t kz_sampler_build(kz_system* sys, int32_t scheme, int64_t q, double* cdf_host, void* stream);
+/* Row draws `start .. start+count-1` of worker `worker` for Prng(base_seed,
+ * worker) (RowSampler.sample, sampling.py:177-182): bit-exact indices. */
+KZ_API int32_t kz_dump_rows(kz_system* sys, int32_t scheme, int64_t q, uint64_t base_seed, int64_t worker,
+                     int64_t start, int64_t count, int32_t* out_host, void* stream);
+
+/* ---- solve: solve_rk / solve_rka_seq / solve_rkab_seq via _drive
+ * (solvers.py:182-263, 294-371) ---------------------------------------- */
+typedef struct {
+    int32_t variant;        /* kz_variant                                                     */
+    int32_t scheme;         /* kz_scheme                                                      */
+    int64_t q;              /* workers (SolverConfig.q)                                       */
+    int64_t block_size;     /* RKAB chain length (SolverConfig.block_size)                    */
+    const double* alphas_host; /* q row weights (resolve_alphas); NULL = unit                  */
+    uint64_t base_seed;     /* SolverConfig.base_seed                                         */
+    double epsilon;         /* stop when ||x - x_ref||^2 < epsilon                            */
+    int64_t max_iterations; /* SolverConfig.max_iterations                                    */
+    int64_t budget;         /* > 0: fixed-budget replay, stop rule disabled (_drive budget)   */
+    int64_t trace_step;     /* > 0: trace mode, records at 0, s, 2s ... (_drive trace)         */
+    double* trace_host;     /* (max_iterations/trace_step + 1) x 3: iteration, ||x-xref||, ||Ax-b|| */
+    int64_t ckpt_every;     /* > 0: store x after every ckpt_every iterations (capture)        */
+    int64_t ckpt_capacity;  /* rows of ckpt_host                                               */
+    double* ckpt_host;      /* ckpt_capacity x n                                               */
+    int32_t kernel;         /* kz_kernel (0 = auto)                                            */
+    int32_t threads;        /* CTA size override (0 = auto)                                    */
+    int32_t ctas;           /* CTA count override for sync kernels (0 = auto)                  */
+    int32_t want_residual;  /* compute ||Ax - b|| at the end of a stop-mode run                */
+} kz_params;
+
+typedef struct {
+    int64_t iterations;     /* RunReport.iterations                                           */
+    int32_t converged;      /* RunReport.converged                                            */
+    int32_t kernel_used;    /* kz_kernel actually run                                         */
+    double final_error_sq;  /* RunReport.final_error_sq (NaN outside stop mode)               */
+    double final_residual;  /* RunReport.final_residual (NaN unless computed)                 */
+    int64_t error_evals;    /* RunReport.error_evals                                          */
+    int64_t n_ckpt;         /* checkpoints written                                            */
+    int64_t n_trace;        /* trace records written                                          */
+    int64_t rows_projected; /* row projections performed (iterations x q x block_size)        */
+    double loop_ms;         /* device time of the iteration loop (CUDA events)                */
+    double kernel_ms;       /* device time inside the solve kernels only                      */
+    int64_t kernel_launches;/* kernels launched by this call                                  */
+    int32_t ctas;           /* CTAs of the solve kernel                                       */
+    int32_t threads;        /* threads per CTA of the solve kernel                            */
+} kz_result;
+
+/* Full solve with host output x_host (n values, may be NULL). */
+KZ_API int32_t kz_solve(kz_system* sys, const kz_params* params, kz_result* result, double* x_host, void* stream);
+/* Device pointer of the final iterate of the last kz_solve on this system (n values). */
+KZ_API int32_t kz_solution_device(kz_system* sys, double** x_dev);
+
+/* ---- norms used by traces and reports (solvers.py:174-179, 246) ---------- */
+/* ||A x - b||_2 and ||x - x_ref||_2 for a host x (n values). */
+KZ_API int32_t kz_norms(kz_system* sys, const double* x_host, double* residual, double* error, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,15 @@
+"""B200-native RK / RKA / RKAB iteration loop (arXiv 2401.17474) behind the
+reference kaczbench entry points.  See DESIGN.md for the architecture and
+include/kz_b200.h for the C-ABI boundary."""
+
+from .errors import (ConvergenceError, DegenerateRowError, DimensionMismatchError, EmptyRangeError,
+                     SpectralConvergenceError, SystemFormatError, TransportProtocolError, UnsupportedVersionError)
+from .harness import (MeasureResult, Protocol, ReplayResult, bench, measure_iterations, plateau_error,
+                      timed_replay, trace_run)
+from .reports import REPORT_HEADER, TRACE_HEADER, RunReport, TraceRecord
+from .solvers import (ALPHA_POLICIES, ENGINES, SAMPLING_SCHEMES, VARIANTS, DeviceSystem, SolverConfig,
+                      resolve_alphas, run_solver, solve_rk, solve_rka_seq, solve_rkab_seq)
+from .sysgen import (GeneratorConfig, LinearSystem, Prng, cgls_solve, crop, generate_mother, make_inconsistent,
+                     partition_bounds, worker_rng)
+
+__version__ = "0.1.0"

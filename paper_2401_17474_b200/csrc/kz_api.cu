@@ -1,0 +1,859 @@
+// kz_api.cu -- the C-ABI (include/kz_b200.h): system residency, row norms,
+// samplers, and the solve driver that replaces the reference's _drive loop
+// (solvers.py:182-263) for RK / RKA / RKAB (solvers.py:294-371).
+//
+// The driver is native: it samples row indices for a chunk of iterations on
+// the device (x-independent, bit-exact with RowSampler.sample), launches one
+// persistent solve kernel per chunk, and reads back a 24-byte status word to
+// learn whether the stop rule fired.  Python never runs per iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kz_b200.h"
+#include "kz_kernels.cuh"
+
+using namespace kz;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define KZ_CUDA(call)                                                                                    \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess) return fail(KZ_ECUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+    } while (0)
+
+#define KZ_TRY(call)              \
+    do {                          \
+        int rc_ = (call);         \
+        if (rc_ != KZ_OK) return rc_; \
+    } while (0)
+
+static int check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(KZ_ECUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+    return KZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SeedSequence -> PCG64 seeding on the host (numpy bit_generator.pyx / pcg64.c,
+// as used by Prng(seed, worker), sampling.py:132-136).  Integer-exact.
+// ---------------------------------------------------------------------------
+namespace {
+
+uint32_t ss_hashmix(uint32_t v, uint32_t& hc) {
+    v ^= hc;
+    hc *= 0x931e8875u;
+    v *= hc;
+    v ^= v >> 16;
+    return v;
+}
+uint32_t ss_mix(uint32_t x, uint32_t y) {
+    uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+    r ^= r >> 16;
+    return r;
+}
+
+PcgPod seed_stream(uint64_t seed, uint64_t stream) {
+    std::vector<uint32_t> words;
+    for (uint64_t v : {seed, stream}) {
+        if (v == 0) {
+            words.push_back(0);
+        } else {
+            while (v) {
+                words.push_back((uint32_t)(v & 0xffffffffu));
+                v >>= 32;
+            }
+        }
+    }
+    uint32_t pool[4];
+    uint32_t hc = 0x43b0d7e5u;
+    for (int i = 0; i < 4; ++i) pool[i] = ss_hashmix(i < (int)words.size() ? words[i] : 0u, hc);
+    for (int s = 0; s < 4; ++s)
+        for (int d = 0; d < 4; ++d)
+            if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], hc));
+    for (size_t s = 4; s < words.size(); ++s)
+        for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(words[s], hc));
+    uint32_t out[8];
+    uint32_t hb = 0x8b51f9ddu;
+    for (int i = 0; i < 8; ++i) {
+        uint32_t v = pool[i % 4];
+        v ^= hb;
+        hb *= 0x58f38dedu;
+        v *= hb;
+        v ^= v >> 16;
+        out[i] = v;
+    }
+    uint64_t u[4];
+    for (int i = 0; i < 4; ++i) u[i] = (uint64_t)out[2 * i] | ((uint64_t)out[2 * i + 1] << 32);
+    const u128 initstate = ((u128)u[0] << 64) | u[1];
+    const u128 initseq = ((u128)u[2] << 64) | u[3];
+    Pcg g;
+    g.inc = (initseq << 1) | 1u;
+    g.s = 0;
+    g.s = g.s * pcg_mult() + g.inc;
+    g.s += initstate;
+    g.s = g.s * pcg_mult() + g.inc;
+    PcgPod p;
+    p.s_hi = (unsigned long long)(g.s >> 64);
+    p.s_lo = (unsigned long long)g.s;
+    p.inc_hi = (unsigned long long)(g.inc >> 64);
+    p.inc_lo = (unsigned long long)g.inc;
+    return p;
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    int ensure(size_t n) {
+        if (n <= cap) return KZ_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(KZ_ENOMEM, "cudaMalloc of %zu bytes failed", n * sizeof(T));
+        }
+        cap = n;
+        return KZ_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// system
+// ---------------------------------------------------------------------------
+struct kz_system {
+    int device = 0;
+    int64_t m = 0, n = 0, ld = 0;
+    int sms = 0;
+    DevBuf<double> A, b, xref, x, sq, cdf, tmp, V, part, ckpt, alphas;
+    DevBuf<int64_t> lo, len;
+    DevBuf<int32_t> idx, rows_out;
+    DevBuf<PcgPod> states;
+    DevBuf<unsigned> barrier;
+    DevBuf<SolveStatus> status;
+    DevBuf<unsigned long long> zero_row;
+    SolveStatus* h_status = nullptr;  // pinned
+    bool norms_valid = false;
+    int64_t bad_row = -1;
+    int sampler_scheme = -1;
+    int64_t sampler_q = 0;
+    bool has_xref = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+extern "C" const char* kz_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t kz_version(void) { return 1; }
+extern "C" int64_t kz_launch_count(void) { return g_launches.load(); }
+
+extern "C" int32_t kz_device_count(int32_t* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *count = 0;
+        return fail(KZ_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    *count = c;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_system_create(int32_t device, int64_t m, int64_t n, kz_system** out) {
+    *out = nullptr;
+    if (m < 1 || n < 1) return fail(KZ_EINVAL, "matrix dimensions must be >= 1, got (%lld, %lld)", (long long)m, (long long)n);
+    if (m > INT32_MAX) return fail(KZ_EINVAL, "m=%lld exceeds the 32-bit row index range", (long long)m);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(KZ_ENODEV, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(KZ_EINVAL, "device %d out of range (%d devices)", device, ndev);
+    KZ_CUDA(cudaSetDevice(device));
+    kz_system* s = new kz_system();
+    s->device = device;
+    s->m = m;
+    s->n = n;
+    s->ld = (n + 15) / 16 * 16;  // 128-byte row pitch
+    cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, device);
+    int rc = KZ_OK;
+    if ((rc = s->A.ensure((size_t)m * s->ld)) || (rc = s->b.ensure(m)) || (rc = s->xref.ensure(s->ld)) ||
+        (rc = s->x.ensure(s->ld)) || (rc = s->sq.ensure(m)) || (rc = s->cdf.ensure(m)) ||
+        (rc = s->tmp.ensure(std::max<int64_t>(m, s->ld))) || (rc = s->status.ensure(1)) ||
+        (rc = s->barrier.ensure(1)) || (rc = s->zero_row.ensure(1))) {
+        kz_system_destroy(s);
+        return rc;
+    }
+    if (cudaMallocHost(&s->h_status, sizeof(SolveStatus)) != cudaSuccess) {
+        cudaGetLastError();
+        kz_system_destroy(s);
+        return fail(KZ_ENOMEM, "pinned status allocation failed");
+    }
+    for (auto& e : s->ev) cudaEventCreate(&e);
+    cudaMemset(s->xref.p, 0, s->ld * sizeof(double));
+    cudaMemset(s->x.p, 0, s->ld * sizeof(double));
+    *out = s;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_system_destroy(kz_system* s) {
+    if (!s) return KZ_OK;
+    cudaSetDevice(s->device);
+    for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas})
+        b->release();
+    s->lo.release();
+    s->len.release();
+    s->idx.release();
+    s->rows_out.release();
+    s->states.release();
+    s->barrier.release();
+    s->status.release();
+    s->zero_row.release();
+    if (s->h_status) cudaFreeHost(s->h_status);
+    for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    delete s;
+    return KZ_OK;
+}
+
+extern "C" int64_t kz_system_pitch(const kz_system* s) { return s ? s->ld : 0; }
+
+static int upload_common(kz_system* s, const double* A, int64_t lda, const double* b, const double* xref,
+                         cudaStream_t st, cudaMemcpyKind kind) {
+    if (lda < s->n) return fail(KZ_EINVAL, "lda=%lld < n=%lld", (long long)lda, (long long)s->n);
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_CUDA(cudaMemcpy2DAsync(s->A.p, s->ld * sizeof(double), A, lda * sizeof(double), s->n * sizeof(double), s->m,
+                              kind, st));
+    if (s->ld > s->n)
+        KZ_CUDA(cudaMemset2DAsync(s->A.p + s->n, s->ld * sizeof(double), 0, (s->ld - s->n) * sizeof(double), s->m, st));
+    KZ_CUDA(cudaMemcpyAsync(s->b.p, b, s->m * sizeof(double), kind, st));
+    if (xref) {
+        KZ_CUDA(cudaMemcpyAsync(s->xref.p, xref, s->n * sizeof(double), kind, st));
+        s->has_xref = true;
+    } else {
+        s->has_xref = false;
+    }
+    s->norms_valid = false;
+    s->sampler_scheme = -1;
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_system_upload(kz_system* s, const double* A, int64_t lda, const double* b, const double* xref,
+                                    void* stream) {
+    if (!s || !A || !b) return fail(KZ_EINVAL, "null argument");
+    return upload_common(s, A, lda, b, xref, (cudaStream_t)stream, cudaMemcpyHostToDevice);
+}
+
+extern "C" int32_t kz_system_upload_device(kz_system* s, const double* A, int64_t lda, const double* b,
+                                           const double* xref, void* stream) {
+    if (!s || !A || !b) return fail(KZ_EINVAL, "null argument");
+    return upload_common(s, A, lda, b, xref, (cudaStream_t)stream, cudaMemcpyDeviceToDevice);
+}
+
+extern "C" int32_t kz_system_device_ptrs(kz_system* s, double** A, double** b, double** xref) {
+    if (!s) return fail(KZ_EINVAL, "null system");
+    if (A) *A = s->A.p;
+    if (b) *b = s->b.p;
+    if (xref) *xref = s->xref.p;
+    s->has_xref = true;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_system_set_xref(kz_system* s, const double* xref, void* stream) {
+    if (!s || !xref) return fail(KZ_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_CUDA(cudaMemcpyAsync(s->xref.p, xref, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    s->has_xref = true;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_system_touch(kz_system* s) {
+    if (!s) return fail(KZ_EINVAL, "null system");
+    s->norms_valid = false;
+    s->sampler_scheme = -1;
+    return KZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// row norms (linalg.py:80-88)
+// ---------------------------------------------------------------------------
+static int ensure_norms(kz_system* s, cudaStream_t st) {
+    if (s->norms_valid) return s->bad_row >= 0 ? fail(KZ_EDEGENERATE, "row %lld has zero norm; sampling probabilities "
+                                                                       "and projection denominators are undefined for "
+                                                                       "zero rows", (long long)s->bad_row)
+                                               : KZ_OK;
+    KZ_CUDA(cudaMemsetAsync(s->zero_row.p, 0xff, sizeof(unsigned long long), st));
+    const int64_t blocks = (s->m + NORM_ROWS_PER_CTA - 1) / NORM_ROWS_PER_CTA;
+    row_sqnorm_kernel<<<(unsigned)blocks, NORM_ROWS_PER_CTA, 0, st>>>(s->A.p, s->m, s->n, s->ld, s->sq.p, s->zero_row.p);
+    KZ_TRY(check_launch("row_sqnorm_kernel"));
+    unsigned long long first = 0;
+    KZ_CUDA(cudaMemcpyAsync(&first, s->zero_row.p, sizeof(first), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    s->norms_valid = true;
+    s->bad_row = (first == ~0ULL) ? -1 : (int64_t)first;
+    s->sampler_scheme = -1;
+    if (s->bad_row >= 0)
+        return fail(KZ_EDEGENERATE, "row %lld has zero norm; sampling probabilities and projection denominators "
+                    "are undefined for zero rows", (long long)s->bad_row);
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_row_norms(kz_system* s, double* sq_host, int64_t* bad_row, void* stream) {
+    if (!s) return fail(KZ_EINVAL, "null system");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    int rc = ensure_norms(s, st);
+    if (bad_row) *bad_row = s->bad_row;
+    if (sq_host && s->norms_valid) {
+        KZ_CUDA(cudaMemcpyAsync(sq_host, s->sq.p, s->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+    }
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+// samplers (sampling.py:189-219, solvers.py:162-171)
+// ---------------------------------------------------------------------------
+static int ensure_sampler(kz_system* s, int scheme, int64_t q, cudaStream_t st) {
+    KZ_TRY(ensure_norms(s, st));
+    if (scheme != KZ_FULL_ACCESS && scheme != KZ_DISTRIBUTED) return fail(KZ_EINVAL, "unknown sampling scheme %d", scheme);
+    if (q < 1) return fail(KZ_EINVAL, "q must be >= 1, got %lld", (long long)q);
+    if (s->sampler_scheme == scheme && (scheme == KZ_FULL_ACCESS || s->sampler_q == q)) {
+        if (scheme == KZ_FULL_ACCESS && s->sampler_q != q) {
+            // full access: one range replicated per worker
+            std::vector<int64_t> lo(q, 0), len(q, s->m);
+            KZ_TRY(s->lo.ensure(q));
+            KZ_TRY(s->len.ensure(q));
+            KZ_CUDA(cudaMemcpyAsync(s->lo.p, lo.data(), q * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            KZ_CUDA(cudaMemcpyAsync(s->len.p, len.data(), q * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            KZ_CUDA(cudaStreamSynchronize(st));
+            s->sampler_q = q;
+        }
+        return KZ_OK;
+    }
+    std::vector<int64_t> lo(q), len(q);
+    int64_t nranges;
+    if (scheme == KZ_FULL_ACCESS) {
+        std::fill(lo.begin(), lo.end(), 0);
+        std::fill(len.begin(), len.end(), s->m);
+        nranges = 1;
+    } else {
+        for (int64_t t = 0; t < q; ++t) {
+            const int64_t a = (t * s->m) / q, b = ((t + 1) * s->m) / q - 1;
+            if (b < a) return fail(KZ_EEMPTYRANGE, "block %lld of %lld is empty for m=%lld", (long long)t, (long long)q,
+                                   (long long)s->m);
+            lo[t] = a;
+            len[t] = b - a + 1;
+        }
+        nranges = q;
+    }
+    KZ_TRY(s->lo.ensure(q));
+    KZ_TRY(s->len.ensure(q));
+    KZ_CUDA(cudaMemcpyAsync(s->lo.p, lo.data(), q * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    KZ_CUDA(cudaMemcpyAsync(s->len.p, len.data(), q * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    cdf_scan_kernel<<<(unsigned)((nranges + 127) / 128), 128, 0, st>>>(s->sq.p, s->lo.p, s->len.p, nranges, s->cdf.p);
+    KZ_TRY(check_launch("cdf_scan_kernel"));
+    const int64_t maxlen = *std::max_element(len.begin(), len.end());
+    dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 1024), (unsigned)nranges);
+    cdf_div_kernel<<<grid, 256, 0, st>>>(s->cdf.p, s->lo.p, s->len.p);
+    KZ_TRY(check_launch("cdf_div_kernel"));
+    cdf_div_last_kernel<<<(unsigned)((nranges + 127) / 128), 128, 0, st>>>(s->cdf.p, s->lo.p, s->len.p, nranges);
+    KZ_TRY(check_launch("cdf_div_last_kernel"));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    s->sampler_scheme = scheme;
+    s->sampler_q = q;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_sampler_build(kz_system* s, int32_t scheme, int64_t q, double* cdf_host, void* stream) {
+    if (!s) return fail(KZ_EINVAL, "null system");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_TRY(ensure_sampler(s, scheme, q, st));
+    if (cdf_host) {
+        KZ_CUDA(cudaMemcpyAsync(cdf_host, s->cdf.p, s->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+    }
+    return KZ_OK;
+}
+
+static int launch_sampler(kz_system* s, const PcgPod* states_dev, const int64_t* lo, const int64_t* len, int64_t q,
+                          int64_t d0, int64_t count, int32_t* out, int64_t stride_w, int64_t stride_d, cudaStream_t st) {
+    const int64_t runs = (count + SAMPLE_RUN - 1) / SAMPLE_RUN;
+    const int64_t threads = runs * q;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((threads + 255) / 256, (int64_t)s->sms * 16));
+    sample_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(s->cdf.p, lo, len, states_dev, q, d0, count, out, stride_w,
+                                                         stride_d);
+    return check_launch("sample_rows_kernel");
+}
+
+extern "C" int32_t kz_dump_rows(kz_system* s, int32_t scheme, int64_t q, uint64_t seed, int64_t worker, int64_t start,
+                                int64_t count, int32_t* out_host, void* stream) {
+    if (!s || !out_host) return fail(KZ_EINVAL, "null argument");
+    if (worker < 0 || worker >= q) return fail(KZ_EINVAL, "worker %lld out of range for q=%lld", (long long)worker, (long long)q);
+    if (start < 0 || count < 0) return fail(KZ_EINVAL, "negative range");
+    if (count == 0) return KZ_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_TRY(ensure_sampler(s, scheme, q, st));
+    KZ_TRY(s->states.ensure(std::max<int64_t>(q, 1)));
+    PcgPod pod = seed_stream(seed, (uint64_t)worker);
+    KZ_CUDA(cudaMemcpyAsync(s->states.p, &pod, sizeof(pod), cudaMemcpyHostToDevice, st));
+    KZ_TRY(s->rows_out.ensure(count));
+    KZ_TRY(launch_sampler(s, s->states.p, s->lo.p + worker, s->len.p + worker, 1, start, count, s->rows_out.p, 0, 1, st));
+    KZ_CUDA(cudaMemcpyAsync(out_host, s->rows_out.p, count * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// norms for traces / reports
+// ---------------------------------------------------------------------------
+static int device_norms(kz_system* s, const double* xdev, double* residual, double* error, cudaStream_t st) {
+    double h[2] = {NAN, NAN};
+    if (residual) {
+        const int rows_per_cta = 8;
+        residual_rows_kernel<<<(unsigned)((s->m + rows_per_cta - 1) / rows_per_cta), rows_per_cta * 32, 0, st>>>(
+            s->A.p, s->b.p, xdev, s->m, s->n, s->ld, s->tmp.p);
+        KZ_TRY(check_launch("residual_rows_kernel"));
+        sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->m, s->part.p);
+        KZ_TRY(check_launch("sum_kernel"));
+        KZ_CUDA(cudaMemcpyAsync(&h[0], s->part.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        *residual = std::sqrt(h[0]);
+    }
+    if (error) {
+        diff_sq_kernel<<<(unsigned)((s->n + 255) / 256), 256, 0, st>>>(xdev, s->xref.p, s->n, s->tmp.p);
+        KZ_TRY(check_launch("diff_sq_kernel"));
+        sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->n, s->part.p);
+        KZ_TRY(check_launch("sum_kernel"));
+        KZ_CUDA(cudaMemcpyAsync(&h[1], s->part.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        *error = std::sqrt(h[1]);
+    }
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_norms(kz_system* s, const double* x_host, double* residual, double* error, void* stream) {
+    if (!s || !x_host) return fail(KZ_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_TRY(s->part.ensure(16));
+    KZ_TRY(s->V.ensure(s->ld));
+    KZ_CUDA(cudaMemsetAsync(s->V.p, 0, s->ld * sizeof(double), st));
+    KZ_CUDA(cudaMemcpyAsync(s->V.p, x_host, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
+    return device_norms(s, s->V.p, residual, error, st);
+}
+
+extern "C" int32_t kz_solution_device(kz_system* s, double** x_dev) {
+    if (!s || !x_dev) return fail(KZ_EINVAL, "null argument");
+    *x_dev = s->x.p;
+    return KZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// solve driver
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Plan {
+    int kernel = KZ_KERNEL_CHAIN;
+    int threads = 256;
+    int ctas = 1;
+    int stages = 2;
+    int ep = 1;         // chain: pairs per thread
+    int lpr = 8;        // sync: lanes per row
+    size_t smem = 0;
+};
+
+const int kChainEP[] = {1, 2, 4, 8, 16};
+int chain_max_threads(int ep) { return ep <= 4 ? 256 : (ep <= 8 ? 512 : 640); }
+
+int chain_smem(int64_t ld, int stages) {
+    return (int)(stages * ld * sizeof(double) + 2 * (stages + 1) * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
+                 2 * 64 * sizeof(double));
+}
+
+size_t sync_smem(int64_t q, int64_t cw, int stages) {
+    return (size_t)stages * q * cw * sizeof(double) + (size_t)stages * q * 2 * sizeof(double) + 2 * cw * sizeof(double) +
+           2 * (q + 1) * sizeof(double) + (q + 1) * sizeof(double) + q * sizeof(double) + 4 * q * sizeof(int32_t);
+}
+
+void* chain_fn(int ep) {
+    switch (ep) {
+        case 1: return (void*)chain_kernel<1>;
+        case 2: return (void*)chain_kernel<2>;
+        case 4: return (void*)chain_kernel<4>;
+        case 8: return (void*)chain_kernel<8>;
+        default: return (void*)chain_kernel<16>;
+    }
+}
+
+void* sync_fn(bool cluster, int lpr) {
+    if (cluster) return lpr == 8 ? (void*)sync_kernel<true, 8> : (void*)sync_kernel<true, 32>;
+    return lpr == 8 ? (void*)sync_kernel<false, 8> : (void*)sync_kernel<false, 32>;
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+}  // namespace
+
+static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
+    const int64_t pairs = s->ld / 2;
+    auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
+    int ep = 0, T = 0;
+    if (p->threads > 0) {
+        T = round32(p->threads);
+        for (int e : kChainEP)
+            if ((int64_t)e * T >= pairs) {
+                ep = e;
+                break;
+            }
+    } else {
+        for (int e : kChainEP) {
+            ep = e;
+            T = round32((pairs + e - 1) / e);
+            if (T <= 256) break;
+        }
+    }
+    if (ep == 0 || T > chain_max_threads(ep) || (int64_t)ep * T < pairs)
+        return fail(KZ_EINVAL, "n=%lld too large for the chain kernel", (long long)s->n);
+    const int64_t stage_bytes = s->ld * (int64_t)sizeof(double);
+    const int64_t fixed = chain_smem(s->ld, 0);
+    int stages = (int)std::min<int64_t>(8, std::max<int64_t>(1, ((int64_t)200 * 1024 - fixed) / stage_bytes));
+    if ((size_t)chain_smem(s->ld, stages) > kSmemLimit)
+        return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
+    pl.kernel = KZ_KERNEL_CHAIN;
+    pl.threads = T;
+    pl.ep = ep;
+    pl.stages = stages;
+    pl.smem = chain_smem(s->ld, stages);
+    pl.ctas = (int)q;
+    void* fn = chain_fn(ep);
+    KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    if (q > 1) {
+        int per_sm = 0;
+        KZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, T, pl.smem));
+        if ((int64_t)per_sm * s->sms < q)
+            return fail(KZ_EINVAL, "q=%lld workers exceed the %d co-resident CTAs of the chain kernel", (long long)q,
+                        per_sm * s->sms);
+    }
+    return KZ_OK;
+}
+
+static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, Plan& pl) {
+    pl.threads = 256;
+    int P;
+    if (cluster) {
+        P = p->ctas > 0 ? p->ctas : 16;
+        if (P > 16) P = 16;
+    } else {
+        P = p->ctas > 0 ? p->ctas : s->sms;
+    }
+    // shrink P (cluster) / grow P (grid) until the slice ring fits and the launch is schedulable
+    for (;;) {
+        if (P < 1) return fail(KZ_EINVAL, "no feasible sync-kernel configuration for q=%lld n=%lld", (long long)q,
+                               (long long)s->n);
+        const int64_t cw = (((s->ld + P - 1) / P) + 1) & ~(int64_t)1;
+        int stages = 4;
+        while (stages > 2 && sync_smem(q, cw, stages) > 200 * 1024) --stages;
+        if (sync_smem(q, cw, stages) > kSmemLimit) {
+            if (cluster) return fail(KZ_EINVAL, "q=%lld row slices do not fit a cluster CTA", (long long)q);
+            if (P >= 4 * s->sms) return fail(KZ_EINVAL, "q=%lld too large for the sync kernel", (long long)q);
+            P *= 2;  // thinner slices, several CTAs per SM
+            continue;
+        }
+        pl.stages = stages;
+        pl.smem = sync_smem(q, cw, stages);
+        pl.lpr = cw <= 64 ? 8 : 32;
+        void* fn = sync_fn(cluster, pl.lpr);
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        if (cluster) {
+            KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(P);
+            cfg.blockDim = dim3(pl.threads);
+            cfg.dynamicSmemBytes = pl.smem;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = P;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+            if (e != cudaSuccess || nclusters < 1) {
+                cudaGetLastError();
+                if (P == 1) return fail(KZ_EINVAL, "cluster kernel not schedulable");
+                P /= 2;
+                continue;
+            }
+        } else {
+            int per_sm = 0;
+            KZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, pl.threads, pl.smem));
+            if ((int64_t)per_sm * s->sms < P) {
+                if (p->ctas > 0)
+                    return fail(KZ_EINVAL, "%d CTAs exceed co-residency (%d per SM)", P, per_sm);
+                P = per_sm * s->sms;
+                continue;
+            }
+        }
+        pl.kernel = cluster ? KZ_KERNEL_SYNC_CLUSTER : KZ_KERNEL_SYNC_GRID;
+        pl.ctas = P;
+        return KZ_OK;
+    }
+}
+
+static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(pl.ctas);
+    cfg.blockDim = dim3(pl.threads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    void* fn;
+    if (pl.kernel == KZ_KERNEL_CHAIN) {
+        fn = chain_fn(pl.ep);
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.numAttrs = pl.ctas > 1 ? 1 : 0;
+    } else if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER) {
+        fn = sync_fn(true, pl.lpr);
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = pl.ctas;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.numAttrs = 1;
+    } else {
+        fn = sync_fn(false, pl.lpr);
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.numAttrs = 1;
+    }
+    void* kargs[] = {&args};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, fn, kargs);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(KZ_ECUDA, "solve kernel launch failed: %s", cudaGetErrorString(e));
+    }
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, double* x_host, void* stream) {
+    if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
+    memset(r, 0, sizeof(*r));
+    r->final_error_sq = NAN;
+    r->final_residual = NAN;
+    cudaStream_t st = (cudaStream_t)stream;
+    // --- validation (SolverConfig.validate, solvers.py:85-101; _drive 200-214) ---
+    if (p->variant < KZ_RK || p->variant > KZ_RKAB) return fail(KZ_EINVAL, "unknown variant %d", p->variant);
+    if (p->q < 1) return fail(KZ_EINVAL, "q must be >= 1, got %lld", (long long)p->q);
+    if (p->block_size < 1) return fail(KZ_EINVAL, "block_size must be >= 1, got %lld", (long long)p->block_size);
+    if (!(p->epsilon > 0)) return fail(KZ_EINVAL, "epsilon must be > 0, got %g", p->epsilon);
+    if (p->max_iterations < 1) return fail(KZ_EINVAL, "max_iterations must be >= 1, got %lld", (long long)p->max_iterations);
+    if (p->budget < 0) return fail(KZ_EINVAL, "fixed iteration budget must be >= 1, got %lld", (long long)p->budget);
+    if (p->trace_step < 0) return fail(KZ_EINVAL, "trace_step must be >= 1, got %lld", (long long)p->trace_step);
+    const bool budget_mode = p->budget > 0;
+    const bool trace_mode = !budget_mode && p->trace_step > 0;
+    const bool stop_mode = !budget_mode && !trace_mode;
+    if ((stop_mode || trace_mode) && !s->has_xref) return fail(KZ_EINVAL, "system carries no reference solution");
+    if (trace_mode && !p->trace_host) return fail(KZ_EINVAL, "trace mode needs a trace buffer");
+    const int64_t q = p->variant == KZ_RK ? 1 : p->q;
+    const int64_t bs = p->variant == KZ_RKAB ? p->block_size : 1;
+    KZ_CUDA(cudaSetDevice(s->device));
+
+    // --- setup: row norms, sampler, streams, weights ---
+    KZ_TRY(ensure_sampler(s, p->scheme, q, st));
+    std::vector<PcgPod> pods(q);
+    for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)t);
+    KZ_TRY(s->states.ensure(q));
+    KZ_CUDA(cudaMemcpyAsync(s->states.p, pods.data(), q * sizeof(PcgPod), cudaMemcpyHostToDevice, st));
+    std::vector<double> al(q, 1.0);
+    if (p->alphas_host) std::copy(p->alphas_host, p->alphas_host + q, al.begin());
+    KZ_TRY(s->alphas.ensure(q));
+    KZ_CUDA(cudaMemcpyAsync(s->alphas.p, al.data(), q * sizeof(double), cudaMemcpyHostToDevice, st));
+    KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
+
+    // --- kernel plan ---
+    Plan pl;
+    int kern = p->kernel;
+    if (kern == KZ_KERNEL_AUTO) {
+        if (q == 1 || bs > 1) {
+            kern = KZ_KERNEL_CHAIN;
+        } else {
+            const double bytes_per_iter = (double)q * s->ld * sizeof(double);
+            kern = bytes_per_iter <= 4.0 * 1024 * 1024 ? KZ_KERNEL_SYNC_CLUSTER : KZ_KERNEL_SYNC_GRID;
+        }
+    }
+    if (kern == KZ_KERNEL_CHAIN) {
+        KZ_TRY(plan_chain(s, p, q, pl));
+    } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {
+        if (bs != 1) return fail(KZ_EINVAL, "the sync kernels run RKA / RKAB with block_size 1 only");
+        int rc = plan_sync(s, p, q, kern == KZ_KERNEL_SYNC_CLUSTER, pl);
+        if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && p->kernel == KZ_KERNEL_AUTO)
+            rc = plan_sync(s, p, q, false, pl);
+        KZ_TRY(rc);
+    } else {
+        return fail(KZ_EINVAL, "unknown kernel selector %d", kern);
+    }
+    r->kernel_used = pl.kernel;
+    r->ctas = pl.ctas;
+    r->threads = pl.threads;
+
+    // --- scratch ---
+    const int64_t draws_per_iter = q * bs;
+    const int64_t idx_cap = std::max<int64_t>(draws_per_iter, (int64_t)8 << 20);
+    const int64_t chunk_cap = std::max<int64_t>(1, idx_cap / draws_per_iter);
+    KZ_TRY(s->idx.ensure(std::min<int64_t>(idx_cap, chunk_cap * draws_per_iter)));
+    if (pl.kernel == KZ_KERNEL_CHAIN && q > 1) KZ_TRY(s->V.ensure((size_t)q * s->ld));
+    KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
+    const int64_t n_ck_cap = p->ckpt_every > 0 ? std::max<int64_t>(0, p->ckpt_capacity) : 0;
+    if (n_ck_cap > 0) KZ_TRY(s->ckpt.ensure((size_t)n_ck_cap * s->n));
+
+    SolveArgs args = {};
+    args.A = s->A.p;
+    args.b = s->b.p;
+    args.sq = s->sq.p;
+    args.xref = s->xref.p;
+    args.x = s->x.p;
+    args.V = s->V.p;
+    args.idx = s->idx.p;
+    args.alphas = s->alphas.p;
+    args.part = s->part.p;
+    args.barrier = s->barrier.p;
+    args.status = s->status.p;
+    args.ckpt = s->ckpt.p;
+    args.n = s->n;
+    args.ld = s->ld;
+    args.q = q;
+    args.bs = bs;
+    args.ckpt_every = n_ck_cap > 0 ? p->ckpt_every : 0;
+    args.ckpt_cap = n_ck_cap;
+    args.eps = p->epsilon;
+    args.use_stop = stop_mode ? 1 : 0;
+    args.stages = pl.stages;
+
+    const int64_t limit = budget_mode ? p->budget : p->max_iterations;
+    int64_t k = 0, evals = 0;
+    bool converged = false;
+    double err = NAN;
+    int64_t n_trace = 0;
+    const long long launches0 = g_launches.load();
+    float kernel_ms = 0.f;
+
+    auto record_trace = [&]() -> int {
+        double res = 0, e = 0;
+        KZ_TRY(device_norms(s, s->x.p, &res, &e, st));
+        p->trace_host[3 * n_trace + 0] = (double)k;
+        p->trace_host[3 * n_trace + 1] = e;
+        p->trace_host[3 * n_trace + 2] = res;
+        ++n_trace;
+        return KZ_OK;
+    };
+
+    KZ_CUDA(cudaEventRecord(s->ev[0], st));
+    if (trace_mode) KZ_TRY(record_trace());
+    int64_t chunk = stop_mode ? std::min<int64_t>(chunk_cap, std::max<int64_t>(64, 4096 / bs)) : chunk_cap;
+    for (;;) {
+        const int64_t remaining = limit - k;
+        if (remaining <= 0 && !stop_mode) break;
+        int64_t c = std::min<int64_t>(chunk, remaining);
+        if (trace_mode) c = std::min<int64_t>(c, p->trace_step - (k % p->trace_step));
+        if (c > 0) {
+            const int64_t count = c * bs;
+            if (pl.kernel == KZ_KERNEL_CHAIN)
+                KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, k * bs, count, s->idx.p, count, 1, st));
+            else
+                KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, k * bs, count, s->idx.p, 1, q, st));
+        }
+        args.k0 = k;
+        args.count = c;
+        args.idx_stride = c * bs;
+        args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
+        KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
+        KZ_CUDA(cudaEventRecord(s->ev[2], st));
+        KZ_TRY(launch_solve(s, pl, args, st));
+        KZ_CUDA(cudaEventRecord(s->ev[3], st));
+        KZ_CUDA(cudaMemcpyAsync(s->h_status, s->status.p, sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, s->ev[2], s->ev[3]);
+        kernel_ms += ms;
+        const SolveStatus hs = *s->h_status;
+        k += hs.iters_done;
+        evals += hs.checks;
+        if (hs.checks > 0) err = hs.err;
+        if (hs.converged) {
+            converged = true;
+            break;
+        }
+        if (hs.iters_done != c) return fail(KZ_ECUDA, "solve kernel stopped early (%lld of %lld iterations)",
+                                            (long long)hs.iters_done, (long long)c);
+        if (trace_mode && k % p->trace_step == 0) KZ_TRY(record_trace());
+        if (stop_mode && k >= p->max_iterations) break;
+        if (stop_mode) chunk = std::min<int64_t>(chunk_cap, chunk * 2);
+    }
+    KZ_CUDA(cudaEventRecord(s->ev[1], st));
+    KZ_CUDA(cudaEventSynchronize(s->ev[1]));
+    float loop_ms = 0.f;
+    cudaEventElapsedTime(&loop_ms, s->ev[0], s->ev[1]);
+
+    r->iterations = k;
+    r->converged = converged ? 1 : 0;
+    r->error_evals = evals;
+    r->final_error_sq = stop_mode ? err : NAN;
+    r->rows_projected = k * q * bs;
+    r->loop_ms = loop_ms;
+    r->kernel_ms = kernel_ms;
+    r->n_trace = n_trace;
+    if (n_ck_cap > 0) {
+        r->n_ckpt = std::min<int64_t>(n_ck_cap, k / p->ckpt_every);
+        if (r->n_ckpt > 0 && p->ckpt_host)
+            KZ_CUDA(cudaMemcpyAsync(p->ckpt_host, s->ckpt.p, (size_t)r->n_ckpt * s->n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    if (stop_mode && p->want_residual) {
+        double res = NAN;
+        KZ_TRY(device_norms(s, s->x.p, &res, nullptr, st));
+        r->final_residual = res;
+    }
+    if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    r->kernel_launches = g_launches.load() - launches0;
+    return KZ_OK;
+}

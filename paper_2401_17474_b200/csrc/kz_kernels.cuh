@@ -1,0 +1,71 @@
+// kz_kernels.cuh -- kernel argument blocks and launch declarations.
+#pragma once
+
+#include "kz_common.cuh"
+
+namespace kz {
+
+// Per-launch status written by the solve kernels (device memory).
+struct SolveStatus {
+    long long iters_done;  // advances applied in this launch
+    int converged;         // stop rule met (||x - x_ref||^2 < eps)
+    int checks;            // stop-rule evaluations in this launch
+    double err;            // last evaluated ||x - x_ref||^2
+};
+
+// Shared by both solve kernels.
+struct SolveArgs {
+    const double* A;       // m x ld, row-major, pitched
+    const double* b;       // m
+    const double* sq;      // m squared row norms (einsum order)
+    const double* xref;    // ld (zero padded)
+    double* x;             // ld, the iterate (in/out)
+    double* V;             // q x ld worker estimates (chain kernel, q > 1)
+    const int32_t* idx;    // row indices of this chunk (layout per kernel)
+    const double* alphas;  // q row weights
+    double* part;          // cross-CTA partial sums (sync kernel, grid mode)
+    unsigned* barrier;     // grid barrier counter (zeroed per launch)
+    SolveStatus* status;
+    double* ckpt;          // checkpoints (ckpt_cap x n, row stride n)
+    int64_t n, ld, q, bs;
+    int64_t k0, count;     // iterations [k0, k0 + count) in this launch
+    int64_t idx_stride;    // chain: draws per worker in the chunk; sync: q
+    int64_t ckpt_every, ckpt_cap;
+    double eps;
+    int use_stop;          // evaluate the stop rule before each iteration
+    int final_check;       // also evaluate it at k0 + count (max_iterations reached)
+    int stages;            // cp.async ring depth
+};
+
+// chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread.
+template <int EP>
+__global__ void chain_kernel(SolveArgs a);
+
+// sync kernel: column-sliced (RKA, RKAB bs=1).  CLUSTER: reduce via DSMEM.
+template <bool CLUSTER, int LPR>
+__global__ void sync_kernel(SolveArgs a);
+
+__global__ void row_sqnorm_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
+                                  double* __restrict__ sq, unsigned long long* __restrict__ first_zero);
+__global__ void cdf_scan_kernel(const double* __restrict__ sq, const int64_t* __restrict__ lo,
+                                const int64_t* __restrict__ len, int64_t nranges, double* __restrict__ cdf);
+__global__ void cdf_div_kernel(double* __restrict__ cdf, const int64_t* __restrict__ lo,
+                               const int64_t* __restrict__ len);
+__global__ void cdf_div_last_kernel(double* __restrict__ cdf, const int64_t* __restrict__ lo,
+                                    const int64_t* __restrict__ len, int64_t nranges);
+__global__ void sample_rows_kernel(const double* __restrict__ cdf, const int64_t* __restrict__ lo,
+                                   const int64_t* __restrict__ len, const PcgPod* __restrict__ base_states,
+                                   int64_t q, int64_t d0, int64_t count, int32_t* __restrict__ out,
+                                   int64_t stride_w, int64_t stride_d);
+__global__ void residual_rows_kernel(const double* __restrict__ A, const double* __restrict__ b,
+                                     const double* __restrict__ x, int64_t m, int64_t n, int64_t ld,
+                                     double* __restrict__ out);
+__global__ void diff_sq_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                               double* __restrict__ out);
+__global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
+
+constexpr int NORM_ROWS_PER_CTA = 128;
+constexpr int SAMPLE_RUN = 8;
+constexpr int IDX_WINDOW = 1024;  // chain kernel: smem ring of row indices
+
+}  // namespace kz

@@ -1,0 +1,367 @@
+"""RK / RKA / RKAB on the B200 behind the reference's entry points.
+
+Same names, signatures, argument meaning and error behaviour as
+kaczbench/solvers.py:55-371 and kaczbench/harness.py:98-114:
+
+    fn(system, cfg, *, x_ref=None, budget=None, trace_step=None, capture=None) -> RunReport
+
+``system`` is a :class:`~.sysgen.LinearSystem` (host arrays, uploaded per
+call, like the reference recomputes its row norms per call) or a
+:class:`DeviceSystem` (resident in HBM; norms and samplers cached).  The whole
+iteration loop -- sampling, projections, averaging, the stop rule -- runs in
+``libkz_b200.so``; there is no host fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import DimensionMismatchError
+from .reports import RunReport, TraceRecord
+from .sysgen import LinearSystem, cgls_solve
+
+VARIANTS = ("ck", "rk", "rka", "rkab", "cgls")
+ALPHA_POLICIES = ("unit", "fixed", "optimal_full", "optimal_partial")
+SAMPLING_SCHEMES = ("full_access", "distributed")
+# "seq" and "threads" name the reference engines whose semantics are honoured
+# (threads: RKAB gets the leading row, solvers.py:346-350); all run on the B200.
+ENGINES = ("b200", "seq", "threads")
+KERNELS = tuple(N.KERNELS)
+
+# capture=list keeps every iterate (reference semantics); refuse absurd sizes
+_CAPTURE_LIMIT_BYTES = 4 << 30
+
+
+@dataclass
+class SolverConfig:
+    """Mirror of kaczbench.SolverConfig (solvers.py:61-104) plus device knobs."""
+
+    variant: str = "rk"
+    q: int = 1
+    alpha_policy: str = "unit"
+    alpha: float = 1.0
+    block_size: int = 1
+    epsilon: float = 1e-8
+    max_iterations: int = 1_000_000
+    base_seed: int = 0
+    sampling_scheme: str = "full_access"
+    engine: str = "b200"
+    kernel: str = "auto"
+    device: int = 0
+
+    def validate(self) -> None:
+        if self.variant not in VARIANTS:
+            raise ValueError(f"unknown variant {self.variant!r}")
+        if self.alpha_policy not in ALPHA_POLICIES:
+            raise ValueError(f"unknown alpha policy {self.alpha_policy!r}")
+        if self.sampling_scheme not in SAMPLING_SCHEMES:
+            raise ValueError(f"unknown sampling scheme {self.sampling_scheme!r}")
+        if self.engine not in ENGINES:
+            raise ValueError(f"unknown engine {self.engine!r}")
+        if self.kernel not in KERNELS:
+            raise ValueError(f"unknown kernel {self.kernel!r}")
+        if self.q < 1:
+            raise ValueError(f"q must be >= 1, got {self.q}")
+        if self.block_size < 1:
+            raise ValueError(f"block_size must be >= 1, got {self.block_size}")
+        if not self.epsilon > 0:
+            raise ValueError(f"epsilon must be > 0, got {self.epsilon}")
+        if self.max_iterations < 1:
+            raise ValueError(f"max_iterations must be >= 1, got {self.max_iterations}")
+
+    def replace(self, **kw) -> "SolverConfig":
+        return dataclasses.replace(self, **kw)
+
+
+class DeviceSystem:
+    """A linear system resident in one GPU's HBM (C-ABI kz_system).
+
+    A is stored row-major with a 128-byte row pitch.  Row norms and samplers
+    are computed on first use and cached; inputs are never modified.
+    """
+
+    def __init__(self, system: LinearSystem | None = None, *, m: int | None = None, n: int | None = None,
+                 device: int = 0):
+        self._lib = N.load_library()
+        if system is not None:
+            m, n = system.A.shape if system.A.ndim == 2 else (None, None)
+        if m is None or n is None:
+            raise DimensionMismatchError("DeviceSystem needs a 2-D system or (m, n)")
+        self.m, self.n, self.device = int(m), int(n), int(device)
+        self.host = system
+        h = C.c_void_p()
+        N.check(self._lib.kz_system_create(self.device, self.m, self.n, C.byref(h)))
+        self.handle = h
+        self._xref_set = False
+        if system is not None:
+            xr = system.x_star if system.x_star is not None else system.x_ls
+            self.upload(system.A, system.b, xr)
+
+    # -- residency -------------------------------------------------------------
+    def upload(self, A, b, x_ref=None, stream=None) -> None:
+        A = N.f64(A)
+        b = N.f64(b)
+        if A.ndim != 2:
+            raise DimensionMismatchError(f"expected a 2-D matrix, got ndim={A.ndim}")
+        if A.shape != (self.m, self.n):
+            raise DimensionMismatchError(f"matrix {A.shape} does not match ({self.m}, {self.n})")
+        if b.shape != (self.m,):
+            raise DimensionMismatchError(f"expected length {self.m}, got {b.shape}")
+        xr = None
+        if x_ref is not None:
+            xr = N.f64(x_ref)
+            if xr.shape != (self.n,):
+                raise DimensionMismatchError(f"expected length {self.n}, got {xr.shape}")
+        N.check(self._lib.kz_system_upload(self.handle, N.ptr(A), self.n, N.ptr(b),
+                                           N.ptr(xr) if xr is not None else None, stream))
+        self._xref_set = xr is not None
+
+    def upload_device(self, A_ptr: int, lda: int, b_ptr: int, xref_ptr: int | None = None, stream=None) -> None:
+        """Copy from caller-owned device arrays (e.g. torch tensors' data_ptr())."""
+        N.check(self._lib.kz_system_upload_device(self.handle, C.c_void_p(A_ptr), lda, C.c_void_p(b_ptr),
+                                                  C.c_void_p(xref_ptr) if xref_ptr else None, stream))
+        self._xref_set = bool(xref_ptr)
+
+    def device_ptrs(self) -> tuple[int, int, int, int]:
+        """(A, b, x_ref, pitch) device pointers, for in-place generation."""
+        a, b, x = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        N.check(self._lib.kz_system_device_ptrs(self.handle, C.byref(a), C.byref(b), C.byref(x)))
+        self._xref_set = True
+        return a.value, b.value, x.value, self.pitch
+
+    def touch(self) -> None:
+        N.check(self._lib.kz_system_touch(self.handle))
+
+    def set_x_ref(self, x_ref) -> None:
+        xr = N.f64(x_ref)
+        if xr.shape != (self.n,):
+            raise DimensionMismatchError(f"expected length {self.n}, got {xr.shape}")
+        N.check(self._lib.kz_system_set_xref(self.handle, N.ptr(xr), None))
+        self._xref_set = True
+
+    @property
+    def pitch(self) -> int:
+        return int(self._lib.kz_system_pitch(self.handle))
+
+    # -- sampler subsystem -----------------------------------------------------
+    def row_norms(self) -> np.ndarray:
+        """Squared row norms, bit-exact with np.einsum (linalg.py:80-88)."""
+        out = np.empty(self.m)
+        bad = C.c_int64(-1)
+        rc = self._lib.kz_row_norms(self.handle, N.ptr(out), C.byref(bad), None)
+        N.check(rc, bad_row=bad.value)
+        return out
+
+    def cdf(self, scheme: str = "full_access", q: int = 1) -> np.ndarray:
+        """make_sampler cdf(s) (sampling.py:189-199), concatenated per block."""
+        out = np.empty(self.m)
+        N.check(self._lib.kz_sampler_build(self.handle, N.SCHEME_IDS[scheme], int(q), N.ptr(out), None))
+        return out
+
+    def dump_rows(self, base_seed: int, worker: int, count: int, *, scheme: str = "full_access", q: int = 1,
+                  start: int = 0) -> np.ndarray:
+        """Draws start..start+count-1 of worker `worker` (RowSampler.sample)."""
+        out = np.empty(count, dtype=np.int32)
+        N.check(self._lib.kz_dump_rows(self.handle, N.SCHEME_IDS[scheme], int(q), int(base_seed), int(worker),
+                                       int(start), int(count), out.ctypes.data_as(C.POINTER(C.c_int32)), None))
+        return out
+
+    def norms(self, x) -> tuple[float, float]:
+        """(||A x - b||, ||x - x_ref||) on the device."""
+        xv = N.f64(x)
+        res, err = C.c_double(), C.c_double()
+        N.check(self._lib.kz_norms(self.handle, N.ptr(xv), C.byref(res), C.byref(err), None))
+        return res.value, err.value
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self._lib.kz_system_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def resolve_alphas(system, cfg: SolverConfig, q: int | None = None) -> np.ndarray:
+    """Per-worker weights (solvers.py:148-159)."""
+    q = cfg.q if q is None else q
+    if cfg.alpha_policy == "unit":
+        return np.ones(q)
+    if cfg.alpha_policy == "fixed":
+        return np.full(q, float(cfg.alpha))
+    from .spectral import optimal_alpha, partial_alphas, spectral_stats  # host setup, off the hot path
+    A = _host_matrix(system)
+    if cfg.alpha_policy == "optimal_full":
+        return np.full(q, optimal_alpha(spectral_stats(A), q))
+    return partial_alphas(A, q)
+
+
+def _host_matrix(system):
+    host = system.host if isinstance(system, DeviceSystem) else system
+    if host is None:
+        raise ValueError("spectral weights need the host copy of A")
+    return host.A
+
+
+def _uniform_alpha(alphas: np.ndarray) -> float:
+    return float(alphas[0]) if np.all(alphas == alphas[0]) else float("nan")
+
+
+def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, trace_step=None, capture=None,
+           lead_row: bool = False, checkpoint_every: int | None = None) -> RunReport:
+    cfg.validate()
+    q = 1 if variant == "rk" else cfg.q
+    steps = cfg.block_size + (1 if lead_row else 0) if variant == "rkab" else 1
+    alphas = N.f64(resolve_alphas(system, cfg, q))
+    if budget is not None and budget < 1:
+        raise ValueError(f"fixed iteration budget must be >= 1, got {budget}")
+    if budget is None and trace_step is not None and trace_step < 1:
+        raise ValueError(f"trace_step must be >= 1, got {trace_step}")
+
+    own = not isinstance(system, DeviceSystem)
+    ds = DeviceSystem(system, device=cfg.device) if own else system
+    try:
+        if x_ref is not None:
+            ds.set_x_ref(x_ref)
+        elif budget is None and not ds._xref_set:
+            host = ds.host if not own else system
+            if host is None:
+                raise ValueError("system carries no reference solution")
+            ds.set_x_ref(host.x_ref())
+        p = N.Params()
+        p.variant = N.VARIANT_IDS[variant]
+        p.scheme = N.SCHEME_IDS[cfg.sampling_scheme]
+        p.q = q
+        p.block_size = steps
+        p.alphas_host = N.ptr(alphas)
+        p.base_seed = int(cfg.base_seed)
+        p.epsilon = float(cfg.epsilon)
+        p.max_iterations = int(cfg.max_iterations)
+        p.budget = int(budget) if budget is not None else 0
+        limit = budget if budget is not None else cfg.max_iterations
+        trace_buf = None
+        if budget is None and trace_step is not None:
+            p.trace_step = int(trace_step)
+            trace_buf = np.empty((cfg.max_iterations // trace_step + 2, 3))
+            p.trace_host = N.ptr(trace_buf)
+        every = checkpoint_every if checkpoint_every else (1 if capture is not None else 0)
+        ck_buf = None
+        if every:
+            cap = limit // every
+            if cap * ds.n * 8 > _CAPTURE_LIMIT_BYTES:
+                raise ValueError(f"capture of {cap} iterates of length {ds.n} exceeds "
+                                 f"{_CAPTURE_LIMIT_BYTES >> 30} GiB; pass checkpoint_every")
+            ck_buf = np.empty((max(cap, 1), ds.n))
+            p.ckpt_every, p.ckpt_capacity, p.ckpt_host = every, cap, N.ptr(ck_buf)
+        p.kernel = N.KERNELS[cfg.kernel]
+        p.want_residual = 1
+        r = N.Result()
+        x = np.empty(ds.n)
+        N.check(N.load_library().kz_solve(ds.handle, C.byref(p), C.byref(r), N.ptr(x), None))
+    finally:
+        if own:
+            ds.close()
+
+    if capture is not None and ck_buf is not None:
+        capture.extend(ck_buf[i].copy() for i in range(r.n_ckpt))
+    trace = None
+    if trace_buf is not None:
+        trace = [TraceRecord(int(t[0]), float(t[1]), float(t[2])) for t in trace_buf[: r.n_trace]]
+    stop_mode = budget is None and trace_step is None
+    return RunReport(
+        variant=variant,
+        q=q,
+        block_size=cfg.block_size if variant == "rkab" else 1,
+        alpha_policy=cfg.alpha_policy,
+        alpha=_uniform_alpha(alphas),
+        seed=cfg.base_seed,
+        iterations=int(r.iterations),
+        converged=bool(r.converged),
+        wall_time_s=float(r.loop_ms) / 1e3,
+        final_error_sq=float(r.final_error_sq) if stop_mode else float("nan"),
+        final_residual=float(r.final_residual) if stop_mode else float("nan"),
+        error_evals=int(r.error_evals),
+        x=x,
+        trace=trace,
+        gpu={
+            "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"),
+            "loop_ms": float(r.loop_ms),
+            "kernel_ms": float(r.kernel_ms),
+            "rows_projected": int(r.rows_projected),
+            "launches": int(r.kernel_launches),
+            "ctas": int(r.ctas),
+            "threads": int(r.threads),
+            "checkpoint_every": every,
+        },
+    )
+
+
+def solve_rk(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
+             checkpoint_every=None) -> RunReport:
+    """Randomized Kaczmarz, worker stream 0 (solvers.py:294-310)."""
+    return _solve(system, cfg, "rk", x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture,
+                  checkpoint_every=checkpoint_every)
+
+
+def solve_rka_seq(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
+                  checkpoint_every=None) -> RunReport:
+    """Averaged RK: q rows from one snapshot, ordered mean (solvers.py:313-334)."""
+    return _solve(system, cfg, "rka", x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture,
+                  checkpoint_every=checkpoint_every)
+
+
+def solve_rkab_seq(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
+                   lead_row: bool = False, checkpoint_every=None) -> RunReport:
+    """Block-averaged RK: q private chains of block_size rows (solvers.py:337-371)."""
+    return _solve(system, cfg, "rkab", x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture,
+                  lead_row=lead_row, checkpoint_every=checkpoint_every)
+
+
+def _run_cgls(system, cfg, x_ref):
+    """harness._run_cgls (harness.py:343-366): host CGLS, off the hot path."""
+    host = system.host if isinstance(system, DeviceSystem) else system
+    import time
+
+    t0 = time.perf_counter()
+    x = cgls_solve(host.A, host.b, tol=1e-10)
+    wall = time.perf_counter() - t0
+    if x_ref is None and (host.x_star is not None or host.x_ls is not None):
+        x_ref = host.x_ref()
+    err = float(np.dot(x - x_ref, x - x_ref)) if x_ref is not None else float("nan")
+    return RunReport(variant="cgls", q=1, block_size=1, alpha_policy=cfg.alpha_policy, alpha=float("nan"),
+                     seed=cfg.base_seed, iterations=-1, converged=True, wall_time_s=wall, final_error_sq=err,
+                     final_residual=float(np.linalg.norm(host.A @ x - host.b)), x=x)
+
+
+def run_solver(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
+               checkpoint_every=None) -> RunReport:
+    """Dispatch on cfg.variant / cfg.engine (harness.py:369-385)."""
+    cfg.validate()
+    if cfg.variant == "cgls":
+        if budget is not None or trace_step is not None:
+            raise ValueError("cgls supports neither fixed-budget replay nor tracing")
+        return _run_cgls(system, cfg, x_ref)
+    if cfg.variant == "ck":
+        raise NotImplementedError("cyclic Kaczmarz (solvers.py:271-291) is outside the B200 hot path")
+    if cfg.engine == "threads" and trace_step is not None:
+        raise ValueError("tracing is supported by the sequential engine only")
+    kw = dict(x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture, checkpoint_every=checkpoint_every)
+    if cfg.variant == "rk":
+        return solve_rk(system, cfg, **kw)
+    if cfg.variant == "rka":
+        return solve_rka_seq(system, cfg, **kw)
+    return solve_rkab_seq(system, cfg, lead_row=(cfg.engine == "threads"), **kw)

@@ -1,0 +1,174 @@
+"""Generate the golden fixtures under tests/golden/ by EXECUTING the reference.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture records numpy's version; the reference's arithmetic lives in
+numpy 2.3.5 / OpenBLAS 0.3.30 (third-party, pkg/pyproject.toml:10).  The
+fixtures pin:
+
+* prng.npz     -- Prng(seed, stream).random() streams and SeedSequence words
+                  (sampling.py:122-162)
+* norms.npz    -- row_norm_cache(A).sq_norms for seeded matrices of many widths
+                  (linalg.py:80-88)
+* systems.npz  -- sha256 of generate_mother / crop / make_inconsistent outputs
+                  (sysgen.py:118-187), so the package's generator restatement
+                  can be checked bitwise without the reference
+* rows.npz     -- RowSampler.sample streams per worker (solvers.py:162-171,
+                  sampling.py:177-199) for RK / RKA / RKAB configurations
+* solves.npz   -- full reference solves: iteration counts, error_evals,
+                  final_error_sq, final x and x checkpoints (capture lists)
+                  for the BASELINE configs c0, c1, c2 and desk-scale cases
+* traces.npz   -- trace_run records on an inconsistent system (harness.py:180-196)
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import kaczbench as kb  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from common import NORM_WIDTHS, norm_matrix, sha  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+META = {"numpy_version": np.__version__, "generator": "tests/golden/make_golden.py"}
+
+
+def save(name, **arrays):
+    arrays.update({f"meta_{k}": np.array(v) for k, v in META.items()})
+    np.savez_compressed(os.path.join(OUT, name), **arrays)
+    print("wrote", name, flush=True)
+
+
+PRNG_TUPLES = [(0, 0), (0, 1), (7, 3), (12345, 63), (2**33 + 1, 2), (2**40 + 5, 511), (3, 0, 5, 6)]
+def gen_prng():
+    out = {}
+    for k, ent in enumerate(PRNG_TUPLES):
+        p = kb.Prng(*ent)
+        out[f"draws_{k}"] = np.array([p.random() for _ in range(1000)])
+        out[f"entropy_{k}"] = np.array(ent, dtype=np.uint64)
+        out[f"ssw_{k}"] = np.random.SeedSequence(entropy=ent).generate_state(8, np.uint32)
+    save("prng.npz", **out)
+
+
+def gen_norms():
+    out = {}
+    for n in NORM_WIDTHS:
+        a = norm_matrix(n)
+        out[f"sq_{n}"] = kb.row_norm_cache(a).sq_norms.copy()
+        out[f"sha_{n}"] = np.array(sha(a))
+    save("norms.npz", **out)
+
+
+def system(m, n, seed):
+    return kb.generate_mother(kb.GeneratorConfig(m_max=m, n_max=n, seed=seed))
+
+
+def streams(sys_, cfg, count):
+    cache = kb.row_norm_cache(sys_.A)
+    samplers, rngs = kb.solvers.worker_streams(cache, cfg)
+    return np.array([[samplers[t].sample(rngs[t]) for _ in range(count)] for t in range(cfg.q)],
+                    dtype=np.int32)
+
+
+def main():
+    t0 = time.time()
+    gen_prng()
+    gen_norms()
+
+    systems = {}
+    c0 = system(2000, 50, 0)
+    s500 = system(500, 20, 1)
+    s2000 = system(2000, 50, 7)
+    inc = kb.make_inconsistent(s2000, noise_seed=11)
+    crop = kb.crop(s2000, 300, 40)
+    c1 = system(20000, 500, 0)
+    for name, s in [("c0", c0), ("s500", s500), ("s2000", s2000), ("inc2000", inc), ("crop300x40", crop),
+                    ("c1", c1)]:
+        systems[f"{name}_A"] = np.array(sha(s.A))
+        systems[f"{name}_b"] = np.array(sha(s.b))
+        ref = s.x_star if s.x_star is not None else s.x_ls
+        systems[f"{name}_xref"] = np.array(sha(ref))
+        systems[f"{name}_shape"] = np.array(s.A.shape)
+    # x_ls itself (CGLS restatement is tolerance-checked, not hashed)
+    systems["inc2000_xls"] = inc.x_ls.copy()
+    print("systems done", time.time() - t0, flush=True)
+
+    rows = {}
+    for seed in range(10):
+        rows[f"c0_rk_s{seed}"] = streams(c0, kb.SolverConfig(variant="rk", base_seed=seed), 2000)
+    for scheme in ("full_access", "distributed"):
+        for seed in (0, 1):
+            cfg = kb.SolverConfig(variant="rka", q=64, base_seed=seed, sampling_scheme=scheme)
+            rows[f"c1_q64_{scheme}_s{seed}"] = streams(c1, cfg, 256)
+        cfg = kb.SolverConfig(variant="rka", q=8, base_seed=5, sampling_scheme=scheme)
+        rows[f"s2000_q8_{scheme}_s5"] = streams(s2000, cfg, 1000)
+    systems_c2 = system(80000, 1000, 0)
+    systems["c2_A"] = np.array(sha(systems_c2.A))
+    systems["c2_b"] = np.array(sha(systems_c2.b))
+    systems["c2_xref"] = np.array(sha(systems_c2.x_star))
+    systems["c2_shape"] = np.array(systems_c2.A.shape)
+    rows["c2_q64_full_access_s0"] = streams(systems_c2, kb.SolverConfig(variant="rkab", q=64, block_size=500,
+                                                                        base_seed=0), 256)
+    save("systems.npz", **systems)
+    save("rows.npz", **rows)
+    print("rows done", time.time() - t0, flush=True)
+
+    solves = {}
+
+    def record(tag, sys_, cfg, every, **kw):
+        cap = []
+        r = kb.run_solver(sys_, cfg, capture=cap, **kw)
+        solves[f"{tag}_iterations"] = np.array(r.iterations)
+        solves[f"{tag}_error_evals"] = np.array(r.error_evals)
+        solves[f"{tag}_converged"] = np.array(r.converged)
+        solves[f"{tag}_final_error_sq"] = np.array(r.final_error_sq)
+        solves[f"{tag}_final_residual"] = np.array(r.final_residual)
+        solves[f"{tag}_x"] = r.x.copy()
+        solves[f"{tag}_every"] = np.array(every)
+        solves[f"{tag}_ckpt"] = np.array(cap[every - 1::every]) if len(cap) >= every else np.zeros((0, sys_.n))
+        print(tag, r.iterations, r.converged, f"{time.time() - t0:.1f}s", flush=True)
+
+    for seed in range(10):
+        record(f"c0_rk_s{seed}", c0, kb.SolverConfig(variant="rk", base_seed=seed), 100)
+    for seed in range(3):
+        record(f"c1_rka64_s{seed}", c1, kb.SolverConfig(variant="rka", q=64, base_seed=seed), 1000)
+    record("c2_rkab64_bs500_s0", systems_c2, kb.SolverConfig(variant="rkab", q=64, block_size=500,
+                                                             base_seed=0), 1)
+    # desk-scale cases: reduction identities, schemes, weights, budget replay
+    record("s500_rk_s5", s500, kb.SolverConfig(variant="rk", base_seed=5), 1)
+    record("s500_rka3_s2", s500, kb.SolverConfig(variant="rka", q=3, base_seed=2), 1)
+    record("s500_rkab3_bs1_s2", s500, kb.SolverConfig(variant="rkab", q=3, block_size=1, base_seed=2), 1)
+    record("s500_rkab4_bs8_s3", s500, kb.SolverConfig(variant="rkab", q=4, block_size=8, base_seed=3), 1)
+    record("s2000_rka8_dist_s1", s2000, kb.SolverConfig(variant="rka", q=8, base_seed=1,
+                                                        sampling_scheme="distributed"), 10)
+    record("s2000_rkab8_bs50_dist_s4", s2000, kb.SolverConfig(variant="rkab", q=8, block_size=50, base_seed=4,
+                                                              sampling_scheme="distributed"), 1)
+    record("s2000_rka16_fixed_s0", s2000, kb.SolverConfig(variant="rka", q=16, alpha_policy="fixed",
+                                                          alpha=1.7, base_seed=0), 10)
+    record("s500_rka4_budget50_s9", s500, kb.SolverConfig(variant="rka", q=4, base_seed=9), 1, budget=50)
+    record("s500_rkab5_bs7_budget20_s6", s500, kb.SolverConfig(variant="rkab", q=5, block_size=7, base_seed=6),
+           1, budget=20)
+    save("solves.npz", **solves)
+
+    traces = {}
+    for q in (1, 4, 16):
+        recs = kb.trace_run(inc, kb.SolverConfig(variant="rka", q=q, base_seed=0), 3000, 100, inc.x_ls)
+        traces[f"inc2000_rka{q}"] = np.array([[r.iteration, r.error_norm, r.residual_norm] for r in recs])
+        traces[f"inc2000_rka{q}_plateau"] = np.array(kb.plateau_error(recs))
+    save("traces.npz", **traces)
+    print("all done", time.time() - t0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+"""T2-T4, T7: full B200 solves against the reference's own solves (golden
+fixtures) and the oracle: iteration counts equal, error_evals equal, every
+checkpoint within 1e-10 relative; the reference's KATs and reduction
+identities re-run through the B200 engine."""
+
+import numpy as np
+import pytest
+
+from conftest import PARITY_TOL, golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(**kw):
+    from paper_2401_17474_b200 import SolverConfig
+
+    return SolverConfig(**kw)
+
+
+def _check(report, g, tag, cap=None):
+    assert report.iterations == int(g[f"{tag}_iterations"]), tag
+    assert report.error_evals == int(g[f"{tag}_error_evals"]), tag
+    assert report.converged == bool(g[f"{tag}_converged"]), tag
+    assert rel_err(report.x, g[f"{tag}_x"]) <= PARITY_TOL, tag
+    if cap is not None:
+        ck = g[f"{tag}_ckpt"]
+        assert len(cap) == len(ck), tag
+        for j, (a, b) in enumerate(zip(cap, ck)):
+            assert rel_err(a, b) <= PARITY_TOL, (tag, j)
+
+
+def test_c0_rk_ten_seeds(gpu, systems):
+    from paper_2401_17474_b200 import DeviceSystem, solve_rk
+
+    g = golden("solves.npz")
+    with DeviceSystem(systems["c0"]) as ds:
+        for seed in range(10):
+            tag = f"c0_rk_s{seed}"
+            r = solve_rk(ds, _cfg(variant="rk", base_seed=seed), checkpoint_every=100)
+            cap = []
+            solve_rk(ds, _cfg(variant="rk", base_seed=seed), capture=cap)
+            _check(r, g, tag, cap[99::100])
+            assert abs(r.final_error_sq - float(g[f"{tag}_final_error_sq"])) <= 1e-12
+            assert abs(r.final_residual - float(g[f"{tag}_final_residual"])) <= 1e-8 * (1 + abs(r.final_residual))
+
+
+@pytest.mark.parametrize("kernel", ["auto", "chain", "sync_cluster", "sync_grid"])
+def test_c1_rka_q64(gpu, c1_system, kernel):
+    from paper_2401_17474_b200 import DeviceSystem, solve_rka_seq
+
+    g = golden("solves.npz")
+    with DeviceSystem(c1_system) as ds:
+        seeds = range(3) if kernel == "auto" else range(1)
+        for seed in seeds:
+            r = solve_rka_seq(ds, _cfg(variant="rka", q=64, base_seed=seed, kernel=kernel), checkpoint_every=1000)
+            tag = f"c1_rka64_s{seed}"
+            cap = []
+            _check(r, g, tag)
+            ck = g[f"{tag}_ckpt"]
+            r2 = solve_rka_seq(ds, _cfg(variant="rka", q=64, base_seed=seed, kernel=kernel), capture=cap)
+            assert r2.iterations == r.iterations and np.array_equal(r2.x, r.x)  # deterministic
+            for j, b in enumerate(ck):
+                assert rel_err(cap[1000 * (j + 1) - 1], b) <= PARITY_TOL, (kernel, seed, j)
+
+
+def test_c2_rkab_q64_bs500(gpu, c2_system):
+    from paper_2401_17474_b200 import DeviceSystem, solve_rkab_seq
+
+    g = golden("solves.npz")
+    tag = "c2_rkab64_bs500_s0"
+    with DeviceSystem(c2_system) as ds:
+        cap = []
+        r = solve_rkab_seq(ds, _cfg(variant="rkab", q=64, block_size=500, base_seed=0), capture=cap)
+    _check(r, g, tag, cap)
+
+
+DESK = [
+    ("s500_rk_s5", "s500", dict(variant="rk", base_seed=5), {}),
+    ("s500_rka3_s2", "s500", dict(variant="rka", q=3, base_seed=2), {}),
+    ("s500_rkab3_bs1_s2", "s500", dict(variant="rkab", q=3, block_size=1, base_seed=2), {}),
+    ("s500_rkab4_bs8_s3", "s500", dict(variant="rkab", q=4, block_size=8, base_seed=3), {}),
+    ("s2000_rka8_dist_s1", "s2000", dict(variant="rka", q=8, base_seed=1, sampling_scheme="distributed"), {}),
+    ("s2000_rkab8_bs50_dist_s4", "s2000", dict(variant="rkab", q=8, block_size=50, base_seed=4,
+                                                sampling_scheme="distributed"), {}),
+    ("s2000_rka16_fixed_s0", "s2000", dict(variant="rka", q=16, alpha_policy="fixed", alpha=1.7, base_seed=0), {}),
+    ("s500_rka4_budget50_s9", "s500", dict(variant="rka", q=4, base_seed=9), dict(budget=50)),
+    ("s500_rkab5_bs7_budget20_s6", "s500", dict(variant="rkab", q=5, block_size=7, base_seed=6), dict(budget=20)),
+]
+
+
+@pytest.mark.parametrize("tag,sysname,cfgkw,kw", DESK, ids=[d[0] for d in DESK])
+def test_desk_scale_solves(gpu, systems, tag, sysname, cfgkw, kw):
+    from paper_2401_17474_b200 import run_solver
+
+    g = golden("solves.npz")
+    cap = []
+    r = run_solver(systems[sysname], _cfg(**cfgkw), capture=cap, **kw)
+    every = int(g[f"{tag}_every"])
+    _check(r, g, tag, cap[every - 1::every])
+    if "budget" in kw:
+        assert r.error_evals == 0 and np.isnan(r.final_error_sq)
+
+
+def test_reduction_identities_bitwise(gpu, systems):
+    """RKA(q=1) == RK, RKAB(bs=1) == RKA, RKAB(q=1,bs=1) == RK (test_acceptance.py:28-55)."""
+    from paper_2401_17474_b200 import DeviceSystem, solve_rk, solve_rka_seq, solve_rkab_seq
+
+    with DeviceSystem(systems["s500"]) as ds:
+        c1, c2 = [], []
+        rk = solve_rk(ds, _cfg(variant="rk", base_seed=3), capture=c1)
+        rka1 = solve_rka_seq(ds, _cfg(variant="rka", q=1, base_seed=3), capture=c2)
+        assert rk.iterations == rka1.iterations and all(np.array_equal(u, v) for u, v in zip(c1, c2))
+        c3, c4 = [], []
+        rka3 = solve_rka_seq(ds, _cfg(variant="rka", q=3, base_seed=3), capture=c3)
+        rkab3 = solve_rkab_seq(ds, _cfg(variant="rkab", q=3, block_size=1, base_seed=3), capture=c4)
+        assert rka3.iterations == rkab3.iterations and all(np.array_equal(u, v) for u, v in zip(c3, c4))
+        rkab11 = solve_rkab_seq(ds, _cfg(variant="rkab", q=1, block_size=1, base_seed=3))
+        assert rkab11.iterations == rk.iterations and np.array_equal(rkab11.x, rk.x)
+
+
+def test_projection_kats(gpu):
+    """test_solvers_seq.py:14-25, 127-132, 188-201 through the B200 engine."""
+    from paper_2401_17474_b200 import LinearSystem, run_solver, solve_rka_seq, solve_rk
+
+    axis = LinearSystem(A=np.array([[1.0, 0.0]]), b=np.array([2.0]), x_star=np.array([2.0, 0.0]))
+    r = solve_rk(axis, _cfg(variant="rk"), budget=1)
+    assert np.array_equal(r.x, [2.0, 0.0])
+    obl = LinearSystem(A=np.array([[3.0, 4.0]]), b=np.array([10.0]), x_star=np.array([1.2, 1.6]))
+    r = solve_rk(obl, _cfg(variant="rk"), budget=1)
+    assert np.allclose(r.x, [1.2, 1.6], rtol=0, atol=1e-15)
+    r = solve_rk(obl, _cfg(variant="rk", alpha_policy="fixed", alpha=0.0), budget=3)
+    assert np.array_equal(r.x, [0.0, 0.0])
+    one = LinearSystem(A=np.array([[2.0]]), b=np.array([6.0]), x_star=np.array([3.0]))
+    r = run_solver(one, _cfg(variant="rk"))
+    assert r.converged and r.iterations == 1 and np.array_equal(r.x, [3.0])
+    ident = LinearSystem(A=np.eye(3), b=np.array([1.0, 2.0, 3.0]), x_star=np.array([1.0, 2.0, 3.0]))
+    r = run_solver(ident, _cfg(variant="rk", base_seed=4))
+    assert r.converged and np.allclose(r.x, [1, 2, 3], atol=1e-4)
+    # identity averaging (test_solvers_seq.py:165-170): two draws from x = 0 average to
+    # (2, 0), (0, 4) or, for distinct rows, (1, 2)
+    eye2 = LinearSystem(A=np.eye(2), b=np.array([2.0, 4.0]), x_star=np.array([2.0, 4.0]))
+    seen = set()
+    for seed in range(50):
+        r = solve_rka_seq(eye2, _cfg(variant="rka", q=2, base_seed=seed), budget=1)
+        seen.add(tuple(r.x.tolist()))
+    assert seen <= {(2.0, 0.0), (0.0, 4.0), (1.0, 2.0)} and (1.0, 2.0) in seen
+
+
+def test_projection_property_1000_steps(gpu):
+    """test_acceptance.py:58-71: after one unit step the sampled equation holds to 1e-10 (1+|b_i|)."""
+    from paper_2401_17474_b200 import LinearSystem, Prng, solve_rk
+
+    rng = Prng(2024, 1)
+    for _ in range(200):
+        n = 2 + int(rng.random() * 10)
+        a = rng.standard_normal((1, n)) * (1 + 9 * rng.random())
+        b = rng.standard_normal(1) * 10
+        r = solve_rk(LinearSystem(A=a, b=b, x_star=np.zeros(n)), _cfg(variant="rk"), budget=1)
+        assert abs(float(a[0] @ r.x) - b[0]) <= 1e-10 * (1 + abs(b[0]))
+
+
+def test_trace_mode_matches_reference(gpu, inc2000):
+    from paper_2401_17474_b200 import DeviceSystem, plateau_error, trace_run
+
+    g = golden("traces.npz")
+    with DeviceSystem(inc2000) as ds:
+        for q in (1, 4, 16):
+            recs = trace_run(ds, _cfg(variant="rka", q=q, base_seed=0), 3000, 100, inc2000.x_ls)
+            ref = g[f"inc2000_rka{q}"]
+            assert len(recs) == len(ref)
+            for rec, row in zip(recs, ref):
+                assert rec.iteration == int(row[0])
+                assert abs(rec.error_norm - row[1]) <= 1e-9 * (1 + row[1])
+                assert abs(rec.residual_norm - row[2]) <= 1e-9 * (1 + row[2])
+            assert abs(plateau_error(recs) - float(g[f"inc2000_rka{q}_plateau"])) <= 1e-9
+
+
+def test_max_iterations_exhausted_is_flagged(gpu, systems):
+    from paper_2401_17474_b200 import run_solver
+
+    r = run_solver(systems["c0"], _cfg(variant="rk", max_iterations=37))
+    assert not r.converged and r.iterations == 37 and r.error_evals == 38
+    r = run_solver(systems["c0"], _cfg(variant="rka", q=8, max_iterations=5))
+    assert not r.converged and r.iterations == 5 and r.error_evals == 6
+
+
+def test_oracle_agreement_random_configs(gpu, oracle, systems):
+    """Cross-check against the oracle on configurations with no reference fixture."""
+    from paper_2401_17474_b200 import DeviceSystem, solve_rka_seq, solve_rkab_seq
+
+    s = systems["s2000"]
+    with DeviceSystem(s) as ds:
+        for q, scheme in ((2, "full_access"), (5, "distributed"), (33, "full_access"), (128, "distributed")):
+            for kernel in ("chain", "sync_cluster", "sync_grid"):
+                r = solve_rka_seq(ds, _cfg(variant="rka", q=q, base_seed=q, sampling_scheme=scheme, kernel=kernel),
+                                  checkpoint_every=50)
+                o = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=q, base_seed=q, scheme=scheme, ckpt_every=50)
+                assert r.iterations == o["iterations"], (q, kernel)
+                assert rel_err(r.x, o["x"]) <= PARITY_TOL
+        for q, bs in ((2, 3), (7, 64), (64, 10)):
+            r = solve_rkab_seq(ds, _cfg(variant="rkab", q=q, block_size=bs, base_seed=1))
+            o = oracle.solve(s.A, s.b, s.x_star, variant="rkab", q=q, block_size=bs, base_seed=1)
+            assert r.iterations == o["iterations"], (q, bs)
+            assert rel_err(r.x, o["x"]) <= PARITY_TOL
