@@ -1,0 +1,296 @@
+"""Benchmark: row projections/s and time-to-||x - x*||^2 < 1e-8 (fp64) of the
+B200 RK / RKA / RKAB engine on BASELINE.json's configurations.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c1]
+
+A *step* is one full solve to epsilon of one solver seed (seeds cycle 0..9,
+the reference protocol's per-seed measurement, harness.py:127-149) on the
+workload's system, which is resident in HBM before timing starts.  `value`
+is rows projected / device time of the K timed steps; L2 is flushed between
+steps (the flush is outside the timed windows).  `e2e` runs the same solves
+through the public API with host (pinned) arrays: H2D of A, b, x*, the
+solve, and the D2H of x are inside its timed region.
+
+`--impl reference` times the reference algorithm's CPU implementation --
+the oracle port in oracle/ (the reference itself is pure Python + numpy and
+cannot be compiled) -- on all host cores, same workload, metric and units.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "row projections/s (fp64, solve to ||x-x*||^2<1e-8)"
+UNIT = "rows/s"
+
+WORKLOADS = {
+    # name: (m, n, solver kwargs, description)
+    "c0": (2000, 50, dict(variant="rk", q=1), "BASELINE c0: sequential RK, 2000x50"),
+    "c1": (20000, 500, dict(variant="rka", q=64), "BASELINE c1: RKA q=64, 20000x500"),
+    "c2": (80000, 1000, dict(variant="rkab", q=64, block_size=500), "BASELINE c2: RKAB q=64 bs=500, 80000x1000"),
+}
+
+
+def read_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_system(name):
+    from paper_2401_17474_b200 import GeneratorConfig, generate_mother
+
+    m, n, kw, _ = WORKLOADS[name]
+    return generate_mother(GeneratorConfig(m_max=m, n_max=n, seed=0)), kw
+
+
+def run_reference(args, name, rank, world):
+    """CPU arm: the oracle port of the reference algorithm on all host cores."""
+    if rank != 0:
+        return
+    import oracle as O
+
+    system, kw = build_system(name)
+    cores = O.max_threads()
+    m, n = system.A.shape
+
+    def one(seed):
+        t0 = time.perf_counter()
+        r = O.solve(system.A, system.b, system.x_star, base_seed=seed, nthreads=cores, **_oracle_kw(kw))
+        return time.perf_counter() - t0, r
+
+    for w in range(args.warmup):
+        one(w % 10)
+    tot_t, rows, iters = 0.0, 0, []
+    for k in range(args.steps):
+        dt, r = one(k % 10)
+        tot_t += dt
+        rows += r["iterations"] * _rows_per_iter(kw)
+        iters.append(r["iterations"])
+    value = rows / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
+        "config": {"workload": WORKLOADS[name][3], "m": m, "n": n, **kw, "seeds": "0..9 cycling"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full solves to eps (oracle/kz_oracle.c, pthreads x{cores})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iterations": iters,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_kw(kw):
+    out = dict(variant=kw["variant"], q=kw.get("q", 1), block_size=kw.get("block_size", 1))
+    return out
+
+
+def _rows_per_iter(kw):
+    return kw.get("q", 1) * (kw.get("block_size", 1) if kw["variant"] == "rkab" else 1)
+
+
+def cpu_baseline(name, system, kw, budget_s=12.0):
+    import oracle as O
+
+    cores = O.max_threads()
+    rows, t, seeds = 0, 0.0, 0
+    while t < budget_s and seeds < 10:
+        t0 = time.perf_counter()
+        r = O.solve(system.A, system.b, system.x_star, base_seed=seeds, nthreads=cores, **_oracle_kw(kw))
+        t += time.perf_counter() - t0
+        rows += r["iterations"] * _rows_per_iter(kw)
+        seeds += 1
+    return {"value": rows / t, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{seeds} full solves to eps (seeds 0..{seeds - 1}) of {name}, oracle/kz_oracle.c pthreads"}
+
+
+def run_b200(args, name, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver
+    from paper_2401_17474_b200 import _native as N
+    from paper_2401_17474_b200.solvers import release_pool
+
+    torch.cuda.set_device(local_rank)
+    system, kw = build_system(name)
+    m, n = system.A.shape
+    cfg = SolverConfig(device=local_rank, **kw)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
+    ds = DeviceSystem(system, device=local_rank)
+    for w in range(args.warmup):
+        run_solver(ds, cfg.replace(base_seed=w % 10))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = N.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    rows = 0
+    kernel_ms = 0.0
+    iters = []
+    kernel_name = None
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            starts[k].record()
+            r = run_solver(ds, cfg.replace(base_seed=k % 10))
+            ends[k].record()
+            assert r.converged, f"seed {k % 10} did not converge"
+            rows += r.gpu["rows_projected"]
+            kernel_ms += r.gpu["kernel_ms"]
+            kernel_name = r.gpu["kernel"]
+            iters.append(r.iterations)
+        torch.cuda.synchronize()
+    launches = N.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([t_ms], device=f"cuda:{local_rank}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        dist.barrier()
+    ds.close()
+
+    # e2e through the public API with pinned host arrays (H2D + solve + D2H per step)
+    from paper_2401_17474_b200 import LinearSystem
+
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    hsys = LinearSystem(A=pin(system.A), b=pin(system.b), x_star=pin(system.x_star), seed=0)
+    run_solver(hsys, cfg.replace(base_seed=0))  # warm the allocation pool
+    torch.cuda.synchronize()
+    e2e_rows = 0
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        r = run_solver(hsys, cfg.replace(base_seed=k % 10))
+        e2e_rows += r.gpu["rows_projected"]
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    release_pool()
+    h2d = system.A.nbytes + system.b.nbytes + system.x_star.nbytes
+    d2h = n * 8
+
+    if rank != 0:
+        return
+    peak, peak_src = read_peak()
+    bytes_per_row = 8 * n
+    achieved = rows * bytes_per_row / (kernel_ms / 1e3) / 1e9
+    value = world * rows / (t_ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0; bitwise = reference)",
+        "config": {"workload": WORKLOADS[name][3], "m": m, "n": n, **kw, "seeds": "0..9 cycling",
+                   "l2": "256 MiB write between steps, outside the timed windows",
+                   "parallelism": "replicas" if world > 1 else "1 GPU", "kernel": kernel_name},
+        "time_to_eps_ms": {"mean": float(np.mean(step_ms)), "min": float(np.min(step_ms)),
+                           "max": float(np.max(step_ms))},
+        "iterations": iters,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src, "kernel": f"kz::sync/chain ({kernel_name})",
+                     "algorithmic_bytes": "8*n per row projection"},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_rows / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, system, kw)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c1")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, args.workload, rank, world)
+    else:
+        run_b200(args, args.workload, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,20 +94,22 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     for (int64_t e = tid; e < IDX_WINDOW && e < total; e += T) sm.win[e] = idx[e];
     __syncthreads();
 
-    auto issue = [&](int64_t d) {
+    // ring bookkeeping in 32-bit: row d lives in stage d % D, its (b_i, sq_i)
+    // in slot d % (D + 1); both advance incrementally (no 64-bit modulo).
+    auto issue = [&](int64_t d, int stage, int slot) {
         if (d < total) {
             const int64_t i = sm.win[d & (IDX_WINDOW - 1)];
             const double* src = a.A + i * ld;
-            double* dst = sm.ring + (d % D) * ld;
+            double* dst = sm.ring + (size_t)stage * ld;
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
                 const int64_t col = 2 * ((int64_t)p * T + tid);
                 if (col < ld) cp_async16(dst + col, src + col);
             }
             if (tid == 0) {
-                double* slot = sm.bsq + 2 * (d % (D + 1));
-                cp_async8(slot, a.b + i);
-                cp_async8(slot + 1, a.sq + i);
+                double* bs_slot = sm.bsq + 2 * slot;
+                cp_async8(bs_slot, a.b + i);
+                cp_async8(bs_slot + 1, a.sq + i);
             }
         }
         cp_async_commit();
@@ -129,7 +131,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         return e;
     };
 
-    for (int j = 0; j < D - 1; ++j) issue(j);
+    for (int j = 0; j < D - 1; ++j) issue(j, j, j);
+    int stage = 0, slot = 0;  // consumption position of draw d
 
     int par = 0;
     unsigned epoch = 0;
@@ -161,9 +164,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 for (int64_t e = d + 512 + tid; e < d + IDX_WINDOW && e < total; e += T)
                     sm.win[e & (IDX_WINDOW - 1)] = idx[e];
             }
-            issue(d + D - 1);
+            issue(d + D - 1, stage == 0 ? D - 1 : stage - 1, slot >= 2 ? slot - 2 : slot + D - 1);
             cp_async_wait_dyn(D - 1);
-            const double* row = sm.ring + (d % D) * ld;
+            const double* row = sm.ring + (size_t)stage * ld;
             double dot = 0.0, e2 = 0.0;
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
@@ -187,8 +190,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 cta_reduce<false>(dot, e2, sm.red, par, lane, warp, nw);
             }
             {
-                const double* slot = sm.bsq + 2 * (d % (D + 1));
-                const double scale = __ddiv_rn(__dmul_rn(alpha, __dsub_rn(slot[0], dot)), slot[1]);
+                const double* bq = sm.bsq + 2 * slot;
+                const double scale = __ddiv_rn(__dmul_rn(alpha, __dsub_rn(bq[0], dot)), bq[1]);
 #pragma unroll
                 for (int p = 0; p < EP; ++p) {
                     const int64_t col = 2 * ((int64_t)p * T + tid);
@@ -199,6 +202,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                     }
                 }
             }
+            stage = (stage + 1 == D) ? 0 : stage + 1;
+            slot = (slot == D) ? 0 : slot + 1;
         }
         const int64_t k = a.k0 + kk;
         const bool ck = a.ckpt_every > 0 && ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;

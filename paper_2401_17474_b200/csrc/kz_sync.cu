@@ -62,16 +62,15 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
     }
     __syncthreads();
 
-    auto issue = [&](int64_t it) {
+    const unsigned np32 = (unsigned)npairs, work = (unsigned)(q * npairs);
+    auto issue = [&](int64_t it, int st) {
         if (it < a.count) {
-            const int st = (int)(it % D);
             const int32_t* ir = iring + (it & 3) * q;
             double* dst = ring + (size_t)st * q * cw;
-            const int64_t work = q * npairs;
-            for (int64_t u = tid; u < work; u += T) {
-                const int64_t t = u / npairs, p = u - t * npairs;
-                const int64_t col = c0 + 2 * p;
-                if (col < c1) cp_async16(dst + t * cw + 2 * p, a.A + (int64_t)ir[t] * ld + col);
+            for (unsigned u = tid; u < work; u += T) {
+                const unsigned t = u / np32, pp = u - t * np32;
+                const int64_t col = c0 + 2 * pp;
+                if (col < c1) cp_async16(dst + (size_t)t * cw + 2 * pp, a.A + (int64_t)ir[t] * ld + col);
             }
             for (int64_t t = tid; t < q; t += T) {
                 cp_async8(bsq + ((size_t)st * q + t) * 2, a.b + ir[t]);
@@ -81,7 +80,8 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
         cp_async_commit();
     };
 
-    for (int j = 0; j < D - 1; ++j) issue(j);
+    for (int j = 0; j < D - 1; ++j) issue(j, j);
+    int st = 0;  // ring stage of iteration kk
 
     unsigned epoch = 0;
     long long done = 0;
@@ -95,14 +95,13 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
         const bool last = (kk == a.count);
         const bool want_check = a.use_stop && (!last || a.final_check);
         if (last && !want_check) break;
-        const int st = (int)(kk % D);
         const double* rows = ring + (size_t)st * q * cw;
         if (!last) {
             cp_async_wait_dyn(D - 2);
         }
         __syncthreads();  // stage kk visible to all; iteration kk-1 fully retired
         if (!last) {
-            issue(kk + D - 1);
+            issue(kk + D - 1, st == 0 ? D - 1 : st - 1);
             // index ring: iteration kk + D, consumed by issue() one iteration from now
             const int64_t itn = kk + D;
             if (itn < a.count)
@@ -112,13 +111,17 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
         double* mypart = part + (kk & 1) * (q + 1);
         double* gpart = a.part + ((size_t)(kk & 1) * P + c) * (q + 1);
         if (!last) {
-            for (int64_t t = g; t < q; t += groups) {
-                const double* r = rows + t * cw;
+            // rounds of `groups` rows; every lane joins each round's shuffles
+            for (int64_t t0 = 0; t0 < q; t0 += groups) {
+                const int64_t t = t0 + g;
                 double s = 0.0;
-                for (int64_t j = gl; j < wdt; j += LPR) s = fma(r[j], xs[j], s);
+                if (t < q) {
+                    const double* r = rows + t * cw;
+                    for (int64_t j = gl; j < wdt; j += LPR) s = fma(r[j], xs[j], s);
+                }
 #pragma unroll
                 for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LPR);
-                if (gl == 0) {
+                if (gl == 0 && t < q) {
                     if (CLUSTER)
                         mypart[t] = s;
                     else
@@ -151,15 +154,20 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
         for (int64_t t = tid; t <= q; t += T) {
             if (t < nt || t == q) {
                 double s = 0.0;
-                for (int cc = 0; cc < P; ++cc) {
-                    double pv;
-                    if (CLUSTER) {
-                        const double* rp = cg::this_cluster().map_shared_rank(part, cc);
-                        pv = rp[(kk & 1) * (q + 1) + t];
-                    } else {
-                        pv = __ldcg(a.part + ((size_t)(kk & 1) * P + cc) * (q + 1) + t);
-                    }
-                    s = (cc == 0) ? pv : __dadd_rn(s, pv);
+                if (CLUSTER) {
+                    // issue all remote (DSMEM) loads first, then add in CTA order
+                    double pv[16];
+#pragma unroll
+                    for (int cc = 0; cc < 16; ++cc)
+                        if (cc < P) pv[cc] = cg::this_cluster().map_shared_rank(part, cc)[(kk & 1) * (q + 1) + t];
+                    s = pv[0];
+#pragma unroll
+                    for (int cc = 1; cc < 16; ++cc)
+                        if (cc < P) s = __dadd_rn(s, pv[cc]);
+                } else {
+                    const double* gp = a.part + (size_t)(kk & 1) * P * (q + 1) + t;
+                    s = __ldcg(gp);
+                    for (int cc = 1; cc < P; ++cc) s = __dadd_rn(s, __ldcg(gp + (size_t)cc * (q + 1)));
                 }
                 if (t < q) {
                     const double* bs2 = bsq + ((size_t)st * q + t) * 2;
@@ -179,6 +187,7 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
             }
         }
         if (last) break;
+        st = (st + 1 == D) ? 0 : st + 1;
         // ---- ordered average over the q projections (solvers.py:131-137) -------------
         const int64_t k = a.k0 + kk;
         const bool ck = a.ckpt_every > 0 && ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;

@@ -35,6 +35,7 @@ KERNELS = tuple(N.KERNELS)
 
 # capture=list keeps every iterate (reference semantics); refuse absurd sizes
 _CAPTURE_LIMIT_BYTES = 4 << 30
+_CAPTURE_FIRST_BYTES = 256 << 20
 
 
 @dataclass
@@ -196,6 +197,44 @@ class DeviceSystem:
             pass
 
 
+# Device allocations for host-array calls are recycled by shape (a caching
+# allocator): every call still uploads A, b, x_ref and recomputes the row norms
+# and sampler, like the reference's per-call row_norm_cache (solvers.py:299).
+_POOL: dict[tuple[int, int, int], list[DeviceSystem]] = {}
+_POOL_MAX_BYTES = 8 << 30
+
+
+def _pool_acquire(system: LinearSystem, device: int) -> DeviceSystem:
+    A = system.A
+    if getattr(A, "ndim", 0) != 2:
+        raise DimensionMismatchError(f"expected a 2-D matrix, got ndim={getattr(A, 'ndim', None)}")
+    key = (A.shape[0], A.shape[1], device)
+    free = _POOL.get(key)
+    if free:
+        ds = free.pop()
+        ds.host = system
+        xr = system.x_star if system.x_star is not None else system.x_ls
+        ds.upload(system.A, system.b, xr)
+        return ds
+    return DeviceSystem(system, device=device)
+
+
+def _pool_release(ds: DeviceSystem) -> None:
+    ds.host = None
+    if ds.m * ds.n * 8 <= _POOL_MAX_BYTES and not _POOL.get((ds.m, ds.n, ds.device)):
+        _POOL.setdefault((ds.m, ds.n, ds.device), []).append(ds)
+    else:
+        ds.close()
+
+
+def release_pool() -> None:
+    """Free the cached device allocations of host-array calls."""
+    for lst in _POOL.values():
+        for ds in lst:
+            ds.close()
+    _POOL.clear()
+
+
 def resolve_alphas(system, cfg: SolverConfig, q: int | None = None) -> np.ndarray:
     """Per-worker weights (solvers.py:148-159)."""
     q = cfg.q if q is None else q
@@ -233,7 +272,7 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
         raise ValueError(f"trace_step must be >= 1, got {trace_step}")
 
     own = not isinstance(system, DeviceSystem)
-    ds = DeviceSystem(system, device=cfg.device) if own else system
+    ds = _pool_acquire(system, cfg.device) if own else system
     try:
         if x_ref is not None:
             ds.set_x_ref(x_ref)
@@ -261,10 +300,9 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
         every = checkpoint_every if checkpoint_every else (1 if capture is not None else 0)
         ck_buf = None
         if every:
-            cap = limit // every
-            if cap * ds.n * 8 > _CAPTURE_LIMIT_BYTES:
-                raise ValueError(f"capture of {cap} iterates of length {ds.n} exceeds "
-                                 f"{_CAPTURE_LIMIT_BYTES >> 30} GiB; pass checkpoint_every")
+            # start with a modest buffer; a stop-mode run that outgrows it is
+            # replayed below with an exact one (runs are deterministic)
+            cap = min(limit // every, max(1, _CAPTURE_FIRST_BYTES // (8 * ds.n)))
             ck_buf = np.empty((max(cap, 1), ds.n))
             p.ckpt_every, p.ckpt_capacity, p.ckpt_host = every, cap, N.ptr(ck_buf)
         p.kernel = N.KERNELS[cfg.kernel]
@@ -272,9 +310,21 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
         r = N.Result()
         x = np.empty(ds.n)
         N.check(N.load_library().kz_solve(ds.handle, C.byref(p), C.byref(r), N.ptr(x), None))
+        if every and r.n_ckpt < r.iterations // every:
+            need = r.iterations // every
+            if need * ds.n * 8 > _CAPTURE_LIMIT_BYTES:
+                raise ValueError(f"capture of {need} iterates of length {ds.n} exceeds "
+                                 f"{_CAPTURE_LIMIT_BYTES >> 30} GiB; pass checkpoint_every")
+            ck_buf = np.empty((need, ds.n))
+            p2 = N.Params.from_buffer_copy(p)
+            p2.budget, p2.trace_step = int(r.iterations), 0
+            p2.ckpt_capacity, p2.ckpt_host = need, N.ptr(ck_buf)
+            r2 = N.Result()
+            N.check(N.load_library().kz_solve(ds.handle, C.byref(p2), C.byref(r2), None, None))
+            r.n_ckpt = r2.n_ckpt
     finally:
         if own:
-            ds.close()
+            _pool_release(ds)
 
     if capture is not None and ck_buf is not None:
         capture.extend(ck_buf[i].copy() for i in range(r.n_ckpt))
