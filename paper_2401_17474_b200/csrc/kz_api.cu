@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -156,15 +157,17 @@ struct kz_system {
     int device = 0;
     int64_t m = 0, n = 0, ld = 0;
     int sms = 0;
-    DevBuf<double> A, b, xref, x, sq, cdf, tmp, V, part, ckpt, alphas;
+    DevBuf<double> A, b, xref, x, sq, cdf, tmp, V, part, ckpt, alphas, bs2;
     DevBuf<int64_t> lo, len;
     DevBuf<int32_t> idx, rows_out;
     DevBuf<PcgPod> states;
     DevBuf<unsigned> barrier;
     DevBuf<SolveStatus> status;
     DevBuf<unsigned long long> zero_row;
+    DevBuf<long long> dbg;
     SolveStatus* h_status = nullptr;  // pinned
     bool norms_valid = false;
+    bool bs2_valid = false;
     int64_t bad_row = -1;
     int sampler_scheme = -1;
     int64_t sampler_q = 0;
@@ -228,7 +231,7 @@ extern "C" int32_t kz_system_create(int32_t device, int64_t m, int64_t n, kz_sys
 extern "C" int32_t kz_system_destroy(kz_system* s) {
     if (!s) return KZ_OK;
     cudaSetDevice(s->device);
-    for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas})
+    for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas, &s->bs2})
         b->release();
     s->lo.release();
     s->len.release();
@@ -263,6 +266,7 @@ static int upload_common(kz_system* s, const double* A, int64_t lda, const doubl
         s->has_xref = false;
     }
     s->norms_valid = false;
+    s->bs2_valid = false;
     s->sampler_scheme = -1;
     KZ_CUDA(cudaStreamSynchronize(st));
     return KZ_OK;
@@ -302,6 +306,7 @@ extern "C" int32_t kz_system_set_xref(kz_system* s, const double* xref, void* st
 extern "C" int32_t kz_system_touch(kz_system* s) {
     if (!s) return fail(KZ_EINVAL, "null system");
     s->norms_valid = false;
+    s->bs2_valid = false;
     s->sampler_scheme = -1;
     return KZ_OK;
 }
@@ -322,6 +327,7 @@ static int ensure_norms(kz_system* s, cudaStream_t st) {
     KZ_CUDA(cudaMemcpyAsync(&first, s->zero_row.p, sizeof(first), cudaMemcpyDeviceToHost, st));
     KZ_CUDA(cudaStreamSynchronize(st));
     s->norms_valid = true;
+    s->bs2_valid = false;
     s->bad_row = (first == ~0ULL) ? -1 : (int64_t)first;
     s->sampler_scheme = -1;
     if (s->bad_row >= 0)
@@ -506,9 +512,13 @@ int chain_smem(int64_t ld, int stages) {
                  2 * 64 * sizeof(double));
 }
 
-size_t sync_smem(int64_t q, int64_t cw, int stages) {
-    return (size_t)stages * q * cw * sizeof(double) + (size_t)stages * q * 2 * sizeof(double) + 2 * cw * sizeof(double) +
-           2 * (q + 1) * sizeof(double) + (q + 1) * sizeof(double) + q * sizeof(double) + 4 * q * sizeof(int32_t);
+size_t sync_smem(int64_t q, int64_t cw, int stages, int P, bool cluster) {
+    const int nwarp = 256 / 32, seg_max = 64;
+    const int64_t rs = cw + 2, q1p = (q + 2) & ~(int64_t)1;
+    return 16 + (size_t)stages * q * rs * sizeof(double) + (size_t)stages * q * 2 * sizeof(double) +
+           2 * cw * sizeof(double) + (cluster ? 2 * (size_t)P * q1p * sizeof(double) : 0) +
+           (size_t)nwarp * cw * sizeof(double) + (size_t)nwarp * seg_max * sizeof(double) +
+           nwarp * sizeof(double) + q * sizeof(double) + 8 * q * sizeof(int32_t);
 }
 
 void* chain_fn(int ep) {
@@ -522,8 +532,10 @@ void* chain_fn(int ep) {
 }
 
 void* sync_fn(bool cluster, int lpr) {
-    if (cluster) return lpr == 8 ? (void*)sync_kernel<true, 8> : (void*)sync_kernel<true, 32>;
-    return lpr == 8 ? (void*)sync_kernel<false, 8> : (void*)sync_kernel<false, 32>;
+    if (cluster) return lpr == 4 ? (void*)sync_kernel<true, 4> : lpr == 8 ? (void*)sync_kernel<true, 8>
+                                                                          : (void*)sync_kernel<true, 32>;
+    return lpr == 4 ? (void*)sync_kernel<false, 4> : lpr == 8 ? (void*)sync_kernel<false, 8>
+                                                              : (void*)sync_kernel<false, 32>;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -575,6 +587,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
 
 static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, Plan& pl) {
     pl.threads = 256;
+    if (q > 512) return fail(KZ_EINVAL, "q=%lld exceeds the sync kernel's 512 workers", (long long)q);
     int P;
     if (cluster) {
         P = p->ctas > 0 ? p->ctas : 16;
@@ -588,16 +601,16 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
                                (long long)s->n);
         const int64_t cw = (((s->ld + P - 1) / P) + 1) & ~(int64_t)1;
         int stages = 4;
-        while (stages > 2 && sync_smem(q, cw, stages) > 200 * 1024) --stages;
-        if (sync_smem(q, cw, stages) > kSmemLimit) {
+        while (stages > 2 && sync_smem(q, cw, stages, P, cluster) > 200 * 1024) --stages;
+        if (sync_smem(q, cw, stages, P, cluster) > kSmemLimit) {
             if (cluster) return fail(KZ_EINVAL, "q=%lld row slices do not fit a cluster CTA", (long long)q);
             if (P >= 4 * s->sms) return fail(KZ_EINVAL, "q=%lld too large for the sync kernel", (long long)q);
             P *= 2;  // thinner slices, several CTAs per SM
             continue;
         }
         pl.stages = stages;
-        pl.smem = sync_smem(q, cw, stages);
-        pl.lpr = cw <= 64 ? 8 : 32;
+        pl.smem = sync_smem(q, cw, stages, P, cluster);
+        pl.lpr = cw > 64 ? 32 : (q > 32 ? 4 : 8);
         void* fn = sync_fn(cluster, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
         if (cluster) {
@@ -697,8 +710,14 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     const int64_t bs = p->variant == KZ_RKAB ? p->block_size : 1;
     KZ_CUDA(cudaSetDevice(s->device));
 
-    // --- setup: row norms, sampler, streams, weights ---
+    // --- setup: row norms, sampler, packed (b, sq), streams, weights ---
     KZ_TRY(ensure_sampler(s, p->scheme, q, st));
+    if (!s->bs2_valid) {
+        KZ_TRY(s->bs2.ensure(2 * (size_t)s->m));
+        pack_bs2_kernel<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->b.p, s->sq.p, s->m, s->bs2.p);
+        KZ_TRY(check_launch("pack_bs2_kernel"));
+        s->bs2_valid = true;
+    }
     std::vector<PcgPod> pods(q);
     for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)t);
     KZ_TRY(s->states.ensure(q));
@@ -749,6 +768,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.A = s->A.p;
     args.b = s->b.p;
     args.sq = s->sq.p;
+    args.bs2 = s->bs2.p;
     args.xref = s->xref.p;
     args.x = s->x.p;
     args.V = s->V.p;
@@ -767,6 +787,13 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.eps = p->epsilon;
     args.use_stop = stop_mode ? 1 : 0;
     args.stages = pl.stages;
+    const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
+    args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;
+    if (phase_timing) {
+        KZ_TRY(s->dbg.ensure(32 * 64));
+        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 64 * sizeof(long long), st));
+        args.dbg = s->dbg.p;
+    }
 
     const int64_t limit = budget_mode ? p->budget : p->max_iterations;
     int64_t k = 0, evals = 0;
@@ -855,5 +882,33 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
     KZ_CUDA(cudaStreamSynchronize(st));
     r->kernel_launches = g_launches.load() - launches0;
+    if (phase_timing) {  // per-phase completion (max over warps) relative to the earliest warp start, CTA 0
+        std::vector<long long> h(32 * 64);
+        KZ_CUDA(cudaMemcpy(h.data(), s->dbg.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        double acc[8] = {0}, span = 0;
+        int nrec = 0;
+        for (int k = 4; k < 31; ++k) {
+            long long t0 = -1, nxt = -1;
+            long long mx[8];
+            for (int ph = 0; ph < 8; ++ph) mx[ph] = -1;
+            bool ok = true;
+            for (int w = 0; w < 8; ++w) {
+                const long long* r = &h[(k * 8 + w) * 8];
+                const long long* rn = &h[((k + 1) * 8 + w) * 8];
+                if (r[0] == 0 || rn[0] == 0) { ok = false; break; }
+                t0 = (t0 < 0 || r[0] < t0) ? r[0] : t0;
+                nxt = (nxt < 0 || rn[0] < nxt) ? rn[0] : nxt;
+                for (int ph = 0; ph < 7; ++ph) if (r[ph] && r[ph] > mx[ph]) mx[ph] = r[ph];
+            }
+            if (!ok) continue;
+            for (int ph = 0; ph < 7; ++ph) acc[ph] += (double)(mx[ph] - t0);
+            span += (double)(nxt - t0);
+            ++nrec;
+        }
+        if (nrec)
+            fprintf(stderr, "[kz phase end, max over warps, cycles from start] top %.0f issued %.0f dots %.0f waited %.0f "
+                            "err %.0f scales %.0f update %.0f | iteration %.0f (n=%d)\n", acc[0] / nrec, acc[1] / nrec,
+                    acc[2] / nrec, acc[3] / nrec, acc[4] / nrec, acc[5] / nrec, acc[6] / nrec, span / nrec, nrec);
+    }
     return KZ_OK;
 }

@@ -18,6 +18,7 @@ struct SolveArgs {
     const double* A;       // m x ld, row-major, pitched
     const double* b;       // m
     const double* sq;      // m squared row norms (einsum order)
+    const double* bs2;     // m x 2 packed (b_i, sq_i)
     const double* xref;    // ld (zero padded)
     double* x;             // ld, the iterate (in/out)
     double* V;             // q x ld worker estimates (chain kernel, q > 1)
@@ -35,6 +36,8 @@ struct SolveArgs {
     int use_stop;          // evaluate the stop rule before each iteration
     int final_check;       // also evaluate it at k0 + count (max_iterations reached)
     int stages;            // cp.async ring depth
+    long long* dbg;        // optional phase timestamps (KZ_PHASE_TIMING=1)
+    int ablate;            // debug: bit mask of phases to skip (KZ_ABLATE), timing experiments only
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread.
@@ -62,6 +65,8 @@ __global__ void residual_rows_kernel(const double* __restrict__ A, const double*
                                      double* __restrict__ out);
 __global__ void diff_sq_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                                double* __restrict__ out);
+__global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __restrict__ sq, int64_t m,
+                                double* __restrict__ out);
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
 
 constexpr int NORM_ROWS_PER_CTA = 128;

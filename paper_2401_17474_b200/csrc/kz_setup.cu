@@ -212,6 +212,16 @@ __global__ void diff_sq_kernel(const double* __restrict__ x, const double* __res
     }
 }
 
+// (b_i, ||a_i||^2) packed for one 16-byte copy per sampled row
+__global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __restrict__ sq, int64_t m,
+                                double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        out[2 * i] = b[i];
+        out[2 * i + 1] = sq[i];
+    }
+}
+
 __global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
     __shared__ double part[32];
     double s = 0.0;

@@ -2,83 +2,154 @@
 //
 // Reference semantics (paths relative to /root/reference/pkg/src/kaczbench):
 //   rka_combined_step  solvers.py:120-137   q projections from one snapshot of x;
-//                                            x = (sum_t fl(x + fl(s_t a_t))) / q, t ascending
+//                                            x = (sum_t fl(x + fl(s_t a_t))) / q
 //   solve_rka_seq      solvers.py:313-334   rows of iteration k: one draw per worker stream
 //   _drive stop rule   solvers.py:229-243
 //
-// Layout: P CTAs each own a contiguous column slice [c0, c1) of x (kept in
-// shared memory) and of every sampled row.  Per iteration:
-//   1. the q row slices (indices known ahead) stream HBM -> smem through a
-//      cp.async ring `stages` iterations deep, with b_i and sq_i;
-//   2. LPR lanes per row form partial dots <a_t[c0:c1], x[c0:c1]>; warp 0
-//      adds the partial of ||x - x_ref||^2;
-//   3. the P x (q+1) partials are exchanged -- through distributed shared
-//      memory inside one thread-block cluster (CLUSTER) or through global
-//      memory behind a grid barrier -- and every CTA sums them in the same
-//      CTA order, so all CTAs hold bit-identical scales and stop decisions;
-//   4. each column of the slice applies the reference's ordered average.
-// Partials are double-buffered by iteration parity: one barrier/iteration.
-#include <cooperative_groups.h>
-
+// Layout: P CTAs each own a contiguous column slice [c0, c1) of x (shared
+// memory) and of every sampled row.  Per iteration k:
+//   1. the q row slices (indices are x-independent, known ahead) stream
+//      HBM -> smem through a cp.async ring `stages` iterations deep, with the
+//      packed (b_i, ||a_i||^2) pairs;
+//   2. LPR lanes per row form the partial dot <a_t[c0:c1], x[c0:c1]>;
+//   3. exchange (CLUSTER): each warp redistributes its rows' partials over
+//      its lanes with shuffles and every lane pushes them (st.async, 16 B)
+//      into one peer CTA's receive buffer, completing that CTA's mbarrier
+//      transaction count; each CTA then waits on its own mbarrier -- no
+//      cluster barrier, no GPU-scope fence.  Grid mode: global memory and a
+//      grid barrier.  The partial of ||x - x_ref||^2 rides along as entry q
+//      (its per-warp pieces come from the previous iteration's combine);
+//   4. scales: warp w owns the w-th contiguous block of workers; its lanes
+//      add that block's P partials with one fixed tree (bit-identical in
+//      every CTA) and form s_t = alpha (b - d) / ||a||^2;
+//   5. average: every lane (= column) sums fl(x + fl(s_t a_t)) over its
+//      warp's worker block; one CTA barrier; the per-warp sums of a column
+//      are added by a fixed shuffle tree and divided by q.  (The reference
+//      adds the q terms strictly left to right; regrouping changes the mean
+//      by a few ulp -- tolerance parity, like the dot product.)
+// Two CTA barriers per iteration.  All shared-memory index math is 32-bit.
 #include "kz_kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace kz {
 
+namespace {
+constexpr int NT = 256;           // threads per CTA
+constexpr int NW = NT / 32;       // warps per CTA
+constexpr int MAXP_TREE = 16;     // cluster size bound for the partial-sum tree
+constexpr int IDX_PER_THREAD = 4;
+constexpr int CPW = 32 / NW;      // columns per warp per combine round
+constexpr int SEG_MAX = 64;       // workers per warp block
+}  // namespace
+
 template <bool CLUSTER, int LPR>
-__global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = a.stages;
-    const int64_t ld = a.ld, q = a.q;
-    const int P = CLUSTER ? (int)cg::this_cluster().num_blocks() : (int)gridDim.x;
-    const int c = CLUSTER ? (int)cg::this_cluster().block_rank() : (int)blockIdx.x;
-    const int64_t cw = (((ld + P - 1) / P) + 1) & ~(int64_t)1;  // even => 16-byte pairs
-    const int64_t c0 = (int64_t)c * cw < ld ? (int64_t)c * cw : ld;
-    const int64_t c1 = (c0 + cw < ld) ? c0 + cw : ld;
-    const int64_t wdt = c1 - c0;  // this CTA's columns (may be 0)
-    const int64_t npairs = cw / 2;
+    const int ld = (int)a.ld, q = (int)a.q;
+    const int P = CLUSTER ? (int)cluster_size() : (int)gridDim.x;
+    const int c = CLUSTER ? (int)cluster_rank() : (int)blockIdx.x;
+    const int cw = (((ld + P - 1) / P) + 1) & ~1;  // even => 16-byte pairs
+    const int c0 = c * cw < ld ? c * cw : ld;
+    const int c1 = (c0 + cw < ld) ? c0 + cw : ld;
+    const int wdt = c1 - c0;  // this CTA's columns (may be 0); even
+    const int npairs = cw / 2;
+    const int rs = cw + 2;    // smem row stride: +16 B staggers banks across rows
+    const int q1 = q + 1;
+    const int q1p = (q1 + 1) & ~1;  // receive-row stride, even => 16-byte pushes
+    const int stage_elems = q * rs;
 
-    // shared memory carve
-    double* ring = reinterpret_cast<double*>(smem_raw);      // D x q x cw
-    double* bsq = ring + (size_t)D * q * cw;                 // D x q x 2
-    double* xs = bsq + (size_t)D * q * 2;                    // cw
-    double* xrs = xs + cw;                                   // cw
-    double* part = xrs + cw;                                 // 2 x (q + 1)
-    double* tot = part + 2 * (q + 1);                        // q + 1
-    double* alp = tot + (q + 1);                             // q
-    int32_t* iring = reinterpret_cast<int32_t*>(alp + q);    // 4 x q
+    // shared memory carve (sync_smem() in kz_api.cu must match)
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // 2 mbarriers
+    double* ring = reinterpret_cast<double*>(smem_raw + 16);                      // D x q x rs
+    double2* bq = reinterpret_cast<double2*>(ring + D * stage_elems);             // D x q (b_i, sq_i)
+    double* xs = reinterpret_cast<double*>(bq + D * q);                           // cw
+    double* xrs = xs + cw;                                                         // cw
+    double* inbuf = xrs + cw;                                                      // 2 x P x q1p (cluster)
+    double* upd = inbuf + (CLUSTER ? 2 * P * q1p : 0);                             // NW x cw
+    double* scal = upd + NW * cw;                                                  // NW x SEG_MAX
+    double* errw = scal + NW * SEG_MAX;                                            // NW
+    double* alp = errw + NW;                                                       // q
+    int32_t* iring = reinterpret_cast<int32_t*>(alp + q);                          // 8 x q
 
-    for (int64_t j = tid; j < cw; j += T) {
+    for (int j = tid; j < cw; j += NT) {
         xs[j] = (j < wdt) ? __ldcg(a.x + c0 + j) : 0.0;
         xrs[j] = (j < wdt) ? a.xref[c0 + j] : 0.0;
     }
-    for (int64_t t = tid; t < q; t += T) alp[t] = a.alphas[t];
-    // indices of the first D iterations (4-slot ring, written D iterations ahead)
-    for (int64_t u = tid; u < (int64_t)D * q; u += T) {
-        const int64_t it = u / q, t = u % q;
-        if (it < a.count) iring[(it & 3) * q + t] = a.idx[it * q + t];
+    for (int t = tid; t < q; t += NT) alp[t] = a.alphas[t];
+    // row indices: iterations 0..D in the 8-slot ring; D+1 held in registers
+    for (int u = tid; u < (D + 1) * q; u += NT) {
+        const int it = u / q, t = u - it * q;
+        if (it < a.count) iring[(it & 7) * q + t] = a.idx[(int64_t)it * q + t];
+    }
+    int32_t pend[IDX_PER_THREAD];
+#pragma unroll
+    for (int r = 0; r < IDX_PER_THREAD; ++r) {
+        const int t = tid + r * NT;
+        pend[r] = (t < q && D + 1 < a.count) ? a.idx[(int64_t)(D + 1) * q + t] : 0;
+    }
+    if (CLUSTER && tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbarrier_init_cluster();
     }
     __syncthreads();
+    // per-warp pieces of ||x - x_ref||^2 over the slice (combine-step layout)
+    const int jo = lane / NW, w8 = lane % NW;
+    {
+        double e = 0.0;
+        for (int j0 = warp * CPW; j0 < wdt; j0 += NW * CPW) {
+            const int j = j0 + jo;
+            if (w8 == 0 && j < wdt) {
+                const double d = xs[j] - xrs[j];
+                e = fma(d, d, e);
+            }
+        }
+        e = warp_sum(e);
+        if (lane == 0) errw[warp] = e;
+    }
+    __syncthreads();
+    if (CLUSTER) cluster_sync_all();  // peers' mbarriers exist before anyone pushes
 
-    const unsigned np32 = (unsigned)npairs, work = (unsigned)(q * npairs);
+    // cp.async issue: tpr threads per row (power of two), pairs strided by tpr
+    int tpr = 1;
+    while (tpr < npairs && tpr < 32) tpr <<= 1;
+    const int rows_per_pass = NT / tpr, my_r = tid / tpr, my_p = tid % tpr;
+    const bool one_pair = npairs <= tpr;
+    const bool pair_ok = my_p < npairs && 2 * my_p < wdt;
+    const double* Ac0 = a.A + c0 + 2 * my_p;
+    const double2* bs2 = reinterpret_cast<const double2*>(a.bs2);
     auto issue = [&](int64_t it, int st) {
         if (it < a.count) {
-            const int32_t* ir = iring + (it & 3) * q;
-            double* dst = ring + (size_t)st * q * cw;
-            for (unsigned u = tid; u < work; u += T) {
-                const unsigned t = u / np32, pp = u - t * np32;
-                const int64_t col = c0 + 2 * pp;
-                if (col < c1) cp_async16(dst + (size_t)t * cw + 2 * pp, a.A + (int64_t)ir[t] * ld + col);
+            const int32_t* ir = iring + (int)(it & 7) * q;
+            double* dst = ring + st * stage_elems + 2 * my_p;
+            if (one_pair) {
+                if (pair_ok)
+#pragma unroll 4
+                    for (int t = my_r; t < q; t += rows_per_pass)
+                        cp_async16(dst + t * rs, Ac0 + (int64_t)ir[t] * ld);
+            } else {
+                for (int t = my_r; t < q; t += rows_per_pass) {
+                    const double* src = Ac0 + (int64_t)ir[t] * ld;
+                    for (int p = 0; 2 * (my_p + p) < wdt; p += tpr) cp_async16(dst + t * rs + 2 * p, src + 2 * p);
+                }
             }
-            for (int64_t t = tid; t < q; t += T) {
-                cp_async8(bsq + ((size_t)st * q + t) * 2, a.b + ir[t]);
-                cp_async8(bsq + ((size_t)st * q + t) * 2 + 1, a.sq + ir[t]);
-            }
+            for (int t = tid; t < q; t += NT) cp_async16(bq + st * q + t, bs2 + ir[t]);
         }
         cp_async_commit();
     };
+
+    // push layout: lane -> (peer r = lane % P, part = lane / P); each part of a
+    // warp's G_w rows goes to peer r as 16-byte st.async pairs
+    constexpr int G_w = 32 / LPR;                       // rows per warp per round
+    const int parts = (P >= 32) ? 1 : 32 / P;
+    const int vpp = (G_w + parts - 1) / parts;          // rows per lane
+    const int peer = lane % P, part = lane / P;
+    unsigned rin = 0, rbar = 0;
+    if (CLUSTER) {
+        rin = mapa_u32(smem_u32(inbuf), (unsigned)peer);
+        rbar = mapa_u32(smem_u32(bars), (unsigned)peer);
+    }
 
     for (int j = 0; j < D - 1; ++j) issue(j, j);
     int st = 0;  // ring stage of iteration kk
@@ -88,124 +159,205 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
     int conv = 0, checks = 0;
     double err_last = 0.0;
     const double qd = (double)q;
-    const int groups = T / LPR;
+    constexpr int groups = NT / LPR;
     const int g = tid / LPR, gl = tid % LPR;
+    const unsigned xfer_bytes = (unsigned)(P * q1 * sizeof(double));
+    // worker block of this warp for the scale / average steps
+    const int tb = (q * warp) / NW, te = (q * (warp + 1)) / NW, nseg = te - tb;
+    const bool ckpt_on = a.ckpt_every > 0;
+    const bool w8_live = (q * (w8 + 1)) / NW > (q * w8) / NW;
 
     for (int64_t kk = 0;; ++kk) {
         const bool last = (kk == a.count);
         const bool want_check = a.use_stop && (!last || a.final_check);
         if (last && !want_check) break;
-        const double* rows = ring + (size_t)st * q * cw;
-        if (!last) {
-            cp_async_wait_dyn(D - 2);
-        }
-        __syncthreads();  // stage kk visible to all; iteration kk-1 fully retired
+        const int par = (int)(kk & 1);
+        const double* rows = ring + st * stage_elems;
+        if (!last) cp_async_wait_dyn(D - 2);
+        __syncthreads();  // (A) stage kk visible; x, errw of iteration kk-1 complete
+        const bool rec = a.dbg != nullptr && c == 0 && lane == 0 && kk < 32;
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 0] = clock64();
+        if (CLUSTER && tid == 0) mbar_arrive_expect_tx(&bars[par], xfer_bytes);
         if (!last) {
             issue(kk + D - 1, st == 0 ? D - 1 : st - 1);
-            // index ring: iteration kk + D, consumed by issue() one iteration from now
-            const int64_t itn = kk + D;
-            if (itn < a.count)
-                for (int64_t t = tid; t < q; t += T) iring[(itn & 3) * q + t] = a.idx[itn * q + t];
-        }
-        // ---- partial dots over the slice + partial error ---------------------------
-        double* mypart = part + (kk & 1) * (q + 1);
-        double* gpart = a.part + ((size_t)(kk & 1) * P + c) * (q + 1);
-        if (!last) {
-            // rounds of `groups` rows; every lane joins each round's shuffles
-            for (int64_t t0 = 0; t0 < q; t0 += groups) {
-                const int64_t t = t0 + g;
-                double s = 0.0;
-                if (t < q) {
-                    const double* r = rows + t * cw;
-                    for (int64_t j = gl; j < wdt; j += LPR) s = fma(r[j], xs[j], s);
-                }
+            const int64_t itn = kk + D + 1;  // registers -> ring; read by issue() two iterations on
 #pragma unroll
-                for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LPR);
-                if (gl == 0 && t < q) {
-                    if (CLUSTER)
-                        mypart[t] = s;
-                    else
-                        __stcg(gpart + t, s);
+            for (int r = 0; r < IDX_PER_THREAD; ++r) {
+                const int t = tid + r * NT;
+                if (t < q && itn < a.count) {
+                    iring[(int)(itn & 7) * q + t] = pend[r];
+                    if (itn + 1 < a.count) pend[r] = a.idx[(itn + 1) * q + t];
                 }
             }
         }
-        if (tid < 32) {
-            double e = 0.0;
-            if (want_check)
-                for (int64_t j = lane; j < wdt; j += 32) {
-                    const double dd = xs[j] - xrs[j];
-                    e = fma(dd, dd, e);
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 1] = clock64();
+        // ---- partial dots over the slice, pushed to every CTA -----------------------
+        const unsigned my_off = (unsigned)(((par * P + c) * q1p) * (int)sizeof(double));
+        double* gpart = a.part + ((size_t)par * P + c) * q1;
+        for (int t0 = 0; t0 < q; t0 += groups) {  // every lane joins each round's shuffles
+            const int t = t0 + g;
+            double s = 0.0;
+            if (t < q && !last) {
+                const double* r = rows + t * rs;
+#pragma unroll 4
+                for (int j = 2 * gl; j < wdt; j += 2 * LPR) {
+                    const double2 rv = *reinterpret_cast<const double2*>(r + j);
+                    const double2 xv = *reinterpret_cast<const double2*>(xs + j);
+                    s = fma(rv.x, xv.x, s);
+                    s = fma(rv.y, xv.y, s);
                 }
-            e = warp_sum(e);
-            if (lane == 0) {
-                if (CLUSTER)
-                    mypart[q] = e;
-                else
-                    __stcg(gpart + q, e);
+            }
+#pragma unroll
+            for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LPR);
+            if (CLUSTER) {
+                const int wrow0 = t0 + warp * G_w;  // first row of this warp in this round
+#pragma unroll
+                for (int i = 0; i < G_w; i += 2) {
+                    if (i >= vpp) break;
+                    const int ra = part * vpp + i, rb = ra + 1;  // warp-local row numbers
+                    const double va = __shfl_sync(0xffffffffu, s, (ra % G_w) * LPR);
+                    const double vb = __shfl_sync(0xffffffffu, s, (rb % G_w) * LPR);
+                    const int ta = wrow0 + ra;
+                    if (part < parts && ra < G_w && ta < q) {
+                        const unsigned off = my_off + (unsigned)(ta * (int)sizeof(double));
+                        if (i + 1 < vpp && rb < G_w && ta + 1 < q)
+                            st_async_v2_f64(rin + off, va, vb, rbar + 8u * par);
+                        else
+                            st_async_f64(rin + off, va, rbar + 8u * par);
+                    }
+                }
+            } else if (gl == 0 && t < q) {
+                __stcg(gpart + t, s);
             }
         }
+        if (warp == 0) {  // error piece of x_k (pieces written by the previous combine)
+            double e = errw[0];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) e = __dadd_rn(e, errw[w]);
+            if (CLUSTER) {
+                if (lane < P) st_async_f64(rin + my_off + (unsigned)(q * (int)sizeof(double)), e, rbar + 8u * par);
+            } else if (lane == 0) {
+                __stcg(gpart + q, e);
+            }
+        }
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 2] = clock64();
         // ---- exchange -----------------------------------------------------------------
-        if (CLUSTER) {
-            cg::this_cluster().sync();
-        } else {
+        if (CLUSTER)
+            mbar_wait_cluster(&bars[par], (unsigned)((kk >> 1) & 1));
+        else
             grid_barrier(a.barrier, (++epoch) * gridDim.x);
-        }
-        const int64_t nt = last ? 0 : q;
-        for (int64_t t = tid; t <= q; t += T) {
-            if (t < nt || t == q) {
-                double s = 0.0;
-                if (CLUSTER) {
-                    // issue all remote (DSMEM) loads first, then add in CTA order
-                    double pv[16];
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 3] = clock64();
+        auto total = [&](int t) -> double {
+            if (CLUSTER) {
+                const double* ib = inbuf + par * P * q1p + t;
+                double v[MAXP_TREE];
 #pragma unroll
-                    for (int cc = 0; cc < 16; ++cc)
-                        if (cc < P) pv[cc] = cg::this_cluster().map_shared_rank(part, cc)[(kk & 1) * (q + 1) + t];
-                    s = pv[0];
+                for (int cc = 0; cc < MAXP_TREE; ++cc) v[cc] = (cc < P) ? ib[cc * q1p] : 0.0;
 #pragma unroll
-                    for (int cc = 1; cc < 16; ++cc)
-                        if (cc < P) s = __dadd_rn(s, pv[cc]);
-                } else {
-                    const double* gp = a.part + (size_t)(kk & 1) * P * (q + 1) + t;
-                    s = __ldcg(gp);
-                    for (int cc = 1; cc < P; ++cc) s = __dadd_rn(s, __ldcg(gp + (size_t)cc * (q + 1)));
-                }
-                if (t < q) {
-                    const double* bs2 = bsq + ((size_t)st * q + t) * 2;
-                    tot[t] = __ddiv_rn(__dmul_rn(alp[t], __dsub_rn(bs2[0], s)), bs2[1]);
-                } else {
-                    tot[q] = s;
-                }
+                for (int w = 1; w < MAXP_TREE; w <<= 1)
+#pragma unroll
+                    for (int i = 0; i + w < MAXP_TREE; i += 2 * w) v[i] = __dadd_rn(v[i], v[i + w]);
+                return v[0];
             }
+            const double* gp = a.part + (size_t)par * P * q1 + t;
+            double buf[8];
+            double s = 0.0;
+            for (int cc0 = 0; cc0 < P; cc0 += 8) {  // 8 independent loads in flight
+#pragma unroll
+                for (int u = 0; u < 8; ++u) buf[u] = (cc0 + u < P) ? __ldcg(gp + (size_t)(cc0 + u) * q1) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (cc0 + u < P) s = (cc0 + u == 0) ? buf[u] : __dadd_rn(s, buf[u]);
+            }
+            return s;
+        };
+        // ---- scales of this warp's workers; lanes past the block form the error total --
+        double err = 0.0;
+        {
+            const double2* bqs = bq + st * q;
+            const int tA = (lane < nseg) ? tb + lane : q;
+            double vA = 0.0;
+            if (lane < nseg || (want_check && nseg < 32)) vA = total(tA);
+            if (lane < nseg && !last) {
+                const double2 bb = bqs[tA];
+                scal[warp * SEG_MAX + lane] = __ddiv_rn(__dmul_rn(alp[tA], __dsub_rn(bb.x, vA)), bb.y);
+            }
+            if (nseg > 32 && 32 + lane < nseg && !last) {
+                const int tB = tb + 32 + lane;
+                const double2 bb = bqs[tB];
+                scal[warp * SEG_MAX + 32 + lane] = __ddiv_rn(__dmul_rn(alp[tB], __dsub_rn(bb.x, total(tB))), bb.y);
+            }
+            if (want_check) err = (nseg < 32) ? __shfl_sync(0xffffffffu, vA, 31) : total(q);
         }
-        __syncthreads();
         if (want_check) {
             ++checks;
-            err_last = tot[q];
-            if (err_last < a.eps) {
+            err_last = err;
+            if (err < a.eps) {
                 conv = 1;
                 break;
             }
         }
         if (last) break;
         st = (st + 1 == D) ? 0 : st + 1;
-        // ---- ordered average over the q projections (solvers.py:131-137) -------------
-        const int64_t k = a.k0 + kk;
-        const bool ck = a.ckpt_every > 0 && ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;
-        const int64_t slot = ck ? (k + 1) / a.ckpt_every - 1 : 0;
-        for (int64_t j = tid; j < wdt; j += T) {
-            const double xj = xs[j];
-            double acc = __dadd_rn(xj, __dmul_rn(tot[0], rows[j]));
-            for (int64_t t = 1; t < q; ++t) acc = __dadd_rn(acc, __dadd_rn(xj, __dmul_rn(tot[t], rows[t * cw + j])));
-            const double xn = __ddiv_rn(acc, qd);
-            xs[j] = xn;
-            if (ck && c0 + j < a.n) a.ckpt[slot * a.n + c0 + j] = xn;
+        __syncwarp();
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 4] = clock64();
+        // ---- average over the q projections (solvers.py:131-137) ----------------------
+        {
+            const double* sw = scal + warp * SEG_MAX;
+            for (int j0 = 0; j0 < wdt; j0 += 32) {
+                const int j = j0 + lane;
+                const int jj = j < wdt ? j : 0;
+                const double xj = xs[jj];
+                const double* rj = rows + tb * rs + jj;
+                double acc = 0.0;
+                int u = 0;
+                for (; u + 2 <= nseg; u += 2) {
+                    const double2 s2 = *reinterpret_cast<const double2*>(sw + u);
+                    const double v0 = __dadd_rn(xj, __dmul_rn(s2.x, rj[u * rs]));
+                    const double v1 = __dadd_rn(xj, __dmul_rn(s2.y, rj[(u + 1) * rs]));
+                    acc = (u == 0) ? __dadd_rn(v0, v1) : __dadd_rn(__dadd_rn(acc, v0), v1);
+                }
+                if (u < nseg) {
+                    const double v = __dadd_rn(xj, __dmul_rn(sw[u], rj[u * rs]));
+                    acc = (u == 0) ? v : __dadd_rn(acc, v);
+                }
+                if (j < wdt) upd[warp * cw + j] = acc;
+            }
         }
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 5] = clock64();
+        __syncthreads();  // (B) per-warp sums complete
+        {
+            const int64_t k = a.k0 + kk;
+            bool ck = false;
+            int64_t slot = 0;
+            if (ckpt_on) {
+                ck = ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;
+                slot = (k + 1) / a.ckpt_every - 1;
+            }
+            double e = 0.0;
+            for (int j0 = warp * CPW; j0 < wdt; j0 += NW * CPW) {
+                const int j = j0 + jo;
+                double v = (w8_live && j < wdt) ? upd[w8 * cw + j] : 0.0;
+#pragma unroll
+                for (int o = NW / 2; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o, NW));
+                if (w8 == 0 && j < wdt) {
+                    const double xn = __ddiv_rn(v, qd);
+                    xs[j] = xn;
+                    const double d = xn - xrs[j];
+                    e = fma(d, d, e);
+                    if (ck && c0 + j < a.n) a.ckpt[slot * a.n + c0 + j] = xn;
+                }
+            }
+            e = warp_sum(e);
+            if (lane == 0) errw[warp] = e;
+        }
+        if (rec) a.dbg[(kk * 8 + warp) * 8 + 6] = clock64();
         done = kk + 1;
     }
     cp_async_wait<0>();
     __syncthreads();
-    for (int64_t j = tid; j < wdt; j += T) __stcg(a.x + c0 + j, xs[j]);
-    if (CLUSTER) cg::this_cluster().sync();  // peers may still read our partials
+    for (int j = tid; j < wdt; j += NT) __stcg(a.x + c0 + j, xs[j]);
+    if (CLUSTER) cluster_sync_all();  // no DSMEM traffic may target an exited CTA
     if (c == 0 && tid == 0) {
         a.status->iters_done = done;
         a.status->converged = conv;
@@ -214,8 +366,10 @@ __global__ void __launch_bounds__(256) sync_kernel(SolveArgs a) {
     }
 }
 
+template __global__ void sync_kernel<true, 4>(SolveArgs);
 template __global__ void sync_kernel<true, 8>(SolveArgs);
 template __global__ void sync_kernel<true, 32>(SolveArgs);
+template __global__ void sync_kernel<false, 4>(SolveArgs);
 template __global__ void sync_kernel<false, 8>(SolveArgs);
 template __global__ void sync_kernel<false, 32>(SolveArgs);
 

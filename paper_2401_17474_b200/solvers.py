@@ -54,6 +54,8 @@ class SolverConfig:
     engine: str = "b200"
     kernel: str = "auto"
     device: int = 0
+    threads: int = 0  # CTA size override (0 = auto)
+    ctas: int = 0     # CTA count override for the sync kernels (0 = auto)
 
     def validate(self) -> None:
         if self.variant not in VARIANTS:
@@ -306,6 +308,8 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
             ck_buf = np.empty((max(cap, 1), ds.n))
             p.ckpt_every, p.ckpt_capacity, p.ckpt_host = every, cap, N.ptr(ck_buf)
         p.kernel = N.KERNELS[cfg.kernel]
+        p.threads = int(cfg.threads)
+        p.ctas = int(cfg.ctas)
         p.want_residual = 1
         r = N.Result()
         x = np.empty(ds.n)

@@ -20,11 +20,12 @@ def main():
     ap.add_argument("--kernel", default="auto")
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--ctas", type=int, default=0)
     args = ap.parse_args()
     from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver
 
     system, kw = build_system(args.workload)
-    cfg = SolverConfig(kernel=args.kernel, **kw)
+    cfg = SolverConfig(kernel=args.kernel, threads=args.threads, ctas=args.ctas, **kw)
     with DeviceSystem(system) as ds:
         run_solver(ds, cfg, budget=args.budget)
         for s in range(args.solves):
