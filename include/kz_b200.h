@@ -100,6 +100,14 @@ KZ_API int32_t kz_sampler_build(kz_system* sys, int32_t scheme, int64_t q, doubl
 KZ_API int32_t kz_dump_rows(kz_system* sys, int32_t scheme, int64_t q, uint64_t base_seed, int64_t worker,
                      int64_t start, int64_t count, int32_t* out_host, void* stream);
 
+/* Explicit per-worker support ranges [lo_t, lo_t + len_t) (row shards: the
+ * reference's distributed scheme restricted to this device's rows,
+ * partition_bounds(m, Q, t) shifted by the shard offset).  Selected with
+ * scheme = KZ_SCHEME_RANGES. */
+#define KZ_SCHEME_RANGES 2
+KZ_API int32_t kz_sampler_set_ranges(kz_system* sys, int64_t q, const int64_t* lo_host, const int64_t* len_host,
+                                     void* stream);
+
 /* ---- solve: solve_rk / solve_rka_seq / solve_rkab_seq via _drive
  * (solvers.py:182-263, 294-371) ---------------------------------------- */
 typedef struct {
@@ -121,6 +129,13 @@ typedef struct {
     int32_t threads;        /* CTA size override (0 = auto)                                    */
     int32_t ctas;           /* CTA count override for sync kernels (0 = auto)                  */
     int32_t want_residual;  /* compute ||Ax - b|| at the end of a stop-mode run                */
+    /* row-sharded (multi-GPU) operation, see kz_average_from / kz_sampler_set_ranges: */
+    int64_t worker_offset;  /* stream id of local worker 0: worker t draws from Prng(seed, offset+t) */
+    int64_t k_start;        /* index of the first iteration (row-draw offset k_start * block_size)   */
+    int32_t keep_x;         /* start from the resident iterate instead of x0 = 0                     */
+    int32_t pad0;
+    double* partial_dev;    /* non-NULL: run ONE iteration and write the un-normalised worker sum   */
+                            /* S = sum_t v_t (n values, device) instead of updating x                */
 } kz_params;
 
 typedef struct {
@@ -142,8 +157,17 @@ typedef struct {
 
 /* Full solve with host output x_host (n values, may be NULL). */
 KZ_API int32_t kz_solve(kz_system* sys, const kz_params* params, kz_result* result, double* x_host, void* stream);
+/* Resident iterate: copy out (n values) / overwrite (NULL = zeros). */
+KZ_API int32_t kz_solution_host(kz_system* sys, double* x_host, void* stream);
+KZ_API int32_t kz_set_x(kz_system* sys, const double* x_host, void* stream);
 /* Device pointer of the final iterate of the last kz_solve on this system (n values). */
 KZ_API int32_t kz_solution_device(kz_system* sys, double** x_dev);
+
+/* x = S / Q from a (reduced) worker sum S (device), then ||x - x_ref||^2 -> *err_host.
+ * The closing half of one row-sharded iteration (distributed.py:296-301). */
+KZ_API int32_t kz_average_from(kz_system* sys, const double* S_dev, int64_t Q, double* err_host, void* stream);
+/* ||x - x_ref||^2 of the resident iterate (deterministic, identical on every rank). */
+KZ_API int32_t kz_error_sq(kz_system* sys, double* err_host, void* stream);
 
 /* ---- norms used by traces and reports (solvers.py:174-179, 246) ---------- */
 /* ||A x - b||_2 and ||x - x_ref||_2 for a host x (n values). */

@@ -22,14 +22,15 @@ KZ_OK, KZ_EINVAL, KZ_EDEGENERATE, KZ_EEMPTYRANGE, KZ_ENOMEM, KZ_ECUDA, KZ_ENODEV
 KERNELS = {"auto": 0, "chain": 1, "sync_cluster": 2, "sync_grid": 3}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 VARIANT_IDS = {"rk": 0, "rka": 1, "rkab": 2}
-SCHEME_IDS = {"full_access": 0, "distributed": 1}
+SCHEME_IDS = {"full_access": 0, "distributed": 1, "ranges": 2}
 
 # Every symbol include/kz_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "kz_last_error", "kz_version", "kz_launch_count", "kz_device_count",
     "kz_system_create", "kz_system_destroy", "kz_system_pitch", "kz_system_upload",
     "kz_system_upload_device", "kz_system_device_ptrs", "kz_system_set_xref", "kz_system_touch",
-    "kz_row_norms", "kz_sampler_build", "kz_dump_rows", "kz_solve", "kz_solution_device", "kz_norms",
+    "kz_row_norms", "kz_sampler_build", "kz_sampler_set_ranges", "kz_dump_rows", "kz_solve",
+    "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
 )
 
 
@@ -61,6 +62,11 @@ class Params(C.Structure):
         ("threads", C.c_int32),
         ("ctas", C.c_int32),
         ("want_residual", C.c_int32),
+        ("worker_offset", C.c_int64),
+        ("k_start", C.c_int64),
+        ("keep_x", C.c_int32),
+        ("pad0", C.c_int32),
+        ("partial_dev", C.c_void_p),
     ]
 
 
@@ -118,6 +124,11 @@ def load_library():
                                    C.POINTER(C.c_int32), vp]
         L.kz_solve.argtypes = [vp, C.POINTER(Params), C.POINTER(Result), _dp, vp]
         L.kz_solution_device.argtypes = [vp, C.POINTER(vp)]
+        L.kz_sampler_set_ranges.argtypes = [vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64), vp]
+        L.kz_average_from.argtypes = [vp, vp, C.c_int64, _dp, vp]
+        L.kz_error_sq.argtypes = [vp, _dp, vp]
+        L.kz_solution_host.argtypes = [vp, _dp, vp]
+        L.kz_set_x.argtypes = [vp, _dp, vp]
         L.kz_norms.argtypes = [vp, _dp, _dp, _dp, vp]
         for name in EXPORTS:
             fn = getattr(L, name)

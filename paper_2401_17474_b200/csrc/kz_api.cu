@@ -171,6 +171,7 @@ struct kz_system {
     int64_t bad_row = -1;
     int sampler_scheme = -1;
     int64_t sampler_q = 0;
+    std::vector<int64_t> custom_lo, custom_len;  // KZ_SCHEME_RANGES
     bool has_xref = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
@@ -354,7 +355,10 @@ extern "C" int32_t kz_row_norms(kz_system* s, double* sq_host, int64_t* bad_row,
 // ---------------------------------------------------------------------------
 static int ensure_sampler(kz_system* s, int scheme, int64_t q, cudaStream_t st) {
     KZ_TRY(ensure_norms(s, st));
-    if (scheme != KZ_FULL_ACCESS && scheme != KZ_DISTRIBUTED) return fail(KZ_EINVAL, "unknown sampling scheme %d", scheme);
+    if (scheme != KZ_FULL_ACCESS && scheme != KZ_DISTRIBUTED && scheme != KZ_SCHEME_RANGES)
+        return fail(KZ_EINVAL, "unknown sampling scheme %d", scheme);
+    if (scheme == KZ_SCHEME_RANGES && (int64_t)s->custom_lo.size() != q)
+        return fail(KZ_EINVAL, "explicit ranges were set for %zu workers, not q=%lld", s->custom_lo.size(), (long long)q);
     if (q < 1) return fail(KZ_EINVAL, "q must be >= 1, got %lld", (long long)q);
     if (s->sampler_scheme == scheme && (scheme == KZ_FULL_ACCESS || s->sampler_q == q)) {
         if (scheme == KZ_FULL_ACCESS && s->sampler_q != q) {
@@ -375,6 +379,10 @@ static int ensure_sampler(kz_system* s, int scheme, int64_t q, cudaStream_t st) 
         std::fill(lo.begin(), lo.end(), 0);
         std::fill(len.begin(), len.end(), s->m);
         nranges = 1;
+    } else if (scheme == KZ_SCHEME_RANGES) {
+        lo = s->custom_lo;
+        len = s->custom_len;
+        nranges = q;
     } else {
         for (int64_t t = 0; t < q; ++t) {
             const int64_t a = (t * s->m) / q, b = ((t + 1) * s->m) / q - 1;
@@ -400,6 +408,20 @@ static int ensure_sampler(kz_system* s, int scheme, int64_t q, cudaStream_t st) 
     KZ_CUDA(cudaStreamSynchronize(st));
     s->sampler_scheme = scheme;
     s->sampler_q = q;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_sampler_set_ranges(kz_system* s, int64_t q, const int64_t* lo, const int64_t* len, void* stream) {
+    if (!s || !lo || !len || q < 1) return fail(KZ_EINVAL, "bad ranges");
+    std::vector<int64_t> l(lo, lo + q), n(len, len + q);
+    for (int64_t t = 0; t < q; ++t)
+        if (n[t] < 1 || l[t] < 0 || l[t] + n[t] > s->m)
+            return fail(KZ_EEMPTYRANGE, "row range [%lld, %lld) invalid for m=%lld", (long long)l[t],
+                        (long long)(l[t] + n[t]), (long long)s->m);
+    s->custom_lo = l;
+    s->custom_len = n;
+    if (s->sampler_scheme == KZ_SCHEME_RANGES) s->sampler_scheme = -1;
+    (void)stream;
     return KZ_OK;
 }
 
@@ -481,6 +503,53 @@ extern "C" int32_t kz_norms(kz_system* s, const double* x_host, double* residual
     KZ_CUDA(cudaMemsetAsync(s->V.p, 0, s->ld * sizeof(double), st));
     KZ_CUDA(cudaMemcpyAsync(s->V.p, x_host, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
     return device_norms(s, s->V.p, residual, error, st);
+}
+
+static int error_sq_dev(kz_system* s, double* out, cudaStream_t st) {
+    KZ_TRY(s->part.ensure(16));
+    diff_sq_kernel<<<(unsigned)((s->n + 255) / 256), 256, 0, st>>>(s->x.p, s->xref.p, s->n, s->tmp.p);
+    KZ_TRY(check_launch("diff_sq_kernel"));
+    sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->n, s->part.p);
+    KZ_TRY(check_launch("sum_kernel"));
+    KZ_CUDA(cudaMemcpyAsync(out, s->part.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_error_sq(kz_system* s, double* err_host, void* stream) {
+    if (!s || !err_host) return fail(KZ_EINVAL, "null argument");
+    KZ_CUDA(cudaSetDevice(s->device));
+    return error_sq_dev(s, err_host, (cudaStream_t)stream);
+}
+
+extern "C" int32_t kz_average_from(kz_system* s, const double* S_dev, int64_t Q, double* err_host, void* stream) {
+    if (!s || !S_dev || Q < 1) return fail(KZ_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    scale_copy_kernel<<<(unsigned)((s->ld + 255) / 256), 256, 0, st>>>(S_dev, (double)Q, s->ld, s->x.p);
+    KZ_TRY(check_launch("scale_copy_kernel"));
+    if (err_host) return error_sq_dev(s, err_host, st);
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_solution_host(kz_system* s, double* x_host, void* stream) {
+    if (!s || !x_host) return fail(KZ_EINVAL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_set_x(kz_system* s, const double* x_host, void* stream) {
+    if (!s) return fail(KZ_EINVAL, "null system");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
+    if (x_host) KZ_CUDA(cudaMemcpyAsync(s->x.p, x_host, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
 }
 
 extern "C" int32_t kz_solution_device(kz_system* s, double** x_dev) {
@@ -719,14 +788,17 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         s->bs2_valid = true;
     }
     std::vector<PcgPod> pods(q);
-    for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)t);
+    for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)(p->worker_offset + t));
     KZ_TRY(s->states.ensure(q));
     KZ_CUDA(cudaMemcpyAsync(s->states.p, pods.data(), q * sizeof(PcgPod), cudaMemcpyHostToDevice, st));
     std::vector<double> al(q, 1.0);
     if (p->alphas_host) std::copy(p->alphas_host, p->alphas_host + q, al.begin());
     KZ_TRY(s->alphas.ensure(q));
     KZ_CUDA(cudaMemcpyAsync(s->alphas.p, al.data(), q * sizeof(double), cudaMemcpyHostToDevice, st));
-    KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
+    if (!p->keep_x) KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
+    const bool partial_mode = p->partial_dev != nullptr;
+    if (partial_mode && !(budget_mode && p->budget == 1))
+        return fail(KZ_EINVAL, "partial (row-sharded) steps run exactly one iteration: set budget = 1");
 
     // --- kernel plan ---
     Plan pl;
@@ -771,6 +843,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.bs2 = s->bs2.p;
     args.xref = s->xref.p;
     args.x = s->x.p;
+    args.partial = p->partial_dev;
     args.V = s->V.p;
     args.idx = s->idx.p;
     args.alphas = s->alphas.p;
@@ -824,11 +897,13 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         if (c > 0) {
             const int64_t count = c * bs;
             if (pl.kernel == KZ_KERNEL_CHAIN)
-                KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, k * bs, count, s->idx.p, count, 1, st));
+                KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, (p->k_start + k) * bs, count, s->idx.p,
+                                      count, 1, st));
             else
-                KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, k * bs, count, s->idx.p, 1, q, st));
+                KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, (p->k_start + k) * bs, count, s->idx.p, 1,
+                                      q, st));
         }
-        args.k0 = k;
+        args.k0 = p->k_start + k;
         args.count = c;
         args.idx_stride = c * bs;
         args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;

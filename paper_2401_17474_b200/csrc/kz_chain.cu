@@ -232,6 +232,10 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             for (int64_t col = c0 + tid; col < c1; col += T) {
                 double acc = __ldcg(a.V + col);
                 for (int64_t t = 1; t < q; ++t) acc = __dadd_rn(acc, __ldcg(a.V + t * ld + col));
+                if (a.partial) {  // row-sharded step: the un-normalised local sum, x untouched
+                    __stcg(a.partial + col, acc);
+                    continue;
+                }
                 const double xn = __ddiv_rn(acc, inv_q_d);
                 __stcg(a.x + col, xn);
                 if (ck && col < a.n) a.ckpt[slot * a.n + col] = xn;
@@ -252,10 +256,11 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
 finish:
     cp_async_wait<0>();
     if (q == 1) {
+        double* dst = a.partial ? a.partial : a.x;
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
             const int64_t col = 2 * ((int64_t)p * T + tid);
-            if (col < ld) __stcg(reinterpret_cast<double2*>(a.x + col), make_double2(v[2 * p], v[2 * p + 1]));
+            if (col < ld) __stcg(reinterpret_cast<double2*>(dst + col), make_double2(v[2 * p], v[2 * p + 1]));
         }
     }
     if (blockIdx.x == 0 && tid == 0) {

@@ -21,6 +21,7 @@ struct SolveArgs {
     const double* bs2;     // m x 2 packed (b_i, sq_i)
     const double* xref;    // ld (zero padded)
     double* x;             // ld, the iterate (in/out)
+    double* partial;       // non-null: one iteration, write sum_t v_t here instead of x
     double* V;             // q x ld worker estimates (chain kernel, q > 1)
     const int32_t* idx;    // row indices of this chunk (layout per kernel)
     const double* alphas;  // q row weights
@@ -67,6 +68,7 @@ __global__ void diff_sq_kernel(const double* __restrict__ x, const double* __res
                                double* __restrict__ out);
 __global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __restrict__ sq, int64_t m,
                                 double* __restrict__ out);
+__global__ void scale_copy_kernel(const double* __restrict__ S, double inv_div, int64_t n, double* __restrict__ x);
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
 
 constexpr int NORM_ROWS_PER_CTA = 128;

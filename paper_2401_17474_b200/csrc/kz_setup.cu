@@ -212,6 +212,12 @@ __global__ void diff_sq_kernel(const double* __restrict__ x, const double* __res
     }
 }
 
+// x = S / Q (IEEE division by the worker count, solvers.py:137 / distributed.py:300)
+__global__ void scale_copy_kernel(const double* __restrict__ S, double div, int64_t n, double* __restrict__ x) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) x[j] = __ddiv_rn(S[j], div);
+}
+
 // (b_i, ||a_i||^2) packed for one 16-byte copy per sampled row
 __global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __restrict__ sq, int64_t m,
                                 double* __restrict__ out) {

@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
                 double v = (w8_live && j < wdt) ? upd[w8 * cw + j] : 0.0;
 #pragma unroll
                 for (int o = NW / 2; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o, NW));
-                if (w8 == 0 && j < wdt) {
+                if (w8 == 0 && j < wdt && a.partial) {  // row-sharded step: un-normalised local sum
+                    __stcg(a.partial + c0 + j, v);
+                } else if (w8 == 0 && j < wdt) {
                     const double xn = __ddiv_rn(v, qd);
                     xs[j] = xn;
                     const double d = xn - xrs[j];
@@ -356,7 +358,8 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();
-    for (int j = tid; j < wdt; j += NT) __stcg(a.x + c0 + j, xs[j]);
+    if (!a.partial)
+        for (int j = tid; j < wdt; j += NT) __stcg(a.x + c0 + j, xs[j]);
     if (CLUSTER) cluster_sync_all();  // no DSMEM traffic may target an exited CTA
     if (c == 0 && tid == 0) {
         a.status->iters_done = done;

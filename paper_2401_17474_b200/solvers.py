@@ -174,6 +174,62 @@ class DeviceSystem:
                                        int(start), int(count), out.ctypes.data_as(C.POINTER(C.c_int32)), None))
         return out
 
+    # -- row-sharded (multi-GPU) primitives -------------------------------------
+    def set_ranges(self, lo, length) -> None:
+        """Explicit per-worker support ranges (sampling scheme "ranges")."""
+        lo = np.ascontiguousarray(lo, dtype=np.int64)
+        ln = np.ascontiguousarray(length, dtype=np.int64)
+        N.check(self._lib.kz_sampler_set_ranges(self.handle, len(lo), lo.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                ln.ctypes.data_as(C.POINTER(C.c_int64)), None))
+
+    def error_sq(self) -> float:
+        """||x - x_ref||^2 of the resident iterate."""
+        out = C.c_double()
+        N.check(self._lib.kz_error_sq(self.handle, C.byref(out), None))
+        return out.value
+
+    def average_from(self, S_ptr: int, Q: int) -> float:
+        """x = S / Q from a reduced worker sum (device pointer); returns ||x - x_ref||^2."""
+        out = C.c_double()
+        N.check(self._lib.kz_average_from(self.handle, C.c_void_p(S_ptr), int(Q), C.byref(out), None))
+        return out.value
+
+    def local_step(self, cfg: "SolverConfig", *, k: int, worker_offset: int, partial_ptr: int,
+                   alphas=None) -> dict:
+        """One iteration of this shard's workers from the resident x; writes the
+        un-normalised worker sum S = sum_t v_t to `partial_ptr` (device)."""
+        variant = cfg.variant
+        q = 1 if variant == "rk" else cfg.q
+        al = N.f64(np.ones(q) if alphas is None else alphas)
+        p = N.Params()
+        p.variant = N.VARIANT_IDS[variant]
+        p.scheme = N.SCHEME_IDS["ranges"]
+        p.q = q
+        p.block_size = cfg.block_size if variant == "rkab" else 1
+        p.alphas_host = N.ptr(al)
+        p.base_seed = int(cfg.base_seed)
+        p.epsilon = float(cfg.epsilon)
+        p.max_iterations = int(cfg.max_iterations)
+        p.budget = 1
+        p.kernel = N.KERNELS[cfg.kernel]
+        p.threads, p.ctas = int(cfg.threads), int(cfg.ctas)
+        p.worker_offset, p.k_start, p.keep_x = int(worker_offset), int(k), 1
+        p.partial_dev = C.c_void_p(partial_ptr)
+        r = N.Result()
+        N.check(self._lib.kz_solve(self.handle, C.byref(p), C.byref(r), None, None))
+        return {"kernel_ms": float(r.kernel_ms), "loop_ms": float(r.loop_ms), "rows": int(r.rows_projected),
+                "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches)}
+
+    def set_x(self, x=None) -> None:
+        """Overwrite the resident iterate (None = zeros)."""
+        xv = None if x is None else N.f64(x)
+        N.check(self._lib.kz_set_x(self.handle, N.ptr(xv) if xv is not None else None, None))
+
+    def x_host(self) -> np.ndarray:
+        out = np.empty(self.n)
+        N.check(self._lib.kz_solution_host(self.handle, N.ptr(out), None))
+        return out
+
     def norms(self, x) -> tuple[float, float]:
         """(||A x - b||, ||x - x_ref||) on the device."""
         xv = N.f64(x)

@@ -1,0 +1,67 @@
+"""Row-sharded (multi-GPU) path on one B200: the partial-sum local step,
+explicit shard ranges and x = S/Q, for world 1 through the production driver
+and for 2 and 4 emulated ranks in one process (each rank's local step is an
+independent kernel; the all-reduce is the host sum of the ranks' S, which is
+what NCCL's sum returns), against the sequential oracle with q_total workers
+and the distributed scheme."""
+
+import numpy as np
+import pytest
+
+from conftest import PARITY_TOL, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _system():
+    from paper_2401_17474_b200 import GeneratorConfig, generate_mother
+
+    return generate_mother(GeneratorConfig(m_max=4000, n_max=64, seed=5))
+
+
+def test_world1_driver(gpu, oracle):
+    from paper_2401_17474_b200 import SolverConfig
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded
+
+    s = _system()
+    for variant, q, bs in (("rka", 8, 1), ("rkab", 4, 6)):
+        plan = plan_shards(s.m, 1, 0, q)
+        shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
+        cfg = SolverConfig(variant=variant, q=q, block_size=bs, base_seed=2, sampling_scheme="distributed")
+        r = solve_sharded(shard, cfg)
+        shard.close()
+        o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=q, block_size=bs, base_seed=2, scheme="distributed")
+        assert r.converged and r.iterations == o["iterations"] and r.error_evals == o["error_evals"]
+        assert rel_err(r.x, o["x"]) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("variant,bs", [("rka", 1), ("rkab", 5)])
+def test_emulated_ranks_one_gpu(gpu, oracle, world, variant, bs):
+    from paper_2401_17474_b200 import SolverConfig
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards
+
+    s = _system()
+    q_local, budget = 4, 60
+    cfg = SolverConfig(variant=variant, q=q_local, block_size=bs, base_seed=7, sampling_scheme="distributed")
+    shards = []
+    for g in range(world):
+        p = plan_shards(s.m, world, g, q_local)
+        shards.append(CudaShard(s.A[p.lo:p.hi + 1], s.b[p.lo:p.hi + 1], s.x_star, p, device=0))
+    for sh in shards:
+        sh.reset()
+    for k in range(budget):
+        S = [sh.step(cfg, k) for sh in shards]
+        tot = S[0].clone()
+        for extra in S[1:]:
+            tot += extra
+        errs = [sh.finish(tot, world * q_local) for sh in shards]
+        assert len(set(errs)) == 1
+    xs = [sh.x() for sh in shards]
+    for sh in shards:
+        sh.close()
+    for x in xs[1:]:
+        assert np.array_equal(x, xs[0])
+    o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=world * q_local, block_size=bs, base_seed=7,
+                     scheme="distributed", budget=budget)
+    assert rel_err(xs[0], o["x"]) <= PARITY_TOL
