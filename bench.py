@@ -172,7 +172,77 @@ def cpu_baseline(name, system, kw, budget_s=12.0):
             "sample": f"{seeds} full solves to eps (seeds 0..{seeds - 1}) of {name}, oracle/kz_oracle.c pthreads"}
 
 
+def run_b200_sharded(args, name, rank, world, local_rank):
+    """N > 1: weak scaling -- every GPU holds a workload-sized row shard of an
+    (m*N) x n system and runs q workers on it; one NCCL all-reduce of the
+    worker sums per outer iteration (multigpu.solve_sharded)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_17474_b200 import GeneratorConfig, SolverConfig, generate_mother
+    from paper_2401_17474_b200 import _native as N
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded
+
+    torch.cuda.set_device(local_rank)
+    m1, n, kw, desc = WORKLOADS[name]
+    m = m1 * world
+    system = generate_mother(GeneratorConfig(m_max=m, n_max=n, seed=0))
+    q_local = kw.get("q", 1)
+    plan = plan_shards(m, world, rank, q_local)
+    cfg = SolverConfig(device=local_rank, sampling_scheme="distributed", **kw)
+    shard = CudaShard(system.A[plan.lo:plan.hi + 1], system.b[plan.lo:plan.hi + 1], system.x_star, plan, local_rank)
+    for w in range(args.warmup):
+        solve_sharded(shard, cfg.replace(base_seed=w % 10))
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = N.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rows, iters = 0, []
+    rows0 = shard.rows
+    with ClockSampler(local_rank) as clk:
+        ev0.record()
+        for k in range(args.steps):
+            r = solve_sharded(shard, cfg.replace(base_seed=k % 10))
+            iters.append(r.iterations)
+        ev1.record()
+        torch.cuda.synchronize()
+    rows = shard.rows - rows0
+    t_ms = ev0.elapsed_time(ev1)
+    tt = torch.tensor([t_ms], device=f"cuda:{local_rank}")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    tot_rows = torch.tensor([float(rows)], device=f"cuda:{local_rank}")
+    dist.all_reduce(tot_rows, op=dist.ReduceOp.SUM)
+    dist.barrier()
+    launches = N.launch_count() - launches0
+    shard.close()
+    if rank != 0:
+        return
+    peak, peak_src = read_peak()
+    value = float(tot_rows.item()) / (t_ms / 1e3)
+    achieved = value / world * 8 * n / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0)",
+        "config": {"workload": desc + f", rows x{world} sharded", "m": m, "n": n, **kw, "q_per_gpu": q_local,
+                   "sampling_scheme": "distributed", "parallelism": f"row shards x{world}, NCCL all-reduce / iteration",
+                   "seeds": "0..9 cycling"},
+        "iterations": iters,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_source": peak_src, "algorithmic_bytes": "8*n per row projection",
+                     "note": "per-GPU rate over the whole step (kernels + all-reduce + host loop)"},
+        "clocks": clk.summary(),
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * n,
+                "note": "shard resident; per-iteration host loop included"},
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_b200(args, name, rank, world, local_rank):
+    if world > 1:
+        return run_b200_sharded(args, name, rank, world, local_rank)
     import torch
     import torch.distributed as dist
 

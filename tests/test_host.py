@@ -1,0 +1,110 @@
+"""Host-side logic on CPU: configuration validation, partitions, report CSV
+schema, and the package's restatement of the reference generator (bitwise
+against tests/golden/systems.npz)."""
+
+import io
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+
+def test_solver_config_validation():
+    from paper_2401_17474_b200 import SolverConfig
+
+    SolverConfig().validate()
+    for bad in (dict(variant="nope"), dict(alpha_policy="x"), dict(sampling_scheme="x"), dict(engine="x"),
+                dict(kernel="x"), dict(q=0), dict(block_size=0), dict(epsilon=0.0), dict(max_iterations=0)):
+        with pytest.raises(ValueError):
+            SolverConfig(**bad).validate()
+    c = SolverConfig(variant="rka", q=4)
+    assert c.replace(q=8).q == 8 and c.q == 4
+
+
+def test_partition_bounds():
+    from paper_2401_17474_b200 import EmptyRangeError, partition_bounds
+
+    for m, q in ((10, 3), (2000, 64), (7, 7)):
+        rows = []
+        for t in range(q):
+            lo, hi = partition_bounds(m, q, t)
+            rows.extend(range(lo, hi + 1))
+        assert rows == list(range(m))
+    with pytest.raises(EmptyRangeError):
+        partition_bounds(3, 4, 0)
+    with pytest.raises(EmptyRangeError):
+        partition_bounds(10, 2, 2)
+
+
+def test_report_csv_roundtrip():
+    from paper_2401_17474_b200.reports import (REPORT_HEADER, RunReport, TraceRecord, format_report_csv,
+                                              read_report_csv, read_trace_csv, trace_row, write_csv)
+
+    r = RunReport("rka", 64, 1, "unit", 1.0, 3, 9431, True, 0.0123456789, 9.87e-9, 1.5e-5)
+    text = format_report_csv([("run", r), ("summary", r)])
+    assert text.splitlines()[0].split(",") == REPORT_HEADER
+    back = read_report_csv(io.StringIO(text))
+    assert back[0][0] == "run" and back[0][1].iterations == 9431 and back[0][1].wall_time_s == 0.0123456789
+    buf = io.StringIO()
+    write_csv(buf, ["iteration", "error_norm", "residual_norm"], [trace_row(TraceRecord(5, 0.5, 1.25))])
+    buf.seek(0)
+    assert read_trace_csv(buf)[0] == TraceRecord(5, 0.5, 1.25)
+
+
+def test_generator_restatement_is_bitwise(systems):
+    from golden.common import sha
+
+    from paper_2401_17474_b200 import crop, make_inconsistent
+
+    g = golden("systems.npz")
+    for name in ("c0", "s500", "s2000"):
+        s = systems[name]
+        assert sha(s.A) == str(g[f"{name}_A"]) and sha(s.b) == str(g[f"{name}_b"])
+        assert sha(s.x_star) == str(g[f"{name}_xref"])
+    c = crop(systems["s2000"], 300, 40)
+    assert sha(c.A) == str(g["crop300x40_A"]) and sha(c.b) == str(g["crop300x40_b"])
+    assert sha(c.x_star) == str(g["crop300x40_xref"])
+    inc = make_inconsistent(systems["s2000"], noise_seed=11)
+    assert sha(inc.b) == str(g["inc2000_b"])
+    ref = g["inc2000_xls"]
+    assert np.max(np.abs(inc.x_ls - ref)) <= 1e-8 * np.max(np.abs(ref))
+
+
+def test_generator_c1_shape_is_bitwise(c1_system):
+    from golden.common import sha
+
+    g = golden("systems.npz")
+    assert sha(c1_system.A) == str(g["c1_A"]) and sha(c1_system.x_star) == str(g["c1_xref"])
+
+
+def test_generator_validation():
+    from paper_2401_17474_b200 import DimensionMismatchError, GeneratorConfig, generate_mother
+
+    with pytest.raises(DimensionMismatchError):
+        generate_mother(GeneratorConfig(m_max=5, n_max=10))
+    with pytest.raises(ValueError):
+        generate_mother(GeneratorConfig(sigma_range=(0.0, 1.0)))
+
+
+def test_harness_helpers():
+    from paper_2401_17474_b200 import Protocol, TraceRecord, plateau_error
+
+    recs = [TraceRecord(i, float(i), 0.0) for i in range(12)]
+    assert plateau_error(recs) == pytest.approx(np.mean(range(2, 12)))
+    with pytest.raises(ValueError):
+        plateau_error(recs[:5])
+    with pytest.raises(ValueError):
+        Protocol(n_seeds=0).validate()
+
+
+def test_spectral_alpha_formula():
+    from paper_2401_17474_b200.spectral import SpectralStats, optimal_alpha, spectral_stats
+
+    assert optimal_alpha(SpectralStats(1, 1, s_min=0.3, s_max=0.9), 1) == 1.0
+    assert abs(optimal_alpha(SpectralStats(1, 1, s_min=0.5, s_max=0.5), 2) - 4 / 3) <= 1e-12
+    assert abs(optimal_alpha(SpectralStats(1, 1, s_min=0.1, s_max=0.9), 3) - 2.0) <= 1e-12
+    st = spectral_stats(np.diag([1.0, 2.0, 3.0]))
+    assert abs(st.s_max - 9 / 14) <= 1e-5 and abs(st.s_min - 1 / 14) <= 1e-5
+    assert math.isfinite(st.sigma_min)
