@@ -565,6 +565,7 @@ namespace {
 
 struct Plan {
     int kernel = KZ_KERNEL_CHAIN;
+    int rows = 1;       // chain: rows per CTA reduction (R)
     int threads = 256;
     int ctas = 1;
     int stages = 2;
@@ -576,9 +577,11 @@ struct Plan {
 const int kChainEP[] = {1, 2, 4, 8, 16};
 int chain_max_threads(int ep) { return ep <= 4 ? 256 : (ep <= 8 ? 512 : 640); }
 
-int chain_smem(int64_t ld, int stages) {
-    return (int)(stages * ld * sizeof(double) + 2 * (stages + 1) * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
-                 2 * 64 * sizeof(double));
+int chain_nv(int R) { return R + R * (R - 1) / 2 + R + 1; }
+
+int chain_smem(int64_t ld, int stages, int R, int T) {
+    return (int)(stages * ld * sizeof(double) + (stages + R) * 2 * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
+                 ((size_t)chain_nv(R) * T + chain_nv(R) + 1) * sizeof(double));
 }
 
 size_t sync_smem(int64_t q, int64_t cw, int stages, int P, bool cluster) {
@@ -590,13 +593,21 @@ size_t sync_smem(int64_t q, int64_t cw, int stages, int P, bool cluster) {
            nwarp * sizeof(double) + q * sizeof(double) + 8 * q * sizeof(int32_t);
 }
 
-void* chain_fn(int ep) {
-    switch (ep) {
-        case 1: return (void*)chain_kernel<1>;
-        case 2: return (void*)chain_kernel<2>;
-        case 4: return (void*)chain_kernel<4>;
-        case 8: return (void*)chain_kernel<8>;
-        default: return (void*)chain_kernel<16>;
+void* chain_fn(int ep, int R) {
+    switch (ep * 100 + R) {
+        case 101: return (void*)chain_kernel<1, 1>;
+        case 104: return (void*)chain_kernel<1, 4>;
+        case 108: return (void*)chain_kernel<1, 8>;
+        case 201: return (void*)chain_kernel<2, 1>;
+        case 204: return (void*)chain_kernel<2, 4>;
+        case 208: return (void*)chain_kernel<2, 8>;
+        case 401: return (void*)chain_kernel<4, 1>;
+        case 402: return (void*)chain_kernel<4, 2>;
+        case 404: return (void*)chain_kernel<4, 4>;
+        case 801: return (void*)chain_kernel<8, 1>;
+        case 802: return (void*)chain_kernel<8, 2>;
+        case 1601: return (void*)chain_kernel<16, 1>;
+        default: return nullptr;
     }
 }
 
@@ -631,18 +642,28 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     }
     if (ep == 0 || T > chain_max_threads(ep) || (int64_t)ep * T < pairs)
         return fail(KZ_EINVAL, "n=%lld too large for the chain kernel", (long long)s->n);
+    // rows per reduction: as many as registers allow (EP small) and the ring holds (> R rows)
+    int R = ep <= 2 ? 8 : (ep == 4 ? 4 : (ep == 8 ? 2 : 1));
+    if (const char* e = getenv("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
     const int64_t stage_bytes = s->ld * (int64_t)sizeof(double);
-    const int64_t fixed = chain_smem(s->ld, 0);
-    int stages = (int)std::min<int64_t>(8, std::max<int64_t>(1, ((int64_t)200 * 1024 - fixed) / stage_bytes));
-    if ((size_t)chain_smem(s->ld, stages) > kSmemLimit)
+    int stages = 0;
+    for (;;) {
+        const int64_t fixed = chain_smem(s->ld, 0, R, T);
+        stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
+        if (stages >= R + 1 || R == 1) break;
+        R = R > 4 ? 4 : (R > 2 ? 2 : 1);
+    }
+    if (stages < 1 || (size_t)chain_smem(s->ld, stages, R, T) > kSmemLimit)
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
+    if (!chain_fn(ep, R)) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d", ep, R);
     pl.kernel = KZ_KERNEL_CHAIN;
     pl.threads = T;
     pl.ep = ep;
+    pl.rows = R;
     pl.stages = stages;
-    pl.smem = chain_smem(s->ld, stages);
+    pl.smem = chain_smem(s->ld, stages, R, T);
     pl.ctas = (int)q;
-    void* fn = chain_fn(ep);
+    void* fn = chain_fn(ep, R);
     KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (q > 1) {
         int per_sm = 0;
@@ -729,7 +750,7 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
     cfg.attrs = attr;
     void* fn;
     if (pl.kernel == KZ_KERNEL_CHAIN) {
-        fn = chain_fn(pl.ep);
+        fn = chain_fn(pl.ep, pl.rows);
         attr[0].id = cudaLaunchAttributeCooperative;
         attr[0].val.cooperative = 1;
         cfg.numAttrs = pl.ctas > 1 ? 1 : 0;
@@ -957,7 +978,23 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
     KZ_CUDA(cudaStreamSynchronize(st));
     r->kernel_launches = g_launches.load() - launches0;
-    if (phase_timing) {  // per-phase completion (max over warps) relative to the earliest warp start, CTA 0
+    if (phase_timing && pl.kernel == KZ_KERNEL_CHAIN) {  // chain: block phases of CTA 0 thread 0
+        std::vector<long long> h(32 * 64);
+        KZ_CUDA(cudaMemcpy(h.data(), s->dbg.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        double acc[8] = {0};
+        int nrec = 0;
+        for (int b = 4; b < 63; ++b) {
+            const long long* r = &h[b * 8];
+            if (r[6] == 0 || h[(b + 1) * 8] == 0) continue;
+            for (int ph = 0; ph < 6; ++ph) acc[ph] += (double)(r[ph + 1] - r[ph]);
+            acc[6] += (double)(h[(b + 1) * 8] - r[6]);
+            ++nrec;
+        }
+        if (nrec)
+            fprintf(stderr, "[kz chain block cycles] issue %.0f wait %.0f partials %.0f reduce %.0f solve %.0f apply %.0f "
+                            "gap %.0f (n=%d, R=%d)\n", acc[0] / nrec, acc[1] / nrec, acc[2] / nrec, acc[3] / nrec,
+                    acc[4] / nrec, acc[5] / nrec, acc[6] / nrec, nrec, pl.rows);
+    } else if (phase_timing) {  // per-phase completion (max over warps) relative to the earliest warp start, CTA 0
         std::vector<long long> h(32 * 64);
         KZ_CUDA(cudaMemcpy(h.data(), s->dbg.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
         double acc[8] = {0}, span = 0;

@@ -1,87 +1,135 @@
 // kz_chain.cu -- worker-per-CTA persistent kernel for RK and RKAB.
 //
 // Reference semantics (paths relative to /root/reference/pkg/src/kaczbench):
-//   kaczmarz_step      solvers.py:107-117   scale = alpha*(b_i - <a_i,v>)/sq_i ; v += scale*a_i
+//   kaczmarz_step      solvers.py:107-117   s = alpha*(b_i - <a_i,v>)/sq_i ; v += s*a_i
 //   rkab_worker_block  solvers.py:140-145   bs chained projections on the private v
 //   RKAB advance       solvers.py:361-367   v_t = x ; chain ; x = (sum_t v_t) / q, t ascending
-//   solve_rk           solvers.py:294-310   (= q 1, bs 1)
+//   solve_rk           solvers.py:294-310   (q = 1, bs = 1)
 //   _drive stop rule   solvers.py:229-243   ||x - x_ref||^2 < eps checked before every iteration
 //
 // Layout: CTA w runs worker w.  Its estimate v lives in registers: thread
 // `tid` owns the 16-byte column pairs col = 2*(p*T + tid), p < EP.  Rows are
-// streamed HBM -> shared memory by per-thread cp.async (16 B, each thread
-// copies exactly the pairs it later reads, so no CTA barrier guards the
-// data) through a `stages`-deep ring; row indices are x-independent and are
-// read from a shared-memory window, so the ring runs stages-1 rows ahead.
-// One CTA reduction (warp shuffles + one bar.sync on a parity-double-
-// buffered scratch) per projection; the stop-rule error is fused into the
-// first projection of each iteration when q == 1.
+// streamed HBM -> shared memory by per-thread cp.async (each thread copies
+// exactly the pairs it later reads) through a ring of `stages` rows; row
+// indices are x-independent and come from a shared-memory window, so the
+// ring runs ahead of the arithmetic.
 //
-// Arithmetic: the axpy is __dmul_rn then __dadd_rn (two roundings, as numpy's
-// `x += scale * row`); the scale is computed in the reference's order; the
-// average is a strictly ordered sum over workers then an IEEE division.  Only
-// the dot product's summation order differs from OpenBLAS (tolerance parity).
+// Row blocks (the latency lever).  A chain of projections is a dependent
+// sequence -- dot, CTA-wide reduction, scale, axpy -- so one reduction per
+// row leaves the memory system idle.  The kernel instead takes R consecutive
+// rows a_1..a_R of a worker's chain and reduces, in ONE CTA reduction,
+//     d_r = <a_r, v>   and   G_rl = <a_r, a_l> (l < r),
+// then resolves the chain exactly as the reference orders it:
+//     <a_r, v_{r-1}> = d_r + sum_{l<r} s_l G_rl,  s_r = alpha (b_r - <a_r, v_{r-1}>) / sq_r,
+// and applies v += s_r a_r row by row with the reference's rounding
+// (__dmul_rn then __dadd_rn).  The dot products are therefore rebracketed
+// (tolerance parity, like any change of summation order); the updates and
+// the averaging are the reference's.  1/sq_r replaces the division.
+//
+// The stop rule (RK and RKAB with q = 1 check between rows) rides along:
+// the same reduction carries ||v - x_ref||^2 and <a_r, x_ref>, and
+//     ||v_r - x_ref||^2 = ||v_{r-1} - x_ref||^2 + 2 s_r (<a_r, v_{r-1}> - <a_r, x_ref>) + s_r^2 sq_r
+// gives the error before each row of the block.  A derived value that comes
+// within 1e-6 (relative) of eps truncates the block, so every decision near
+// the threshold is taken on a directly reduced ||x - x_ref||^2.
+//
+// RKAB with q > 1 averages the worker estimates in worker order behind two
+// grid barriers (cooperative launch) and checks the averaged x directly.
 #include "kz_kernels.cuh"
 
 namespace kz {
 
 namespace {
 
-struct ChainSmem {
-    double* ring;   // stages x ld
-    double* bsq;    // (stages + 1) x 2 : b_i, sq_i per in-flight row
-    int32_t* win;   // IDX_WINDOW row indices
-    double* red;    // 2 parities x 2 values x 32 warps
+template <int R>
+struct Blk {
+    static constexpr int NG = R * (R - 1) / 2;  // Gram entries l < r
+    static constexpr int NVN = R + NG;          // without stop-rule terms
+    static constexpr int NVC = NVN + R + 1;     // + <a_r, x_ref>, ||v - x_ref||^2
 };
 
-__device__ __forceinline__ ChainSmem carve(unsigned char* raw, int stages, int64_t ld) {
-    ChainSmem s;
-    s.ring = reinterpret_cast<double*>(raw);
-    s.bsq = s.ring + (size_t)stages * ld;
-    s.win = reinterpret_cast<int32_t*>(s.bsq + 2 * (stages + 1));
-    s.red = reinterpret_cast<double*>(s.win + IDX_WINDOW);
-    return s;
-}
+__host__ __device__ constexpr int gidx(int r, int l) { return r * (r - 1) / 2 + l; }
 
-// Sum of one (or two) per-thread values over the CTA; every thread returns
-// the same bits (fixed shuffle tree, fixed warp order).
-template <bool TWO>
-__device__ __forceinline__ void cta_reduce(double& v0, double& v1, double* red, int& par, int lane, int warp, int nw) {
-    v0 = warp_sum(v0);
-    if (TWO) v1 = warp_sum(v1);
-    double* r = red + par * 64;
-    if (lane == 0) {
-        r[warp] = v0;
-        if (TWO) r[32 + warp] = v1;
+struct ChainSmem {
+    double* ring;   // stages x ld
+    double2* bsq;   // stages + R slots of (b_i, sq_i)
+    int32_t* win;   // IDX_WINDOW row indices
+    double* scr;    // NVC x T reduction scratch (value-major)
+    double* tot;    // NVC totals
+};
+
+// CTA-wide sums of NV per-thread values; every thread receives every total,
+// bit-identical.  Value-major transpose through shared memory: thread t
+// stores its NV partials at scr[i*T + t]; for each value, nw threads each add
+// 32 consecutive entries (4 interleaved accumulators, 16-byte loads), a fixed
+// xor tree joins the nw pieces, and the totals come back through `tot`.
+// Two CTA barriers; ~NV + 2*NV/nw... instructions per thread instead of 15*NV
+// for per-value shuffle trees.
+template <int NV>
+__device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double* tot, int tid, int T, int nw) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scr[i * T + tid] = v[i];
+    __syncthreads();
+    const int lg = 32 - __clz(nw - 1);  // W = 2^lg >= nw lanes per value (zero pieces pad)
+    const int W = 1 << lg;
+    for (int u0 = 0; u0 < NV * W; u0 += T) {
+        const int u = u0 + tid, i = u >> lg, part = u & (W - 1);
+        double sum = 0.0;
+        if (i < NV && part < nw) {
+            const double2* src = reinterpret_cast<const double2*>(scr + i * T + part * 32);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 16; k += 2) {
+                const double2 x0 = src[k], x1 = src[k + 1];
+                a0 = __dadd_rn(a0, x0.x);
+                a1 = __dadd_rn(a1, x0.y);
+                a2 = __dadd_rn(a2, x1.x);
+                a3 = __dadd_rn(a3, x1.y);
+            }
+            sum = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+        }
+        for (int o = W >> 1; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o, W));
+        if (part == 0 && i < NV) tot[i] = sum;
     }
     __syncthreads();
-    v0 = warp_sum(lane < nw ? r[lane] : 0.0);
-    if (TWO) v1 = warp_sum(lane < nw ? r[32 + lane] : 0.0);
-    par ^= 1;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = tot[i];
 }
+
+struct TrueT {
+    static constexpr bool value = true;
+};
+struct FalseT {
+    static constexpr bool value = false;
+};
 
 }  // namespace
 
-// Largest CTA each pair count is launched with (keeps v register-resident).
 template <int EP>
 struct ChainMaxThreads {
     static constexpr int value = EP <= 4 ? 256 : (EP <= 8 ? 512 : 640);
 };
 
-template <int EP>
+template <int EP, int R>
 __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     const int D = a.stages;
+    const int BS = D + R;  // (b, sq) slots
     const int64_t ld = a.ld, q = a.q, bs = a.bs;
-    ChainSmem sm = carve(smem_raw, D, ld);
+    ChainSmem sm;
+    sm.ring = reinterpret_cast<double*>(smem_raw);
+    sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ld);
+    sm.win = reinterpret_cast<int32_t*>(sm.bsq + BS);
+    sm.scr = reinterpret_cast<double*>(sm.win + IDX_WINDOW);
+    sm.tot = sm.scr + (size_t)Blk<R>::NVC * T;
 
     const int64_t w = blockIdx.x;  // worker id
     const int32_t* idx = a.idx + w * a.idx_stride;
     const double alpha = a.alphas[w];
     const int64_t total = a.count * bs;  // draws of this worker in the launch
+    const double2* bs2 = reinterpret_cast<const double2*>(a.bs2);
 
-    // v = x (x0 = 0 on the first launch, the carried iterate afterwards)
     double v[2 * EP];
 #pragma unroll
     for (int p = 0; p < EP; ++p) {
@@ -94,61 +142,221 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     for (int64_t e = tid; e < IDX_WINDOW && e < total; e += T) sm.win[e] = idx[e];
     __syncthreads();
 
-    // ring bookkeeping in 32-bit: row d lives in stage d % D, its (b_i, sq_i)
-    // in slot d % (D + 1); both advance incrementally (no 64-bit modulo).
-    auto issue = [&](int64_t d, int stage, int slot) {
-        if (d < total) {
-            const int64_t i = sm.win[d & (IDX_WINDOW - 1)];
+    // ---- issue side of the row ring ---------------------------------------------------
+    int64_t issued = 0, win_next = IDX_WINDOW / 2;
+    int iss_stage = 0, iss_slot = 0;
+    auto issue_upto = [&](int64_t lim) {
+        if (lim > total) lim = total;
+        while (issued < lim) {
+            if (issued >= win_next) {  // refill the window half the issue pointer has left
+                for (int64_t e = win_next + IDX_WINDOW / 2 + tid; e < win_next + IDX_WINDOW && e < total; e += T)
+                    sm.win[e & (IDX_WINDOW - 1)] = idx[e];
+                win_next += IDX_WINDOW / 2;
+                __syncwarp();
+            }
+            const int64_t i = sm.win[issued & (IDX_WINDOW - 1)];
             const double* src = a.A + i * ld;
-            double* dst = sm.ring + (size_t)stage * ld;
+            double* dst = sm.ring + (size_t)iss_stage * ld;
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
                 const int64_t col = 2 * ((int64_t)p * T + tid);
                 if (col < ld) cp_async16(dst + col, src + col);
             }
-            if (tid == 0) {
-                double* bs_slot = sm.bsq + 2 * slot;
-                cp_async8(bs_slot, a.b + i);
-                cp_async8(bs_slot + 1, a.sq + i);
-            }
+            if (tid == 0) cp_async16(sm.bsq + iss_slot, bs2 + i);
+            cp_async_commit();
+            ++issued;
+            iss_stage = (iss_stage + 1 == D) ? 0 : iss_stage + 1;
+            iss_slot = (iss_slot + 1 == BS) ? 0 : iss_slot + 1;
         }
-        cp_async_commit();
     };
 
-    // stop-rule error of the current v (= x), every CTA computes the same bits
-    auto err_partial = [&]() {
-        double e = 0.0;
+    // direct ||v - x_ref||^2 over the CTA
+    auto err_direct = [&]() {
+        double e[1] = {0.0};
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
             const int64_t col = 2 * ((int64_t)p * T + tid);
             if (col < ld) {
                 const double2 r = __ldg(reinterpret_cast<const double2*>(a.xref + col));
                 const double d0 = v[2 * p] - r.x, d1 = v[2 * p + 1] - r.y;
-                e = fma(d0, d0, e);
-                e = fma(d1, d1, e);
+                e[0] = fma(d0, d0, e[0]);
+                e[0] = fma(d1, d1, e[0]);
             }
         }
-        return e;
+        cta_reduce<1>(e, sm.scr, sm.tot, tid, T, nw);
+        return e[0];
     };
 
-    for (int j = 0; j < D - 1; ++j) issue(j, j, j);
-    int stage = 0, slot = 0;  // consumption position of draw d
-
-    int par = 0;
     unsigned epoch = 0;
-    int64_t d = 0;
     long long done = 0;
     int conv = 0, checks = 0;
     double err_last = 0.0;
-    const double inv_q_d = (double)q;
+    const double qd = (double)q;
+    const bool use_stop = a.use_stop != 0;
+    const bool ckpt_on = a.ckpt_every > 0;
+    int nblk = 0;                 // blocks processed (phase timing)
+    int64_t d = 0;                // rows consumed
+    int64_t next_check = 0;       // q == 1: next row preceded by a stop-rule check (multiple of bs)
+    int64_t outer_end = bs;       // q == 1: row count at which the current outer iteration completes
+    int64_t kdone = a.k0;         // q == 1: outer iterations completed (global index)
+    int64_t next_ck = ckpt_on ? (a.k0 / a.ckpt_every + 1) * a.ckpt_every : 0;
+    int c_stage = 0, c_slot = 0;  // ring position of row d
 
-    for (int64_t kk = 0;; ++kk) {
-        const bool last = (kk == a.count);
-        const bool want_check = a.use_stop && (!last || a.final_check);
-        if (last || q > 1) {
-            if (want_check) {
-                double e = err_partial(), dummy = 0.0;
-                cta_reduce<false>(e, dummy, sm.red, par, lane, warp, nw);
+    // Process rows [d, d + Rp) of the chain (Rp <= R).  CHECK: stop rule before
+    // rows with (d + r) % bs == 0 (q == 1 only).  Returns rows applied.
+    auto block = [&](int Rp, auto check_tag) -> int {
+        constexpr bool CHECK = decltype(check_tag)::value;
+        constexpr int NV = CHECK ? Blk<R>::NVC : Blk<R>::NVN;
+        const bool rec = a.dbg != nullptr && blockIdx.x == 0 && tid == 0 && nblk < 64;
+        if (rec) a.dbg[nblk * 8 + 0] = clock64();
+        issue_upto(d + D);
+        if (rec) a.dbg[nblk * 8 + 1] = clock64();
+        cp_async_wait_dyn((int)(issued - (d + Rp)));
+        if (rec) a.dbg[nblk * 8 + 2] = clock64();
+        int stg[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int s0 = c_stage + r;
+            stg[r] = s0 >= D ? s0 - D : s0;
+        }
+        double vals[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) vals[i] = 0.0;
+#pragma unroll
+        for (int p = 0; p < EP; ++p) {
+            const int64_t col = 2 * ((int64_t)p * T + tid);
+            if (col < ld) {
+                double2 rr[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    rr[r] = (r < Rp) ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ld + col)
+                                     : make_double2(0.0, 0.0);
+                const double vx = v[2 * p], vy = v[2 * p + 1];
+#pragma unroll
+                for (int r = 0; r < R; ++r) vals[r] = fma(rr[r].y, vy, fma(rr[r].x, vx, vals[r]));
+#pragma unroll
+                for (int r = 1; r < R; ++r)
+#pragma unroll
+                    for (int l = 0; l < r; ++l)
+                        vals[R + gidx(r, l)] = fma(rr[r].y, rr[l].y, fma(rr[r].x, rr[l].x, vals[R + gidx(r, l)]));
+                if (CHECK) {
+                    const double2 xr = __ldg(reinterpret_cast<const double2*>(a.xref + col));
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        vals[Blk<R>::NVN + r] = fma(rr[r].y, xr.y, fma(rr[r].x, xr.x, vals[Blk<R>::NVN + r]));
+                    const double d0 = vx - xr.x, d1 = vy - xr.y;
+                    vals[NV - 1] = fma(d1, d1, fma(d0, d0, vals[NV - 1]));
+                }
+            }
+        }
+        if (rec) a.dbg[nblk * 8 + 3] = clock64();
+        cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw);
+        if (rec) a.dbg[nblk * 8 + 4] = clock64();
+        // (b_r, sq_r): lane r loads its row's pair and forms 1/sq_r; shuffled to all
+        double2 bq = make_double2(0.0, 1.0);
+        if (lane < Rp) {
+            const int sl = c_slot + lane;
+            bq = sm.bsq[sl >= BS ? sl - BS : sl];
+        }
+        const double inv_l = 1.0 / bq.y;
+        double s[R];
+        int Reff = Rp;
+        double e = CHECK ? vals[NV - 1] : 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r < Reff) {
+                const double br = __shfl_sync(0xffffffffu, bq.x, r);
+                const double sqr = __shfl_sync(0xffffffffu, bq.y, r);
+                const double invr = __shfl_sync(0xffffffffu, inv_l, r);
+                double dr = vals[r];
+#pragma unroll
+                for (int l = 0; l < r; ++l) dr = fma(s[l], vals[R + gidx(r, l)], dr);
+                if (CHECK && d + r == next_check) {
+                    if (r == 0) {
+                        ++checks;
+                        err_last = e;
+                        if (e < a.eps) {
+                            conv = 1;
+                            Reff = 0;
+                        }
+                    } else if (e < a.eps * (1.0 + 1e-6)) {
+                        Reff = r;  // decide on a direct reduction next block
+                    } else {
+                        ++checks;
+                        err_last = e;
+                    }
+                }
+                if (r < Reff) {
+                    if (CHECK && d + r == next_check) next_check += bs;
+                    s[r] = __dmul_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), invr);
+                    if (CHECK) e = fma(s[r] * s[r], sqr, fma(2.0 * s[r], dr - vals[Blk<R>::NVN + r], e));
+                }
+            }
+        }
+        if (rec) a.dbg[nblk * 8 + 5] = clock64();
+        // apply the Reff projections in order with the reference's rounding
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r < Reff) {
+#pragma unroll
+                for (int p = 0; p < EP; ++p) {
+                    const int64_t col = 2 * ((int64_t)p * T + tid);
+                    if (col < ld) {
+                        const double2 rv = *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ld + col);
+                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], rv.x));
+                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], rv.y));
+                    }
+                }
+                if (q == 1 && d + r + 1 == outer_end) {  // outer iteration kdone completes here
+                    outer_end += bs;
+                    ++kdone;
+                    if (ckpt_on && kdone == next_ck) {
+                        next_ck += a.ckpt_every;
+                        const int64_t slot = kdone / a.ckpt_every - 1;
+                        if (slot < a.ckpt_cap) {
+#pragma unroll
+                            for (int p = 0; p < EP; ++p) {
+                                const int64_t col = 2 * ((int64_t)p * T + tid);
+                                if (col < a.n) a.ckpt[slot * a.n + col] = v[2 * p];
+                                if (col + 1 < a.n) a.ckpt[slot * a.n + col + 1] = v[2 * p + 1];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (rec) a.dbg[nblk * 8 + 6] = clock64();
+        ++nblk;
+        d += Reff;
+        c_stage += Reff;
+        if (c_stage >= D) c_stage -= D;
+        c_slot += Reff;
+        if (c_slot >= BS) c_slot -= BS;
+        return Reff;
+    };
+
+    if (q == 1) {
+        // one chain: outer iteration k = rows [k*bs, (k+1)*bs); x = v after each
+        while (d < total) {
+            const int Rp = (int)((total - d) < R ? (total - d) : R);
+            if (use_stop)
+                block(Rp, TrueT{});
+            else
+                block(Rp, FalseT{});
+            if (conv) break;
+        }
+        done = d / bs;
+        if (!conv && use_stop && a.final_check) {
+            const double e = err_direct();
+            ++checks;
+            err_last = e;
+            if (e < a.eps) conv = 1;
+        }
+    } else {
+        for (int64_t kk = 0;; ++kk) {
+            const bool last = (kk == a.count);
+            if (use_stop && (!last || a.final_check)) {
+                const double e = err_direct();  // identical in every CTA
                 ++checks;
                 err_last = e;
                 if (e < a.eps) {
@@ -157,68 +365,12 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 }
             }
             if (last) break;
-        }
-        for (int64_t s = 0; s < bs; ++s, ++d) {
-            const bool chk = want_check && q == 1 && s == 0;
-            if ((d & 511) == 0 && d > 0) {  // refill the index window half we are leaving
-                for (int64_t e = d + 512 + tid; e < d + IDX_WINDOW && e < total; e += T)
-                    sm.win[e & (IDX_WINDOW - 1)] = idx[e];
-            }
-            issue(d + D - 1, stage == 0 ? D - 1 : stage - 1, slot >= 2 ? slot - 2 : slot + D - 1);
-            cp_async_wait_dyn(D - 1);
-            const double* row = sm.ring + (size_t)stage * ld;
-            double dot = 0.0, e2 = 0.0;
-#pragma unroll
-            for (int p = 0; p < EP; ++p) {
-                const int64_t col = 2 * ((int64_t)p * T + tid);
-                if (col < ld) {
-                    const double2 r = *reinterpret_cast<const double2*>(row + col);
-                    dot = fma(r.x, v[2 * p], dot);
-                    dot = fma(r.y, v[2 * p + 1], dot);
-                }
-            }
-            if (chk) {
-                e2 = err_partial();
-                cta_reduce<true>(dot, e2, sm.red, par, lane, warp, nw);
-                ++checks;
-                err_last = e2;
-                if (e2 < a.eps) {
-                    conv = 1;
-                    goto finish;
-                }
-            } else {
-                cta_reduce<false>(dot, e2, sm.red, par, lane, warp, nw);
-            }
-            {
-                const double* bq = sm.bsq + 2 * slot;
-                const double scale = __ddiv_rn(__dmul_rn(alpha, __dsub_rn(bq[0], dot)), bq[1]);
-#pragma unroll
-                for (int p = 0; p < EP; ++p) {
-                    const int64_t col = 2 * ((int64_t)p * T + tid);
-                    if (col < ld) {
-                        const double2 r = *reinterpret_cast<const double2*>(row + col);
-                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(scale, r.x));
-                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(scale, r.y));
-                    }
-                }
-            }
-            stage = (stage + 1 == D) ? 0 : stage + 1;
-            slot = (slot == D) ? 0 : slot + 1;
-        }
-        const int64_t k = a.k0 + kk;
-        const bool ck = a.ckpt_every > 0 && ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;
-        const int64_t slot = ck ? (k + 1) / a.ckpt_every - 1 : 0;
-        if (q == 1) {
-            if (ck) {
-#pragma unroll
-                for (int p = 0; p < EP; ++p) {
-                    const int64_t col = 2 * ((int64_t)p * T + tid);
-                    if (col < a.n) a.ckpt[slot * a.n + col] = v[2 * p];
-                    if (col + 1 < a.n) a.ckpt[slot * a.n + col + 1] = v[2 * p + 1];
-                }
-            }
-        } else {
+            const int64_t end = (kk + 1) * bs;
+            while (d < end) block((int)((end - d) < R ? (end - d) : R), FalseT{});
             // publish v_w, average column slices in worker order, redistribute x
+            const int64_t k = a.k0 + kk;
+            const bool ck = ckpt_on && ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;
+            const int64_t slot = ck ? (k + 1) / a.ckpt_every - 1 : 0;
             double* vw = a.V + w * ld;
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
@@ -236,7 +388,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                     __stcg(a.partial + col, acc);
                     continue;
                 }
-                const double xn = __ddiv_rn(acc, inv_q_d);
+                const double xn = __ddiv_rn(acc, qd);
                 __stcg(a.x + col, xn);
                 if (ck && col < a.n) a.ckpt[slot * a.n + col] = xn;
             }
@@ -250,10 +402,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                     v[2 * p + 1] = xv.y;
                 }
             }
+            done = kk + 1;
         }
-        done = kk + 1;
     }
-finish:
     cp_async_wait<0>();
     if (q == 1) {
         double* dst = a.partial ? a.partial : a.x;
@@ -271,10 +422,19 @@ finish:
     }
 }
 
-template __global__ void chain_kernel<1>(SolveArgs);
-template __global__ void chain_kernel<2>(SolveArgs);
-template __global__ void chain_kernel<4>(SolveArgs);
-template __global__ void chain_kernel<8>(SolveArgs);
-template __global__ void chain_kernel<16>(SolveArgs);
+#define KZ_CHAIN(EP, R) template __global__ void chain_kernel<EP, R>(SolveArgs);
+KZ_CHAIN(1, 1)
+KZ_CHAIN(1, 4)
+KZ_CHAIN(1, 8)
+KZ_CHAIN(2, 1)
+KZ_CHAIN(2, 4)
+KZ_CHAIN(2, 8)
+KZ_CHAIN(4, 1)
+KZ_CHAIN(4, 2)
+KZ_CHAIN(4, 4)
+KZ_CHAIN(8, 1)
+KZ_CHAIN(8, 2)
+KZ_CHAIN(16, 1)
+#undef KZ_CHAIN
 
 }  // namespace kz

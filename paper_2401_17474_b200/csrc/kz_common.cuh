@@ -89,7 +89,7 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_dyn(int n) {
-    // wait_group needs an immediate; dispatch the small range we use.
+    // wait_group needs an immediate; dispatch the range we use (0..15).
     switch (n) {
         case 0: cp_async_wait<0>(); break;
         case 1: cp_async_wait<1>(); break;
@@ -98,7 +98,15 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
         case 4: cp_async_wait<4>(); break;
         case 5: cp_async_wait<5>(); break;
         case 6: cp_async_wait<6>(); break;
-        default: cp_async_wait<7>(); break;
+        case 7: cp_async_wait<7>(); break;
+        case 8: cp_async_wait<8>(); break;
+        case 9: cp_async_wait<9>(); break;
+        case 10: cp_async_wait<10>(); break;
+        case 11: cp_async_wait<11>(); break;
+        case 12: cp_async_wait<12>(); break;
+        case 13: cp_async_wait<13>(); break;
+        case 14: cp_async_wait<14>(); break;
+        default: cp_async_wait<15>(); break;
     }
 }
 

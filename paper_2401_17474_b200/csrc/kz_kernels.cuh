@@ -41,8 +41,9 @@ struct SolveArgs {
     int ablate;            // debug: bit mask of phases to skip (KZ_ABLATE), timing experiments only
 };
 
-// chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread.
-template <int EP>
+// chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
+// R = rows resolved per CTA reduction (Gram-corrected block).
+template <int EP, int R>
 __global__ void chain_kernel(SolveArgs a);
 
 // sync kernel: column-sliced (RKA, RKAB bs=1).  CLUSTER: reduce via DSMEM.
