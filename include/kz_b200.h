@@ -80,6 +80,14 @@ KZ_API int32_t kz_system_upload_device(kz_system* sys, const double* A_dev, int6
 KZ_API int32_t kz_system_device_ptrs(kz_system* sys, double** A_dev, double** b_dev, double** xref_dev);
 /* Replace the stopping reference x_ref (n values, host). */
 KZ_API int32_t kz_system_set_xref(kz_system* sys, const double* xref_host, void* stream);
+/* BASELINE config 3 generator: fills A (leading m x n of the counter-keyed
+ * mother system), x_ref = x* and b = A x* on the device.  Entries depend only
+ * on (seed, i, j), so any m' x n' system is an exact leading crop. */
+KZ_API int32_t kz_generate_counter(kz_system* sys, uint64_t seed, double mu_lo, double mu_hi, double sigma_lo,
+                                   double sigma_hi, void* stream);
+/* Copy the leading m2 x n2 block of A (row-major, ld n2), b[:m2] and x_ref[:n2] to the host (any may be NULL). */
+KZ_API int32_t kz_system_download(kz_system* sys, int64_t m2, int64_t n2, double* A_host, double* b_host,
+                                  double* xref_host, void* stream);
 /* Invalidate cached row norms / samplers after A was written in place. */
 KZ_API int32_t kz_system_touch(kz_system* sys);
 

@@ -29,6 +29,7 @@ EXPORTS = (
     "kz_last_error", "kz_version", "kz_launch_count", "kz_device_count",
     "kz_system_create", "kz_system_destroy", "kz_system_pitch", "kz_system_upload",
     "kz_system_upload_device", "kz_system_device_ptrs", "kz_system_set_xref", "kz_system_touch",
+    "kz_generate_counter", "kz_system_download",
     "kz_row_norms", "kz_sampler_build", "kz_sampler_set_ranges", "kz_dump_rows", "kz_solve",
     "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
 )
@@ -118,6 +119,8 @@ def load_library():
         L.kz_system_device_ptrs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
         L.kz_system_set_xref.argtypes = [vp, _dp, vp]
         L.kz_system_touch.argtypes = [vp]
+        L.kz_generate_counter.argtypes = [vp, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double, vp]
+        L.kz_system_download.argtypes = [vp, C.c_int64, C.c_int64, _dp, _dp, _dp, vp]
         L.kz_row_norms.argtypes = [vp, _dp, C.POINTER(C.c_int64), vp]
         L.kz_sampler_build.argtypes = [vp, C.c_int32, C.c_int64, _dp, vp]
         L.kz_dump_rows.argtypes = [vp, C.c_int32, C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,

@@ -304,6 +304,44 @@ extern "C" int32_t kz_system_set_xref(kz_system* s, const double* xref, void* st
     return KZ_OK;
 }
 
+extern "C" int32_t kz_generate_counter(kz_system* s, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,
+                                       double sg_hi, void* stream) {
+    if (!s) return fail(KZ_EINVAL, "null system");
+    if (!(sg_lo > 0) || sg_hi < sg_lo || mu_hi < mu_lo) return fail(KZ_EINVAL, "bad generator ranges");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    const int64_t pairs = s->m * (s->ld / 2);
+    const unsigned blocks = (unsigned)std::min<int64_t>((pairs + 255) / 256, (int64_t)s->sms * 64);
+    gen_counter_kernel<<<blocks, 256, 0, st>>>(s->A.p, s->m, s->n, s->ld, seed, mu_lo, mu_hi, sg_lo, sg_hi);
+    KZ_TRY(check_launch("gen_counter_kernel"));
+    gen_xstar_kernel<<<(unsigned)((s->ld / 2 + 255) / 256), 256, 0, st>>>(s->xref.p, s->n, s->ld, seed, mu_lo, mu_hi,
+                                                                          sg_lo, sg_hi);
+    KZ_TRY(check_launch("gen_xstar_kernel"));
+    gemv_rows_kernel<<<(unsigned)((s->m + 7) / 8), 256, 0, st>>>(s->A.p, s->xref.p, s->m, s->n, s->ld, s->b.p);
+    KZ_TRY(check_launch("gemv_rows_kernel"));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    s->has_xref = true;
+    s->norms_valid = false;
+    s->bs2_valid = false;
+    s->sampler_scheme = -1;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_system_download(kz_system* s, int64_t m2, int64_t n2, double* A_host, double* b_host,
+                                      double* xref_host, void* stream) {
+    if (!s || m2 < 0 || n2 < 0 || m2 > s->m || n2 > s->n) return fail(KZ_EINVAL, "bad crop");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    if (A_host && m2 > 0 && n2 > 0)
+        KZ_CUDA(cudaMemcpy2DAsync(A_host, n2 * sizeof(double), s->A.p, s->ld * sizeof(double), n2 * sizeof(double), m2,
+                                  cudaMemcpyDeviceToHost, st));
+    if (b_host && m2 > 0) KZ_CUDA(cudaMemcpyAsync(b_host, s->b.p, m2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (xref_host && n2 > 0)
+        KZ_CUDA(cudaMemcpyAsync(xref_host, s->xref.p, n2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    return KZ_OK;
+}
+
 extern "C" int32_t kz_system_touch(kz_system* s) {
     if (!s) return fail(KZ_EINVAL, "null system");
     s->norms_valid = false;

@@ -1,0 +1,89 @@
+// kz_gen.cu -- counter-based generator for BASELINE config 3.
+//
+// The reference's generator (sysgen.py:125-145) is one sequential PCG64
+// stream, so a 160000 x 20000 (25.6 GB) system cannot be produced in
+// parallel or cropped consistently.  Config 3 asks for entries "from a
+// counter-based RNG keyed on (seed, i, j), so that smaller systems are exact
+// leading-row/column crops".  This generator keeps the reference's
+// distribution family -- per row mu_i ~ U(mu_range), sigma_i ~ U(sigma_range),
+// A_ij ~ N(mu_i, sigma_i); x*_j ~ N(mu*, sigma*) with one more (mu*, sigma*)
+// pair; b = A x* -- but draws every value from a counter hash:
+//     u(key, a, b) = splitmix64(splitmix64(key ^ a*C1) ^ b*C2) >> 11 * 2^-53,
+// normals by Box-Muller on two such uniforms (two normals per column pair).
+// It is defined by this device code: CPU oracles use crops copied back.
+#include "kz_kernels.cuh"
+
+namespace kz {
+
+namespace {
+
+__device__ __forceinline__ uint64_t smix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double u01(uint64_t key, uint64_t a, uint64_t b) {
+    const uint64_t h = smix(smix(key ^ (a * 0xD1B54A32D192ED03ULL)) ^ (b * 0x8CB92BA72F3D8DD7ULL));
+    return ((double)(h >> 11) + 0.5) * (1.0 / 9007199254740992.0);  // (0, 1)
+}
+
+// two independent standard normals for counter (a, b)
+__device__ __forceinline__ double2 normal2(uint64_t key, uint64_t a, uint64_t b) {
+    const double u1 = u01(key, a, 2 * b), u2 = u01(key, a, 2 * b + 1);
+    const double r = sqrt(-2.0 * log(u1));
+    double s, c;
+    sincospi(2.0 * u2, &s, &c);
+    return make_double2(r * c, r * s);
+}
+
+constexpr uint64_t TAG_ROW = 0x524F57ULL;   // "ROW"
+constexpr uint64_t TAG_XS = 0x585354ULL;    // "XST"
+
+}  // namespace
+
+__global__ void gen_counter_kernel(double* __restrict__ A, int64_t m, int64_t n, int64_t ld, uint64_t seed,
+                                   double mu_lo, double mu_hi, double sg_lo, double sg_hi) {
+    const int64_t pairs = ld / 2;
+    const int64_t total = m * pairs;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = g / pairs, p = g - i * pairs;
+        const double mu = mu_lo + (mu_hi - mu_lo) * u01(seed, TAG_ROW, 2 * (uint64_t)i);
+        const double sg = sg_lo + (sg_hi - sg_lo) * u01(seed, TAG_ROW, 2 * (uint64_t)i + 1);
+        const double2 z = normal2(seed, (uint64_t)i, (uint64_t)p);
+        const int64_t j = 2 * p;
+        double2 out;
+        out.x = (j < n) ? fma(sg, z.x, mu) : 0.0;
+        out.y = (j + 1 < n) ? fma(sg, z.y, mu) : 0.0;
+        *reinterpret_cast<double2*>(A + i * ld + j) = out;
+    }
+}
+
+__global__ void gen_xstar_kernel(double* __restrict__ x, int64_t n, int64_t ld, uint64_t seed, double mu_lo,
+                                 double mu_hi, double sg_lo, double sg_hi) {
+    const double mu = mu_lo + (mu_hi - mu_lo) * u01(seed, TAG_XS, 0);
+    const double sg = sg_lo + (sg_hi - sg_lo) * u01(seed, TAG_XS, 1);
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+        const double2 z = normal2(seed ^ TAG_XS, 0, (uint64_t)p);
+        const int64_t j = 2 * p;
+        x[j] = (j < n) ? fma(sg, z.x, mu) : 0.0;
+        x[j + 1] = (j + 1 < n) ? fma(sg, z.y, mu) : 0.0;
+    }
+}
+
+// b = A x, one warp per row, fixed (deterministic) reduction order
+__global__ void gemv_rows_kernel(const double* __restrict__ A, const double* __restrict__ x, int64_t m, int64_t n,
+                                 int64_t ld, double* __restrict__ b) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (row >= m) return;
+    const double* a = A + row * ld;
+    double acc = 0.0;
+    for (int64_t j = lane; j < n; j += 32) acc = fma(a[j], x[j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) b[row] = acc;
+}
+
+}  // namespace kz

@@ -72,6 +72,13 @@ __global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __re
 __global__ void scale_copy_kernel(const double* __restrict__ S, double inv_div, int64_t n, double* __restrict__ x);
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
 
+__global__ void gen_counter_kernel(double* __restrict__ A, int64_t m, int64_t n, int64_t ld, uint64_t seed,
+                                   double mu_lo, double mu_hi, double sg_lo, double sg_hi);
+__global__ void gen_xstar_kernel(double* __restrict__ x, int64_t n, int64_t ld, uint64_t seed, double mu_lo,
+                                 double mu_hi, double sg_lo, double sg_hi);
+__global__ void gemv_rows_kernel(const double* __restrict__ A, const double* __restrict__ x, int64_t m, int64_t n,
+                                 int64_t ld, double* __restrict__ b);
+
 constexpr int NORM_ROWS_PER_CTA = 128;
 constexpr int SAMPLE_RUN = 8;
 constexpr int IDX_WINDOW = 1024;  // chain kernel: smem ring of row indices

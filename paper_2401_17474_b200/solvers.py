@@ -137,6 +137,22 @@ class DeviceSystem:
         self._xref_set = True
         return a.value, b.value, x.value, self.pitch
 
+    def generate_counter(self, seed: int = 0, mu_range=(-5.0, 5.0), sigma_range=(1.0, 20.0)) -> None:
+        """Fill the system with the counter-keyed BASELINE config-3 generator (device only)."""
+        N.check(self._lib.kz_generate_counter(self.handle, int(seed), float(mu_range[0]), float(mu_range[1]),
+                                              float(sigma_range[0]), float(sigma_range[1]), None))
+        self._xref_set = True
+
+    def download(self, m2: int | None = None, n2: int | None = None):
+        """(A[:m2, :n2], b[:m2], x_ref[:n2]) copied to the host."""
+        m2 = self.m if m2 is None else m2
+        n2 = self.n if n2 is None else n2
+        A = np.empty((m2, n2))
+        b = np.empty(m2)
+        xr = np.empty(n2)
+        N.check(self._lib.kz_system_download(self.handle, m2, n2, N.ptr(A), N.ptr(b), N.ptr(xr), None))
+        return A, b, xr
+
     def touch(self) -> None:
         N.check(self._lib.kz_system_touch(self.handle))
 
