@@ -604,6 +604,7 @@ namespace {
 struct Plan {
     int kernel = KZ_KERNEL_CHAIN;
     int rows = 1;       // chain: rows per CTA reduction (R)
+    int pair = 1;       // chain: CTAs per worker (cluster of 1 or 2)
     int threads = 256;
     int ctas = 1;
     int stages = 2;
@@ -613,12 +614,13 @@ struct Plan {
 };
 
 const int kChainEP[] = {1, 2, 4, 8, 16};
-int chain_max_threads(int ep) { return ep <= 4 ? 256 : (ep <= 8 ? 512 : 640); }
+int chain_max_threads(int ep) { return ep <= 4 ? 256 : (ep <= 8 ? 384 : 320); }
 
 int chain_nv(int R) { return R + R * (R - 1) / 2 + R + 1; }
 
-int chain_smem(int64_t ld, int stages, int R, int T) {
-    return (int)(stages * ld * sizeof(double) + (stages + R) * 2 * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
+int chain_smem(int64_t ldc, int stages, int R, int T) {
+    return (int)(144 + (2 * chain_nv(R) + 2) * sizeof(double) + stages * ldc * sizeof(double) +
+                 stages * 2 * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
                  ((size_t)chain_nv(R) * T + chain_nv(R) + 1) * sizeof(double));
 }
 
@@ -631,20 +633,26 @@ size_t sync_smem(int64_t q, int64_t cw, int stages, int P, bool cluster) {
            nwarp * sizeof(double) + q * sizeof(double) + 8 * q * sizeof(int32_t);
 }
 
-void* chain_fn(int ep, int R) {
-    switch (ep * 100 + R) {
-        case 101: return (void*)chain_kernel<1, 1>;
-        case 104: return (void*)chain_kernel<1, 4>;
-        case 108: return (void*)chain_kernel<1, 8>;
-        case 201: return (void*)chain_kernel<2, 1>;
-        case 204: return (void*)chain_kernel<2, 4>;
-        case 208: return (void*)chain_kernel<2, 8>;
-        case 401: return (void*)chain_kernel<4, 1>;
-        case 402: return (void*)chain_kernel<4, 2>;
-        case 404: return (void*)chain_kernel<4, 4>;
-        case 801: return (void*)chain_kernel<8, 1>;
-        case 802: return (void*)chain_kernel<8, 2>;
-        case 1601: return (void*)chain_kernel<16, 1>;
+void* chain_fn(int ep, int R, int C) {
+    switch (C * 10000 + ep * 100 + R) {
+        case 10101: return (void*)chain_kernel<1, 1, 1>;
+        case 10104: return (void*)chain_kernel<1, 4, 1>;
+        case 10108: return (void*)chain_kernel<1, 8, 1>;
+        case 10201: return (void*)chain_kernel<2, 1, 1>;
+        case 10204: return (void*)chain_kernel<2, 4, 1>;
+        case 10208: return (void*)chain_kernel<2, 8, 1>;
+        case 10401: return (void*)chain_kernel<4, 1, 1>;
+        case 10402: return (void*)chain_kernel<4, 2, 1>;
+        case 10404: return (void*)chain_kernel<4, 4, 1>;
+        case 10801: return (void*)chain_kernel<8, 1, 1>;
+        case 10802: return (void*)chain_kernel<8, 2, 1>;
+        case 11601: return (void*)chain_kernel<16, 1, 1>;
+        case 20204: return (void*)chain_kernel<2, 4, 2>;
+        case 20402: return (void*)chain_kernel<4, 2, 2>;
+        case 20404: return (void*)chain_kernel<4, 4, 2>;
+        case 20801: return (void*)chain_kernel<8, 1, 2>;
+        case 20802: return (void*)chain_kernel<8, 2, 2>;
+        case 21601: return (void*)chain_kernel<16, 1, 2>;
         default: return nullptr;
     }
 }
@@ -661,7 +669,11 @@ constexpr size_t kSmemLimit = 227 * 1024;
 }  // namespace
 
 static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
-    const int64_t pairs = s->ld / 2;
+    // a worker is one CTA, or a CTA pair (thread-block cluster of 2, each CTA
+    // half the columns) when the rows are long and the pairs fit the SMs
+    int C = (s->ld >= 2048 && 2 * q <= s->sms) ? 2 : 1;
+    if (const char* e = getenv("KZ_CHAIN_PAIR")) C = atoi(e) == 2 && 2 * q <= s->sms ? 2 : 1;
+    const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
     int ep = 0, T = 0;
     if (p->threads > 0) {
@@ -682,31 +694,36 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         return fail(KZ_EINVAL, "n=%lld too large for the chain kernel", (long long)s->n);
     // rows per reduction: as many as registers allow (EP small) and the ring holds (> R rows)
     int R = ep <= 2 ? 8 : (ep == 4 ? 4 : (ep == 8 ? 2 : 1));
+    if (C == 2) R = std::min(R, 4);
     if (const char* e = getenv("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
-    const int64_t stage_bytes = s->ld * (int64_t)sizeof(double);
+    const int64_t ldc = s->ld / C;
+    const int64_t stage_bytes = ldc * (int64_t)sizeof(double);
     int stages = 0;
     for (;;) {
-        const int64_t fixed = chain_smem(s->ld, 0, R, T);
+        while (R > 1 && !chain_fn(ep, R, C)) R /= 2;
+        const int64_t fixed = chain_smem(ldc, 0, R, T);
         stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
+        if (const char* e = getenv("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
         if (stages >= R + 1 || R == 1) break;
         R = R > 4 ? 4 : (R > 2 ? 2 : 1);
     }
-    if (stages < 1 || (size_t)chain_smem(s->ld, stages, R, T) > kSmemLimit)
+    if (stages < 1 || (size_t)chain_smem(ldc, stages, R, T) > kSmemLimit)
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
-    if (!chain_fn(ep, R)) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d", ep, R);
+    void* fn = chain_fn(ep, R, C);
+    if (!fn) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d C=%d", ep, R, C);
     pl.kernel = KZ_KERNEL_CHAIN;
     pl.threads = T;
     pl.ep = ep;
     pl.rows = R;
+    pl.pair = C;
     pl.stages = stages;
-    pl.smem = chain_smem(s->ld, stages, R, T);
-    pl.ctas = (int)q;
-    void* fn = chain_fn(ep, R);
+    pl.smem = chain_smem(ldc, stages, R, T);
+    pl.ctas = (int)(q * C);
     KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    if (q > 1) {
+    if (pl.ctas > 1) {
         int per_sm = 0;
         KZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, T, pl.smem));
-        if ((int64_t)per_sm * s->sms < q)
+        if ((int64_t)per_sm * s->sms < pl.ctas)
             return fail(KZ_EINVAL, "q=%lld workers exceed the %d co-resident CTAs of the chain kernel", (long long)q,
                         per_sm * s->sms);
     }
@@ -787,11 +804,24 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
     cudaLaunchAttribute attr[1];
     cfg.attrs = attr;
     void* fn;
+    cudaLaunchAttribute attr2[2];
     if (pl.kernel == KZ_KERNEL_CHAIN) {
-        fn = chain_fn(pl.ep, pl.rows);
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.numAttrs = pl.ctas > 1 ? 1 : 0;
+        fn = chain_fn(pl.ep, pl.rows, pl.pair);
+        int na = 0;
+        if (pl.ctas > 1) {
+            attr2[na].id = cudaLaunchAttributeCooperative;
+            attr2[na].val.cooperative = 1;
+            ++na;
+        }
+        if (pl.pair == 2) {
+            attr2[na].id = cudaLaunchAttributeClusterDimension;
+            attr2[na].val.clusterDim.x = 2;
+            attr2[na].val.clusterDim.y = 1;
+            attr2[na].val.clusterDim.z = 1;
+            ++na;
+        }
+        cfg.attrs = attr2;
+        cfg.numAttrs = na;
     } else if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER) {
         fn = sync_fn(true, pl.lpr);
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -968,7 +998,17 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
         KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
         KZ_CUDA(cudaEventRecord(s->ev[2], st));
-        KZ_TRY(launch_solve(s, pl, args, st));
+        int lrc = launch_solve(s, pl, args, st);
+        if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && k == 0) {
+            // CTA-pair clusters not launchable cooperatively here: one CTA per worker
+            setenv("KZ_CHAIN_PAIR", "1", 1);
+            KZ_TRY(plan_chain(s, p, q, pl));
+            args.stages = pl.stages;
+            r->ctas = pl.ctas;
+            r->threads = pl.threads;
+            lrc = launch_solve(s, pl, args, st);
+        }
+        KZ_TRY(lrc);
         KZ_CUDA(cudaEventRecord(s->ev[3], st));
         KZ_CUDA(cudaMemcpyAsync(s->h_status, s->status.p, sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
         KZ_CUDA(cudaStreamSynchronize(st));

@@ -107,24 +107,41 @@ struct FalseT {
 
 template <int EP>
 struct ChainMaxThreads {
-    static constexpr int value = EP <= 4 ? 256 : (EP <= 8 ? 512 : 640);
+    static constexpr int value = EP <= 4 ? 256 : (EP <= 8 ? 384 : 320);
 };
 
-template <int EP, int R>
+template <int EP, int R, int C>
 __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     const int D = a.stages;
-    const int BS = D + R;  // (b, sq) slots
     const int64_t ld = a.ld, q = a.q, bs = a.bs;
+    // C == 2: a worker is a CTA pair (thread-block cluster); CTA h owns columns
+    // [h*ld/2, (h+1)*ld/2) and the two halves of every reduction are joined
+    // through distributed shared memory (st.async + mbarrier).
+    const int h = (C == 2) ? (int)cluster_rank() : 0;
+    const int64_t ldc = ld / C, cb = h * ldc;  // this CTA's columns
     ChainSmem sm;
-    sm.ring = reinterpret_cast<double*>(smem_raw);
-    sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ld);
-    sm.win = reinterpret_cast<int32_t*>(sm.bsq + BS);
+    unsigned long long* xbar = reinterpret_cast<unsigned long long*>(smem_raw);  // 2 exchange mbarriers
+    unsigned long long* full = xbar + 2;                                         // 16 row-stage mbarriers
+    double* xbuf = reinterpret_cast<double*>(smem_raw + 144);                     // 2 x NVC partner totals
+    sm.ring = xbuf + 2 * Blk<R>::NVC + 2;
+    sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ldc);
+    sm.win = reinterpret_cast<int32_t*>(sm.bsq + D);
     sm.scr = reinterpret_cast<double*>(sm.win + IDX_WINDOW);
     sm.tot = sm.scr + (size_t)Blk<R>::NVC * T;
+    if (tid == 0) {
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        for (int k = 0; k < D; ++k) mbar_init(&full[k], 1);
+        fence_mbarrier_init_cluster();
+    }
+    __syncthreads();
+    if (C == 2) cluster_sync_all();
+    int nex = 0;  // pair exchanges done
+    const unsigned partner = (unsigned)(h ^ 1);
 
-    const int64_t w = blockIdx.x;  // worker id
+    const int64_t w = blockIdx.x / C;  // worker id
     const int32_t* idx = a.idx + w * a.idx_stride;
     const double alpha = a.alphas[w];
     const int64_t total = a.count * bs;  // draws of this worker in the launch
@@ -133,50 +150,68 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     double v[2 * EP];
 #pragma unroll
     for (int p = 0; p < EP; ++p) {
-        const int64_t col = 2 * ((int64_t)p * T + tid);
+        const int64_t lc = 2 * ((int64_t)p * T + tid);
         double2 xv = make_double2(0.0, 0.0);
-        if (col < ld) xv = __ldcg(reinterpret_cast<const double2*>(a.x + col));
+        if (lc < ldc) xv = __ldcg(reinterpret_cast<const double2*>(a.x + cb + lc));
         v[2 * p] = xv.x;
         v[2 * p + 1] = xv.y;
     }
     for (int64_t e = tid; e < IDX_WINDOW && e < total; e += T) sm.win[e] = idx[e];
     __syncthreads();
 
-    // ---- issue side of the row ring ---------------------------------------------------
+    // ---- issue side of the row ring: one bulk copy (TMA engine) per row slice
+    // and one per (b, sq) pair, both completing the stage's mbarrier --------------
     int64_t issued = 0, win_next = IDX_WINDOW / 2;
-    int iss_stage = 0, iss_slot = 0;
+    int iss_stage = 0;
+    const unsigned row_bytes = (unsigned)(ldc * sizeof(double));
     auto issue_upto = [&](int64_t lim) {
         if (lim > total) lim = total;
         while (issued < lim) {
-            if (issued >= win_next) {  // refill the window half the issue pointer has left
-                for (int64_t e = win_next + IDX_WINDOW / 2 + tid; e < win_next + IDX_WINDOW && e < total; e += T)
-                    sm.win[e & (IDX_WINDOW - 1)] = idx[e];
+            if (issued >= win_next) {
+                // refill the window half the issue pointer has left.  Only warp 0
+                // touches the window (thread 0 is its only reader), so no other
+                // warp can overwrite entries thread 0 has yet to issue.
+                if (warp == 0) {
+                    for (int64_t e = win_next + IDX_WINDOW / 2 + lane; e < win_next + IDX_WINDOW && e < total; e += 32)
+                        sm.win[e & (IDX_WINDOW - 1)] = idx[e];
+                    __syncwarp();
+                }
                 win_next += IDX_WINDOW / 2;
-                __syncwarp();
             }
-            const int64_t i = sm.win[issued & (IDX_WINDOW - 1)];
-            const double* src = a.A + i * ld;
-            double* dst = sm.ring + (size_t)iss_stage * ld;
-#pragma unroll
-            for (int p = 0; p < EP; ++p) {
-                const int64_t col = 2 * ((int64_t)p * T + tid);
-                if (col < ld) cp_async16(dst + col, src + col);
+            if (tid == 0) {
+                const int64_t i = sm.win[issued & (IDX_WINDOW - 1)];
+                mbar_arrive_expect_tx(&full[iss_stage], row_bytes + 16u);
+                bulk_g2s(sm.ring + (size_t)iss_stage * ldc, a.A + i * ld + cb, row_bytes, &full[iss_stage]);
+                bulk_g2s(sm.bsq + iss_stage, bs2 + i, 16u, &full[iss_stage]);
             }
-            if (tid == 0) cp_async16(sm.bsq + iss_slot, bs2 + i);
-            cp_async_commit();
             ++issued;
             iss_stage = (iss_stage + 1 == D) ? 0 : iss_stage + 1;
-            iss_slot = (iss_slot + 1 == BS) ? 0 : iss_slot + 1;
         }
     };
 
     // direct ||v - x_ref||^2 over the CTA
+    // join the two halves of a CTA pair: totals += partner's totals (IEEE
+    // addition is commutative, so both CTAs hold the same bits)
+    auto pair_join = [&](double* vals, int nv) {
+        if (C != 2) return;
+        const int xp = nex & 1;
+        const unsigned ph = (unsigned)((nex >> 1) & 1);
+        ++nex;
+        if (tid == 0) mbar_arrive_expect_tx(&xbar[xp], (unsigned)(nv * sizeof(double)));
+        if (tid < nv)
+            st_async_f64(mapa_u32(smem_u32(xbuf + xp * Blk<R>::NVC + tid), partner), sm.tot[tid],
+                         mapa_u32(smem_u32(&xbar[xp]), partner));
+        mbar_wait_cluster(&xbar[xp], ph);
+        for (int i = 0; i < nv; ++i) vals[i] = __dadd_rn(vals[i], xbuf[xp * Blk<R>::NVC + i]);
+    };
+
     auto err_direct = [&]() {
         double e[1] = {0.0};
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
-            const int64_t col = 2 * ((int64_t)p * T + tid);
-            if (col < ld) {
+            const int64_t lc = 2 * ((int64_t)p * T + tid);
+            const int64_t col = cb + lc;
+            if (lc < ldc) {
                 const double2 r = __ldg(reinterpret_cast<const double2*>(a.xref + col));
                 const double d0 = v[2 * p] - r.x, d1 = v[2 * p + 1] - r.y;
                 e[0] = fma(d0, d0, e[0]);
@@ -184,6 +219,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             }
         }
         cta_reduce<1>(e, sm.scr, sm.tot, tid, T, nw);
+        pair_join(e, 1);
         return e[0];
     };
 
@@ -200,7 +236,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     int64_t outer_end = bs;       // q == 1: row count at which the current outer iteration completes
     int64_t kdone = a.k0;         // q == 1: outer iterations completed (global index)
     int64_t next_ck = ckpt_on ? (a.k0 / a.ckpt_every + 1) * a.ckpt_every : 0;
-    int c_stage = 0, c_slot = 0;  // ring position of row d
+    int c_stage = 0;              // ring stage of row d
+    unsigned c_par = 0;           // mbarrier phase parity of row d's stage
 
     // Process rows [d, d + Rp) of the chain (Rp <= R).  CHECK: stop rule before
     // rows with (d + r) % bs == 0 (q == 1 only).  Returns rows applied.
@@ -209,41 +246,60 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         constexpr int NV = CHECK ? Blk<R>::NVC : Blk<R>::NVN;
         const bool rec = a.dbg != nullptr && blockIdx.x == 0 && tid == 0 && nblk < 64;
         if (rec) a.dbg[nblk * 8 + 0] = clock64();
-        issue_upto(d + D);
         if (rec) a.dbg[nblk * 8 + 1] = clock64();
-        cp_async_wait_dyn((int)(issued - (d + Rp)));
-        if (rec) a.dbg[nblk * 8 + 2] = clock64();
         int stg[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int s0 = c_stage + r;
-            stg[r] = s0 >= D ? s0 - D : s0;
+            int s0 = c_stage + r;
+            unsigned pr = c_par;
+            if (s0 >= D) {
+                s0 -= D;
+                pr ^= 1u;
+            }
+            stg[r] = s0;
+            if (r < Rp) mbar_wait(&full[s0], pr);  // row d + r landed
+        }
+        if (rec) a.dbg[nblk * 8 + 2] = clock64();
+        // rows -> registers (kept for the update), (b, sq) -> lane r
+        double2 rr[R][EP];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int p = 0; p < EP; ++p) {
+                const int64_t lc = 2 * ((int64_t)p * T + tid);
+                rr[r][p] = (r < Rp && lc < ldc)
+                               ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldc + lc)
+                               : make_double2(0.0, 0.0);
+            }
+        double2 bq = make_double2(0.0, 1.0);
+        if (lane < Rp) {
+            int sl = c_stage + lane;
+            if (sl >= D) sl -= D;
+            bq = sm.bsq[sl];
         }
         double vals[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) vals[i] = 0.0;
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
-            const int64_t col = 2 * ((int64_t)p * T + tid);
-            if (col < ld) {
-                double2 rr[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    rr[r] = (r < Rp) ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ld + col)
-                                     : make_double2(0.0, 0.0);
+            const int64_t lc = 2 * ((int64_t)p * T + tid);
+            const int64_t col = cb + lc;
+            if (lc < ldc) {
                 const double vx = v[2 * p], vy = v[2 * p + 1];
 #pragma unroll
-                for (int r = 0; r < R; ++r) vals[r] = fma(rr[r].y, vy, fma(rr[r].x, vx, vals[r]));
+                for (int r = 0; r < R; ++r) vals[r] = fma(rr[r][p].y, vy, fma(rr[r][p].x, vx, vals[r]));
 #pragma unroll
                 for (int r = 1; r < R; ++r)
 #pragma unroll
                     for (int l = 0; l < r; ++l)
-                        vals[R + gidx(r, l)] = fma(rr[r].y, rr[l].y, fma(rr[r].x, rr[l].x, vals[R + gidx(r, l)]));
+                        vals[R + gidx(r, l)] =
+                            fma(rr[r][p].y, rr[l][p].y, fma(rr[r][p].x, rr[l][p].x, vals[R + gidx(r, l)]));
                 if (CHECK) {
                     const double2 xr = __ldg(reinterpret_cast<const double2*>(a.xref + col));
 #pragma unroll
                     for (int r = 0; r < R; ++r)
-                        vals[Blk<R>::NVN + r] = fma(rr[r].y, xr.y, fma(rr[r].x, xr.x, vals[Blk<R>::NVN + r]));
+                        vals[Blk<R>::NVN + r] =
+                            fma(rr[r][p].y, xr.y, fma(rr[r][p].x, xr.x, vals[Blk<R>::NVN + r]));
                     const double d0 = vx - xr.x, d1 = vy - xr.y;
                     vals[NV - 1] = fma(d1, d1, fma(d0, d0, vals[NV - 1]));
                 }
@@ -251,13 +307,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         }
         if (rec) a.dbg[nblk * 8 + 3] = clock64();
         cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw);
+        pair_join(vals, NV);
         if (rec) a.dbg[nblk * 8 + 4] = clock64();
-        // (b_r, sq_r): lane r loads its row's pair and forms 1/sq_r; shuffled to all
-        double2 bq = make_double2(0.0, 1.0);
-        if (lane < Rp) {
-            const int sl = c_slot + lane;
-            bq = sm.bsq[sl >= BS ? sl - BS : sl];
-        }
+        // (b_r, sq_r) sit in lane r; 1/sq_r formed there and shuffled to all
         const double inv_l = 1.0 / bq.y;
         double s[R];
         int Reff = Rp;
@@ -300,11 +352,10 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             if (r < Reff) {
 #pragma unroll
                 for (int p = 0; p < EP; ++p) {
-                    const int64_t col = 2 * ((int64_t)p * T + tid);
-                    if (col < ld) {
-                        const double2 rv = *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ld + col);
-                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], rv.x));
-                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], rv.y));
+                    const int64_t lc = 2 * ((int64_t)p * T + tid);
+                    if (lc < ldc) {
+                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], rr[r][p].x));
+                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], rr[r][p].y));
                     }
                 }
                 if (q == 1 && d + r + 1 == outer_end) {  // outer iteration kdone completes here
@@ -316,7 +367,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                         if (slot < a.ckpt_cap) {
 #pragma unroll
                             for (int p = 0; p < EP; ++p) {
-                                const int64_t col = 2 * ((int64_t)p * T + tid);
+                                const int64_t col = cb + 2 * ((int64_t)p * T + tid);
                                 if (col < a.n) a.ckpt[slot * a.n + col] = v[2 * p];
                                 if (col + 1 < a.n) a.ckpt[slot * a.n + col + 1] = v[2 * p + 1];
                             }
@@ -329,12 +380,15 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         ++nblk;
         d += Reff;
         c_stage += Reff;
-        if (c_stage >= D) c_stage -= D;
-        c_slot += Reff;
-        if (c_slot >= BS) c_slot -= BS;
+        if (c_stage >= D) {
+            c_stage -= D;
+            c_par ^= 1u;
+        }
+        issue_upto(d + D);  // stages of the applied rows are free (every thread holds them in registers)
         return Reff;
     };
 
+    issue_upto(D);
     if (q == 1) {
         // one chain: outer iteration k = rows [k*bs, (k+1)*bs); x = v after each
         while (d < total) {
@@ -374,8 +428,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             double* vw = a.V + w * ld;
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
-                const int64_t col = 2 * ((int64_t)p * T + tid);
-                if (col < ld) __stcg(reinterpret_cast<double2*>(vw + col), make_double2(v[2 * p], v[2 * p + 1]));
+                const int64_t lc = 2 * ((int64_t)p * T + tid);
+                if (lc < ldc) __stcg(reinterpret_cast<double2*>(vw + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
             }
             grid_barrier(a.barrier, (++epoch) * gridDim.x);
             const int64_t G = gridDim.x;
@@ -395,9 +449,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             grid_barrier(a.barrier, (++epoch) * gridDim.x);
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
-                const int64_t col = 2 * ((int64_t)p * T + tid);
-                if (col < ld) {
-                    const double2 xv = __ldcg(reinterpret_cast<const double2*>(a.x + col));
+                const int64_t lc = 2 * ((int64_t)p * T + tid);
+                if (lc < ldc) {
+                    const double2 xv = __ldcg(reinterpret_cast<const double2*>(a.x + cb + lc));
                     v[2 * p] = xv.x;
                     v[2 * p + 1] = xv.y;
                 }
@@ -405,15 +459,23 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             done = kk + 1;
         }
     }
-    cp_async_wait<0>();
+    // drain bulk copies still in flight (rows issued ahead of a stop) before exit
+    for (int64_t row = d; row < issued; ++row) {
+        mbar_wait(&full[c_stage], c_par);
+        if (++c_stage == D) {
+            c_stage = 0;
+            c_par ^= 1u;
+        }
+    }
     if (q == 1) {
         double* dst = a.partial ? a.partial : a.x;
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
-            const int64_t col = 2 * ((int64_t)p * T + tid);
-            if (col < ld) __stcg(reinterpret_cast<double2*>(dst + col), make_double2(v[2 * p], v[2 * p + 1]));
+            const int64_t lc = 2 * ((int64_t)p * T + tid);
+            if (lc < ldc) __stcg(reinterpret_cast<double2*>(dst + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
         }
     }
+    if (C == 2) cluster_sync_all();  // no DSMEM traffic may target an exited CTA
     if (blockIdx.x == 0 && tid == 0) {
         a.status->iters_done = done;
         a.status->converged = conv;
@@ -422,19 +484,25 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     }
 }
 
-#define KZ_CHAIN(EP, R) template __global__ void chain_kernel<EP, R>(SolveArgs);
-KZ_CHAIN(1, 1)
-KZ_CHAIN(1, 4)
-KZ_CHAIN(1, 8)
-KZ_CHAIN(2, 1)
-KZ_CHAIN(2, 4)
-KZ_CHAIN(2, 8)
-KZ_CHAIN(4, 1)
-KZ_CHAIN(4, 2)
-KZ_CHAIN(4, 4)
-KZ_CHAIN(8, 1)
-KZ_CHAIN(8, 2)
-KZ_CHAIN(16, 1)
+#define KZ_CHAIN(EP, R, C) template __global__ void chain_kernel<EP, R, C>(SolveArgs);
+KZ_CHAIN(1, 1, 1)
+KZ_CHAIN(1, 4, 1)
+KZ_CHAIN(1, 8, 1)
+KZ_CHAIN(2, 1, 1)
+KZ_CHAIN(2, 4, 1)
+KZ_CHAIN(2, 8, 1)
+KZ_CHAIN(4, 1, 1)
+KZ_CHAIN(4, 2, 1)
+KZ_CHAIN(4, 4, 1)
+KZ_CHAIN(8, 1, 1)
+KZ_CHAIN(8, 2, 1)
+KZ_CHAIN(16, 1, 1)
+KZ_CHAIN(2, 4, 2)
+KZ_CHAIN(4, 2, 2)
+KZ_CHAIN(4, 4, 2)
+KZ_CHAIN(8, 1, 2)
+KZ_CHAIN(8, 2, 2)
+KZ_CHAIN(16, 1, 2)
 #undef KZ_CHAIN
 
 }  // namespace kz

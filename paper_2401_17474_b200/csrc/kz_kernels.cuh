@@ -42,8 +42,8 @@ struct SolveArgs {
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
-// R = rows resolved per CTA reduction (Gram-corrected block).
-template <int EP, int R>
+// R = rows resolved per CTA reduction (Gram-corrected block), C = CTAs per worker.
+template <int EP, int R, int C>
 __global__ void chain_kernel(SolveArgs a);
 
 // sync kernel: column-sliced (RKA, RKAB bs=1).  CLUSTER: reduce via DSMEM.
