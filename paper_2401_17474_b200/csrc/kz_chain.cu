@@ -167,25 +167,33 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     auto issue_upto = [&](int64_t lim) {
         if (lim > total) lim = total;
         while (issued < lim) {
+            // rows [issued, issued + cnt) without crossing a window refill point
+            int64_t stop = lim < win_next ? lim : win_next;
             if (issued >= win_next) {
                 // refill the window half the issue pointer has left.  Only warp 0
-                // touches the window (thread 0 is its only reader), so no other
-                // warp can overwrite entries thread 0 has yet to issue.
+                // touches the window (its lanes are the only readers), so no other
+                // warp can overwrite entries that are still to be issued.
                 if (warp == 0) {
                     for (int64_t e = win_next + IDX_WINDOW / 2 + lane; e < win_next + IDX_WINDOW && e < total; e += 32)
                         sm.win[e & (IDX_WINDOW - 1)] = idx[e];
                     __syncwarp();
                 }
                 win_next += IDX_WINDOW / 2;
+                stop = lim < win_next ? lim : win_next;
             }
-            if (tid == 0) {
-                const int64_t i = sm.win[issued & (IDX_WINDOW - 1)];
-                mbar_arrive_expect_tx(&full[iss_stage], row_bytes + 16u);
-                bulk_g2s(sm.ring + (size_t)iss_stage * ldc, a.A + i * ld + cb, row_bytes, &full[iss_stage]);
-                bulk_g2s(sm.bsq + iss_stage, bs2 + i, 16u, &full[iss_stage]);
+            const int cnt = (int)(stop - issued);
+            // lane l of warp 0 issues row issued + l: arm its stage, then two bulk copies
+            if (warp == 0 && lane < cnt) {
+                int st = iss_stage + lane;
+                if (st >= D) st -= D;
+                const int64_t i = sm.win[(issued + lane) & (IDX_WINDOW - 1)];
+                mbar_arrive_expect_tx(&full[st], row_bytes + 16u);
+                bulk_g2s(sm.ring + (size_t)st * ldc, a.A + i * ld + cb, row_bytes, &full[st]);
+                bulk_g2s(sm.bsq + st, bs2 + i, 16u, &full[st]);
             }
-            ++issued;
-            iss_stage = (iss_stage + 1 == D) ? 0 : iss_stage + 1;
+            issued += cnt;
+            iss_stage += cnt;
+            if (iss_stage >= D) iss_stage -= D;
         }
     };
 
