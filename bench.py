@@ -240,6 +240,66 @@ def run_b200_sharded(args, name, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def extra_workloads(device, peak, steps=3):
+    """The other BASELINE configurations on this GPU (same metric; fixed budgets for
+    the large ones, time-to-eps for c0 / c2).  Kernel-time roofline per workload."""
+    import torch
+
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, SolverConfig, generate_mother, run_solver
+
+    out = []
+
+    def measure(tag, ds, n, cfg, budget, desc):
+        run_solver(ds, cfg, budget=budget)  # warm-up
+        torch.cuda.synchronize()
+        rows, kms, lms, its = 0, 0.0, 0.0, []
+        for k in range(steps):
+            r = run_solver(ds, cfg.replace(base_seed=k), budget=budget)
+            rows += r.gpu["rows_projected"]
+            kms += r.gpu["kernel_ms"]
+            lms += r.gpu["loop_ms"]
+            its.append(r.iterations)
+        gbs = rows * 8 * n / (kms / 1e3) / 1e9
+        out.append({"workload": tag, "desc": desc, "rows_per_s": rows / (lms / 1e3),
+                    "ms_per_step": lms / steps, "iterations": its, "kernel": r.gpu["kernel"],
+                    "ctas": r.gpu["ctas"], "threads": r.gpu["threads"],
+                    "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak}})
+
+    try:
+        ds = DeviceSystem(m=160000, n=20000, device=device)
+        ds.generate_counter(0)
+        measure("c3_rkab_bs1000", ds, 20000, SolverConfig(variant="rkab", q=64, block_size=1000,
+                sampling_scheme="distributed", device=device), 1,
+                "c3: 160000x20000 counter-keyed, RKAB q=64 bs=1000 distributed, 1 outer iteration per step")
+        measure("c3_rka", ds, 20000, SolverConfig(variant="rka", q=64, sampling_scheme="distributed", device=device),
+                200, "c3: 160000x20000 counter-keyed, RKA q=64 distributed, 200 iterations per step")
+        measure("c3_rkab_bs1", ds, 20000, SolverConfig(variant="rkab", q=64, block_size=1,
+                sampling_scheme="distributed", device=device), 200,
+                "c3: RKAB q=64 bs=1 (= RKA) distributed, 200 iterations per step")
+        ds.close()
+        s4 = generate_mother(GeneratorConfig(m_max=80000, n_max=2000, seed=0))
+        ds = DeviceSystem(s4, device=device)
+        measure("c4_rka_q64", ds, 2000, SolverConfig(variant="rka", q=64, device=device), 2000,
+                "c4 shape 80000x2000: RKA q=64, 2000 iterations per step")
+        measure("c4_rka_q512", ds, 2000, SolverConfig(variant="rka", q=512, device=device), 500,
+                "c4 shape 80000x2000: RKA q=512, 500 iterations per step")
+        measure("c4_rk_q1", ds, 2000, SolverConfig(variant="rk", device=device), 20000,
+                "c4 shape 80000x2000: RK (q=1), 20000 iterations per step")
+        ds.close()
+        s2 = generate_mother(GeneratorConfig(m_max=80000, n_max=1000, seed=0))
+        ds = DeviceSystem(s2, device=device)
+        measure("c2", ds, 1000, SolverConfig(variant="rkab", q=64, block_size=500, device=device), None,
+                "c2: RKAB q=64 bs=500 80000x1000, solve to eps")
+        ds.close()
+        s0 = generate_mother(GeneratorConfig(m_max=2000, n_max=50, seed=0))
+        ds = DeviceSystem(s0, device=device)
+        measure("c0", ds, 50, SolverConfig(variant="rk", device=device), None, "c0: RK 2000x50, solve to eps")
+        ds.close()
+    except Exception as exc:  # extras must never sink the headline line
+        out.append({"error": repr(exc)})
+    return out
+
+
 def run_b200(args, name, rank, world, local_rank):
     if world > 1:
         return run_b200_sharded(args, name, rank, world, local_rank)
@@ -331,6 +391,8 @@ def run_b200(args, name, rank, world, local_rank):
         "e2e": {"value": e2e_rows / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
     }
+    if not args.no_extra:
+        line["extra_workloads"] = extra_workloads(local_rank, peak)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, system, kw)
     print(json.dumps(line), flush=True)
@@ -344,6 +406,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE workloads")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
