@@ -174,6 +174,11 @@ struct kz_system {
     std::vector<int64_t> custom_lo, custom_len;  // KZ_SCHEME_RANGES
     bool has_xref = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // TMA descriptors of A (box = one CTA's column slice) and of the packed (b, sq) pairs
+    CUtensorMap tmA{}, tmB{};
+    int tm_box = 0;
+    const void* tm_a = nullptr;
+    const void* tm_b = nullptr;
 };
 
 extern "C" const char* kz_last_error(void) { return g_err.c_str(); }
@@ -610,6 +615,9 @@ struct Plan {
     int stages = 2;
     int ep = 1;         // chain: pairs per thread
     int lpr = 8;        // sync: lanes per row
+    int cluster = 1;    // sync (cluster mode): CTAs per thread-block cluster
+    bool tma = false;   // sync: the TMA-gather rka kernel
+    int lg = 32, epl = 1, box = 0;  // rka kernel: lanes per row group, pairs per lane, TMA box width
     size_t smem = 0;
 };
 
@@ -665,6 +673,7 @@ void* sync_fn(bool cluster, int lpr) {
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
+constexpr int MAXG_CLUSTERS = 10;  // = MAXG in kz_sync.cu
 
 }  // namespace
 
@@ -733,28 +742,43 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
 static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, Plan& pl) {
     pl.threads = 256;
     if (q > 512) return fail(KZ_EINVAL, "q=%lld exceeds the sync kernel's 512 workers", (long long)q);
-    int P;
+    // cluster mode: G clusters of Pc CTAs (column slices over all G*Pc CTAs);
+    // grid mode: P CTAs behind a grid barrier
+    int Pc = 16, G = 1, P = 0;
     if (cluster) {
-        P = p->ctas > 0 ? p->ctas : 16;
-        if (P > 16) P = 16;
+        if (p->ctas > 16) {
+            G = p->ctas / 16;
+        } else if (p->ctas > 0) {
+            Pc = p->ctas;
+        } else {
+            // several clusters once every CTA of one cluster would carry > 128 columns
+            G = (int)std::max<int64_t>(1, std::min<int64_t>(MAXG_CLUSTERS, s->ld / (16 * 128)));
+        }
+        if (const char* e = getenv("KZ_SYNC_CLUSTERS")) G = std::max(1, std::min(MAXG_CLUSTERS, atoi(e)));
     } else {
         P = p->ctas > 0 ? p->ctas : s->sms;
     }
-    // shrink P (cluster) / grow P (grid) until the slice ring fits and the launch is schedulable
+    // grow G / P until the slice ring fits; shrink until the launch is schedulable
     for (;;) {
-        if (P < 1) return fail(KZ_EINVAL, "no feasible sync-kernel configuration for q=%lld n=%lld", (long long)q,
-                               (long long)s->n);
+        if (cluster) P = Pc * G;
+        if (P < 1 || Pc < 1) return fail(KZ_EINVAL, "no feasible sync-kernel configuration for q=%lld n=%lld",
+                                         (long long)q, (long long)s->n);
         const int64_t cw = (((s->ld + P - 1) / P) + 1) & ~(int64_t)1;
         int stages = 4;
-        while (stages > 2 && sync_smem(q, cw, stages, P, cluster) > 200 * 1024) --stages;
-        if (sync_smem(q, cw, stages, P, cluster) > kSmemLimit) {
-            if (cluster) return fail(KZ_EINVAL, "q=%lld row slices do not fit a cluster CTA", (long long)q);
+        while (stages > 2 && sync_smem(q, cw, stages, cluster ? Pc : P, cluster) > 200 * 1024) --stages;
+        if (sync_smem(q, cw, stages, cluster ? Pc : P, cluster) > kSmemLimit) {
+            if (cluster) {
+                if (G >= MAXG_CLUSTERS || Pc < 16)
+                    return fail(KZ_EINVAL, "q=%lld row slices do not fit the cluster CTAs", (long long)q);
+                ++G;
+                continue;
+            }
             if (P >= 4 * s->sms) return fail(KZ_EINVAL, "q=%lld too large for the sync kernel", (long long)q);
             P *= 2;  // thinner slices, several CTAs per SM
             continue;
         }
         pl.stages = stages;
-        pl.smem = sync_smem(q, cw, stages, P, cluster);
+        pl.smem = sync_smem(q, cw, stages, cluster ? Pc : P, cluster);
         pl.lpr = cw > 64 ? 32 : (q > 32 ? 4 : 8);
         void* fn = sync_fn(cluster, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -766,7 +790,7 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
             cfg.dynamicSmemBytes = pl.smem;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = P;
+            attr[0].val.clusterDim.x = Pc;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
@@ -775,8 +799,12 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
             cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
             if (e != cudaSuccess || nclusters < 1) {
                 cudaGetLastError();
-                if (P == 1) return fail(KZ_EINVAL, "cluster kernel not schedulable");
-                P /= 2;
+                if (Pc == 1) return fail(KZ_EINVAL, "cluster kernel not schedulable");
+                Pc /= 2;
+                continue;
+            }
+            if (nclusters < G) {  // every cluster must be co-resident (they poll each other)
+                G = nclusters;
                 continue;
             }
         } else {
@@ -791,8 +819,178 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
         }
         pl.kernel = cluster ? KZ_KERNEL_SYNC_CLUSTER : KZ_KERNEL_SYNC_GRID;
         pl.ctas = P;
+        pl.cluster = cluster ? Pc : 1;
         return KZ_OK;
     }
+}
+
+namespace {
+
+template <bool TM>
+void* rka_fn_t(int lg, int epl) {
+    if (lg == 8) return (void*)rka_kernel<8, 1, TM>;
+    if (lg == 16) return (void*)rka_kernel<16, 1, TM>;
+    switch (epl) {
+        case 1: return (void*)rka_kernel<32, 1, TM>;
+        case 2: return (void*)rka_kernel<32, 2, TM>;
+        case 3: return (void*)rka_kernel<32, 3, TM>;
+        case 4: return (void*)rka_kernel<32, 4, TM>;
+        default: return nullptr;
+    }
+}
+
+// the timing variant (per-phase clock stamps) only under KZ_PHASE_TIMING
+void* rka_fn(int lg, int epl) {
+    return getenv("KZ_PHASE_TIMING") ? rka_fn_t<true>(lg, epl) : rka_fn_t<false>(lg, epl);
+}
+
+size_t rka_smem(int64_t q, int box, int stages, int Pc) {
+    const int64_t q4 = (q + 3) & ~(int64_t)3, q1p = (q + 2) & ~(int64_t)1;
+    const size_t stage = (size_t)q4 * box * sizeof(double) + (size_t)q4 * 32;
+    return 256 + (size_t)stages * stage + (size_t)(2 * Pc * q1p + RKA_NW * box + q4 + q) * sizeof(double);
+}
+
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+TmapEncodeFn tmap_encode() {
+    static TmapEncodeFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = (TmapEncodeFn)ptr;
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+}  // namespace
+
+// Tensor maps for the rka kernel: A as (columns = ld, rows = m) with a box of
+// `box` columns x 1 row (gather4 fetches 4 rows per instruction); the packed
+// (b_i, ||a_i||^2) pairs as (2, m) with a 2 x 1 box.
+static int ensure_tmaps(kz_system* s, int box) {
+    if (s->tm_box == box && s->tm_a == s->A.p && s->tm_b == s->bs2.p) return KZ_OK;
+    TmapEncodeFn enc = tmap_encode();
+    if (!enc) return fail(KZ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint32_t es[2] = {1, 1};
+    {
+        const cuuint64_t dims[2] = {(cuuint64_t)s->ld, (cuuint64_t)s->m};
+        const cuuint64_t strides[1] = {(cuuint64_t)s->ld * sizeof(double)};
+        const cuuint32_t bx[2] = {(cuuint32_t)box, 1};
+        CUresult r = enc(&s->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)s->A.p, dims, strides, bx, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(KZ_ECUDA, "tensor map of A failed (%d)", (int)r);
+    }
+    {
+        const cuuint64_t dims[2] = {2, (cuuint64_t)s->m};
+        const cuuint64_t strides[1] = {2 * sizeof(double)};
+        const cuuint32_t bx[2] = {2, 1};
+        CUresult r = enc(&s->tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)s->bs2.p, dims, strides, bx, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(KZ_ECUDA, "tensor map of (b, sq) failed (%d)", (int)r);
+    }
+    s->tm_box = box;
+    s->tm_a = s->A.p;
+    s->tm_b = s->bs2.p;
+    return KZ_OK;
+}
+
+// rka kernel plan: G clusters of Pc CTAs; every CTA's slice <= 256 columns (one
+// TMA box) and at least two ring stages.
+static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
+    if (getenv("KZ_SYNC_V5")) return fail(KZ_EINVAL, "rka kernel disabled (KZ_SYNC_V5)");
+    if (q > 512) return fail(KZ_EINVAL, "q=%lld exceeds the rka kernel's 512 workers", (long long)q);
+    const int64_t ld = s->ld;
+    int Pc = 16, G = 1;
+    if (p->ctas > 16) {
+        G = p->ctas / 16;
+    } else if (p->ctas > 0) {
+        Pc = 1;
+        while (2 * Pc <= p->ctas) Pc *= 2;
+    } else {
+        // several clusters once a CTA would stage more than ~24 KB of rows per iteration
+        const double bytes = (double)q * (double)ld * sizeof(double);
+        G = (int)std::ceil(bytes / (16.0 * 24 * 1024));
+    }
+    if (const char* e = getenv("KZ_SYNC_CLUSTERS")) G = atoi(e);
+    G = std::max<int>(G, (int)((ld + Pc * 256 - 1) / (Pc * 256)));
+    G = std::max(1, std::min(RKA_MAXG, G));
+    int gcap = RKA_MAXG;
+    for (int guard = 0; guard < 64; ++guard) {
+        if (G > gcap) return fail(KZ_EINVAL, "rka kernel: %d clusters needed, %d co-resident", G, gcap);
+        const int P = Pc * G;
+        const int64_t cw = (((ld + P - 1) / P) + 1) & ~(int64_t)1;
+        const int box = (int)((cw + 3) & ~(int64_t)3);
+        if (box > 256) {
+            ++G;
+            continue;
+        }
+        const int npairs = box / 2;
+        const int lg = npairs <= 8 ? 8 : (npairs <= 16 ? 16 : 32);
+        const int epl = lg == 32 ? (npairs + 31) / 32 : 1;
+        const size_t stage = (size_t)((q + 3) & ~3) * box * sizeof(double) + (size_t)((q + 3) & ~3) * 32;
+        const size_t fixed = rka_smem(q, box, 0, Pc);
+        int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);
+        if (const char* e = getenv("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+        if (stages < 2 || rka_smem(q, box, stages, Pc) > kSmemLimit) {
+            if (Pc > 2 && 2 * (size_t)Pc * (q + 2) * sizeof(double) > 32 * 1024) {
+                Pc /= 2;
+                G *= 2;
+            } else {
+                ++G;
+            }
+            continue;
+        }
+        void* fn = rka_fn(lg, epl);
+        if (!fn) return fail(KZ_EINVAL, "no rka kernel for LG=%d EPL=%d", lg, epl);
+        const size_t smem = rka_smem(q, box, stages, Pc);
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(P);
+        cfg.blockDim = dim3(RKA_NT);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = Pc;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+        if (e != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            if (Pc == 1) return fail(KZ_EINVAL, "rka kernel not schedulable");
+            Pc /= 2;
+            G *= 2;
+            continue;
+        }
+        if (nclusters < G) {  // every cluster must be co-resident (they poll each other)
+            gcap = std::min(gcap, nclusters);
+            G = gcap;
+            continue;
+        }
+        pl.kernel = KZ_KERNEL_SYNC_CLUSTER;
+        pl.tma = true;
+        pl.threads = RKA_NT;
+        pl.ctas = P;
+        pl.cluster = Pc;
+        pl.stages = stages;
+        pl.smem = smem;
+        pl.lg = lg;
+        pl.epl = epl;
+        pl.box = box;
+        return KZ_OK;
+    }
+    return fail(KZ_EINVAL, "no feasible rka kernel configuration for q=%lld n=%lld", (long long)q, (long long)s->n);
 }
 
 static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStream_t st) {
@@ -823,19 +1021,27 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
         cfg.attrs = attr2;
         cfg.numAttrs = na;
     } else if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER) {
-        fn = sync_fn(true, pl.lpr);
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = pl.ctas;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.numAttrs = 1;
+        fn = pl.tma ? rka_fn(pl.lg, pl.epl) : sync_fn(true, pl.lpr);
+        int na = 0;
+        attr2[na].id = cudaLaunchAttributeClusterDimension;
+        attr2[na].val.clusterDim.x = pl.cluster;
+        attr2[na].val.clusterDim.y = 1;
+        attr2[na].val.clusterDim.z = 1;
+        ++na;
+        if (pl.ctas > pl.cluster) {  // clusters poll each other: all must be co-resident
+            attr2[na].id = cudaLaunchAttributeCooperative;
+            attr2[na].val.cooperative = 1;
+            ++na;
+        }
+        cfg.attrs = attr2;
+        cfg.numAttrs = na;
     } else {
         fn = sync_fn(false, pl.lpr);
         attr[0].id = cudaLaunchAttributeCooperative;
         attr[0].val.cooperative = 1;
         cfg.numAttrs = 1;
     }
-    void* kargs[] = {&args};
+    void* kargs[] = {&args, &s->tmA, &s->tmB};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, kargs);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (e != cudaSuccess) {
@@ -896,15 +1102,15 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         if (q == 1 || bs > 1) {
             kern = KZ_KERNEL_CHAIN;
         } else {
-            const double bytes_per_iter = (double)q * s->ld * sizeof(double);
-            kern = bytes_per_iter <= 4.0 * 1024 * 1024 ? KZ_KERNEL_SYNC_CLUSTER : KZ_KERNEL_SYNC_GRID;
+            kern = KZ_KERNEL_SYNC_CLUSTER;  // one or several clusters; grid barrier as the fallback
         }
     }
     if (kern == KZ_KERNEL_CHAIN) {
         KZ_TRY(plan_chain(s, p, q, pl));
     } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {
         if (bs != 1) return fail(KZ_EINVAL, "the sync kernels run RKA / RKAB with block_size 1 only");
-        int rc = plan_sync(s, p, q, kern == KZ_KERNEL_SYNC_CLUSTER, pl);
+        int rc = kern == KZ_KERNEL_SYNC_CLUSTER ? plan_rka(s, p, q, pl) : KZ_EINVAL;
+        if (rc != KZ_OK) rc = plan_sync(s, p, q, kern == KZ_KERNEL_SYNC_CLUSTER, pl);
         if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && p->kernel == KZ_KERNEL_AUTO)
             rc = plan_sync(s, p, q, false, pl);
         KZ_TRY(rc);
@@ -949,6 +1155,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.eps = p->epsilon;
     args.use_stop = stop_mode ? 1 : 0;
     args.stages = pl.stages;
+    args.box = pl.box;
+    if (pl.tma) KZ_TRY(ensure_tmaps(s, pl.box));
     const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
     args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;
     if (phase_timing) {
@@ -997,6 +1205,10 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         args.idx_stride = c * bs;
         args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
         KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
+        if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER && pl.ctas > pl.cluster) {  // tags restart at 1 per launch
+            KZ_CUDA(cudaMemsetAsync(s->part.p, 0, 4 * (size_t)(pl.ctas / pl.cluster) * (q + 1) * sizeof(double), st));
+            KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
+        }
         KZ_CUDA(cudaEventRecord(s->ev[2], st));
         int lrc = launch_solve(s, pl, args, st);
         if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && k == 0) {
@@ -1008,6 +1220,17 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             r->threads = pl.threads;
             lrc = launch_solve(s, pl, args, st);
         }
+        if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_SYNC_CLUSTER && pl.ctas > pl.cluster && k == 0 &&
+            p->kernel == KZ_KERNEL_AUTO) {
+            // several clusters not launchable cooperatively here: grid-barrier kernel
+            KZ_TRY(plan_sync(s, p, q, false, pl));
+            KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
+            args.part = s->part.p;
+            args.stages = pl.stages;
+            r->kernel_used = pl.kernel;
+            r->ctas = pl.ctas;
+            lrc = launch_solve(s, pl, args, st);
+        }
         KZ_TRY(lrc);
         KZ_CUDA(cudaEventRecord(s->ev[3], st));
         KZ_CUDA(cudaMemcpyAsync(s->h_status, s->status.p, sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
@@ -1016,6 +1239,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         cudaEventElapsedTime(&ms, s->ev[2], s->ev[3]);
         kernel_ms += ms;
         const SolveStatus hs = *s->h_status;
+        if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER && pl.ctas > pl.cluster && hs.aborted)
+            return fail(KZ_ECUDA, "cross-cluster exchange timed out (clusters not co-resident)");
         k += hs.iters_done;
         evals += hs.checks;
         if (hs.checks > 0) err = hs.err;

@@ -187,6 +187,57 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// ---- flag-in-data ("LL") words for cross-cluster exchange -----------------
+// A double travels as two 64-bit words {low 32 bits, tag} and {high 32 bits,
+// tag}; each aligned 64-bit store is single-copy atomic, so a reader that sees
+// the expected tag in both words holds the value -- no fence, no barrier.
+__device__ __forceinline__ void ll_store(unsigned long long* p, double v, unsigned tag) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long w0 = (bits & 0xffffffffull) | ((unsigned long long)tag << 32);
+    const unsigned long long w1 = (bits >> 32) | ((unsigned long long)tag << 32);
+    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ void ll_load_raw(const unsigned long long* p, unsigned long long& w0,
+                                            unsigned long long& w1) {
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
+__device__ __forceinline__ bool ll_ok(unsigned long long w0, unsigned long long w1, unsigned tag) {
+    return (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag;
+}
+__device__ __forceinline__ double ll_value(unsigned long long w0, unsigned long long w1) {
+    return __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+}
+// Sum of G tagged values p[0], p[stride], ... in fixed order g = 0..G-1.
+// All G loads are in flight together; stragglers are re-polled.  A spin
+// beyond 2^22 polls sets *abort (reported to the host) instead of hanging, and
+// once *abort is set every other spinner gives up within 1024 polls.
+template <int GMAX>
+__device__ __noinline__ double ll_sum(const unsigned long long* p, int stride, int G, unsigned tag, int* abort) {
+    unsigned long long w0[GMAX], w1[GMAX];
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g)
+        if (g < G) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+    double s = 0.0;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) {
+        if (g < G) {
+            unsigned spins = 0;
+            while (!ll_ok(w0[g], w1[g], tag)) {
+                ++spins;
+                if ((spins & 1023u) == 0 && *(volatile int*)abort) break;
+                if (spins > (1u << 22)) {
+                    atomicExch(abort, 1);
+                    break;
+                }
+                ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+            }
+            const double v = ll_value(w0[g], w1[g]);
+            s = (g == 0) ? v : __dadd_rn(s, v);
+        }
+    }
+    return s;
+}
+
 __device__ __forceinline__ unsigned cluster_rank() {
     unsigned r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -258,6 +309,42 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
             : "r"(a), "r"(parity)
             : "memory");
     }
+}
+
+}  // namespace kz
+
+namespace kz {
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+    unsigned done;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
+// TMA gather4: rows r0..r3 of a 2-D tensor map, columns [c0, c0 + box), into
+// four consecutive box-wide rows of shared memory; completes the bytes on `bar`.
+__device__ __forceinline__ void tma_gather4(unsigned dst, const void* map, int c0, int r0, int r1, int r2, int r3,
+                                            unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
+
+// Named barrier over the first `count` threads (the compute warps).
+__device__ __forceinline__ void named_sync(unsigned id, unsigned count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
 }  // namespace kz

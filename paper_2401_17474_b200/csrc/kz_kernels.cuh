@@ -1,6 +1,8 @@
 // kz_kernels.cuh -- kernel argument blocks and launch declarations.
 #pragma once
 
+#include <cuda.h>
+
 #include "kz_common.cuh"
 
 namespace kz {
@@ -11,6 +13,8 @@ struct SolveStatus {
     int converged;         // stop rule met (||x - x_ref||^2 < eps)
     int checks;            // stop-rule evaluations in this launch
     double err;            // last evaluated ||x - x_ref||^2
+    int aborted;           // cross-cluster exchange timed out (co-residency violated)
+    int pad;
 };
 
 // Shared by both solve kernels.
@@ -39,6 +43,7 @@ struct SolveArgs {
     int stages;            // cp.async ring depth
     long long* dbg;        // optional phase timestamps (KZ_PHASE_TIMING=1)
     int ablate;            // debug: bit mask of phases to skip (KZ_ABLATE), timing experiments only
+    int box;               // rka kernel: TMA box width (columns of the row slice)
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
@@ -49,6 +54,16 @@ __global__ void chain_kernel(SolveArgs a);
 // sync kernel: column-sliced (RKA, RKAB bs=1).  CLUSTER: reduce via DSMEM.
 template <bool CLUSTER, int LPR>
 __global__ void sync_kernel(SolveArgs a);
+
+// rka kernel: column-sliced RKA with TMA-gather row staging by a producer warp,
+// 8 compute warps, DSMEM exchange inside each cluster and tagged global words
+// between clusters.  LG = lanes per row group, EPL = column pairs per lane.
+constexpr int RKA_NW = 8;                  // compute warps
+constexpr int RKA_NT = (RKA_NW + 1) * 32;  // + the producer warp
+constexpr int RKA_MAXG = 10;               // clusters exchanging through tagged words
+template <int LG, int EPL, bool TIMING>
+__global__ void rka_kernel(const __grid_constant__ SolveArgs a, const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB);
 
 __global__ void row_sqnorm_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
                                   double* __restrict__ sq, unsigned long long* __restrict__ first_zero);

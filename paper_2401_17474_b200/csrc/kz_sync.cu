@@ -16,9 +16,14 @@
 //      its lanes with shuffles and every lane pushes them (st.async, 16 B)
 //      into one peer CTA's receive buffer, completing that CTA's mbarrier
 //      transaction count; each CTA then waits on its own mbarrier -- no
-//      cluster barrier, no GPU-scope fence.  Grid mode: global memory and a
-//      grid barrier.  The partial of ||x - x_ref||^2 rides along as entry q
-//      (its per-warp pieces come from the previous iteration's combine);
+//      cluster barrier, no GPU-scope fence.  With G > 1 clusters (column
+//      slices over all G x Pc CTAs) each cluster's rank-0 CTA then publishes
+//      its cluster totals as tagged 64-bit words (value halves + iteration
+//      tag, single-copy atomic) and every CTA polls the G words of its
+//      workers: one L2 round trip, no grid barrier, no fence.  Grid mode:
+//      global memory and a grid barrier.  The partial of ||x - x_ref||^2
+//      rides along as entry q (its per-warp pieces come from the previous
+//      iteration's combine);
 //   4. scales: warp w owns the w-th contiguous block of workers; its lanes
 //      add that block's P partials with one fixed tree (bit-identical in
 //      every CTA) and form s_t = alpha (b - d) / ||a||^2;
@@ -39,6 +44,7 @@ constexpr int MAXP_TREE = 16;     // cluster size bound for the partial-sum tree
 constexpr int IDX_PER_THREAD = 4;
 constexpr int CPW = 32 / NW;      // columns per warp per combine round
 constexpr int SEG_MAX = 64;       // workers per warp block
+constexpr int MAXG = 10;          // clusters exchanging through tagged global words
 }  // namespace
 
 template <bool CLUSTER, int LPR>
@@ -47,8 +53,13 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = a.stages;
     const int ld = (int)a.ld, q = (int)a.q;
-    const int P = CLUSTER ? (int)cluster_size() : (int)gridDim.x;
-    const int c = CLUSTER ? (int)cluster_rank() : (int)blockIdx.x;
+    const int P = (int)gridDim.x;  // column slices
+    const int c = (int)blockIdx.x;
+    // exchange group: the thread-block cluster (CLUSTER) or the whole grid; with
+    // several clusters (G > 1) their totals meet through tagged global words
+    const int Pc = CLUSTER ? (int)cluster_size() : P;
+    const int cr = CLUSTER ? (int)cluster_rank() : c;
+    const int G = P / Pc, gid = c / Pc;
     const int cw = (((ld + P - 1) / P) + 1) & ~1;  // even => 16-byte pairs
     const int c0 = c * cw < ld ? c * cw : ld;
     const int c1 = (c0 + cw < ld) ? c0 + cw : ld;
@@ -65,8 +76,8 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     double2* bq = reinterpret_cast<double2*>(ring + D * stage_elems);             // D x q (b_i, sq_i)
     double* xs = reinterpret_cast<double*>(bq + D * q);                           // cw
     double* xrs = xs + cw;                                                         // cw
-    double* inbuf = xrs + cw;                                                      // 2 x P x q1p (cluster)
-    double* upd = inbuf + (CLUSTER ? 2 * P * q1p : 0);                             // NW x cw
+    double* inbuf = xrs + cw;                                                      // 2 x Pc x q1p (cluster)
+    double* upd = inbuf + (CLUSTER ? 2 * Pc * q1p : 0);                            // NW x cw
     double* scal = upd + NW * cw;                                                  // NW x SEG_MAX
     double* errw = scal + NW * SEG_MAX;                                            // NW
     double* alp = errw + NW;                                                       // q
@@ -142,9 +153,9 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     // push layout: lane -> (peer r = lane % P, part = lane / P); each part of a
     // warp's G_w rows goes to peer r as 16-byte st.async pairs
     constexpr int G_w = 32 / LPR;                       // rows per warp per round
-    const int parts = (P >= 32) ? 1 : 32 / P;
+    const int parts = (Pc >= 32) ? 1 : 32 / Pc;
     const int vpp = (G_w + parts - 1) / parts;          // rows per lane
-    const int peer = lane % P, part = lane / P;
+    const int peer = lane % Pc, part = lane / Pc;
     unsigned rin = 0, rbar = 0;
     if (CLUSTER) {
         rin = mapa_u32(smem_u32(inbuf), (unsigned)peer);
@@ -161,7 +172,7 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     const double qd = (double)q;
     constexpr int groups = NT / LPR;
     const int g = tid / LPR, gl = tid % LPR;
-    const unsigned xfer_bytes = (unsigned)(P * q1 * sizeof(double));
+    const unsigned xfer_bytes = (unsigned)(Pc * q1 * sizeof(double));
     // worker block of this warp for the scale / average steps
     const int tb = (q * warp) / NW, te = (q * (warp + 1)) / NW, nseg = te - tb;
     const bool ckpt_on = a.ckpt_every > 0;
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
         }
         if (rec) a.dbg[(kk * 8 + warp) * 8 + 1] = clock64();
         // ---- partial dots over the slice, pushed to every CTA -----------------------
-        const unsigned my_off = (unsigned)(((par * P + c) * q1p) * (int)sizeof(double));
+        const unsigned my_off = (unsigned)(((par * Pc + cr) * q1p) * (int)sizeof(double));
         double* gpart = a.part + ((size_t)par * P + c) * q1;
         for (int t0 = 0; t0 < q; t0 += groups) {  // every lane joins each round's shuffles
             const int t = t0 + g;
@@ -235,7 +246,7 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
 #pragma unroll
             for (int w = 1; w < NW; ++w) e = __dadd_rn(e, errw[w]);
             if (CLUSTER) {
-                if (lane < P) st_async_f64(rin + my_off + (unsigned)(q * (int)sizeof(double)), e, rbar + 8u * par);
+                if (lane < Pc) st_async_f64(rin + my_off + (unsigned)(q * (int)sizeof(double)), e, rbar + 8u * par);
             } else if (lane == 0) {
                 __stcg(gpart + q, e);
             }
@@ -249,10 +260,10 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
         if (rec) a.dbg[(kk * 8 + warp) * 8 + 3] = clock64();
         auto total = [&](int t) -> double {
             if (CLUSTER) {
-                const double* ib = inbuf + par * P * q1p + t;
+                const double* ib = inbuf + par * Pc * q1p + t;
                 double v[MAXP_TREE];
 #pragma unroll
-                for (int cc = 0; cc < MAXP_TREE; ++cc) v[cc] = (cc < P) ? ib[cc * q1p] : 0.0;
+                for (int cc = 0; cc < MAXP_TREE; ++cc) v[cc] = (cc < Pc) ? ib[cc * q1p] : 0.0;
 #pragma unroll
                 for (int w = 1; w < MAXP_TREE; w <<= 1)
 #pragma unroll
@@ -276,18 +287,39 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
         {
             const double2* bqs = bq + st * q;
             const int tA = (lane < nseg) ? tb + lane : q;
-            double vA = 0.0;
-            if (lane < nseg || (want_check && nseg < 32)) vA = total(tA);
+            const int tB = tb + 32 + lane;
+            const bool needA = lane < nseg || (want_check && nseg < 32);
+            const bool needB = nseg > 32 && 32 + lane < nseg;
+            const bool needE = want_check && nseg >= 32;
+            double vA = needA ? total(tA) : 0.0;
+            double vB = needB ? total(tB) : 0.0;
+            double vE = needE ? total(q) : 0.0;
+            if (CLUSTER && G > 1) {
+                // cluster totals -> tagged words [par][cluster][t]; every CTA adds the
+                // G cluster totals in cluster order (bit-identical everywhere)
+                const unsigned tag = (unsigned)kk + 1u;
+                unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * q1 * 2;
+                if (cr == 0) {
+                    unsigned long long* mine = ll + (size_t)gid * q1 * 2;
+                    if (lane < nseg) ll_store(mine + 2 * tA, vA, tag);
+                    if (needB) ll_store(mine + 2 * tB, vB, tag);
+                    if (warp == 0 && want_check && lane == (nseg < 32 ? nseg : 0))
+                        ll_store(mine + 2 * q, nseg < 32 ? vA : vE, tag);
+                }
+                int* abort = &a.status->aborted;
+                if (needA) vA = ll_sum<MAXG>(ll + 2 * tA, 2 * q1, G, tag, abort);
+                if (needB) vB = ll_sum<MAXG>(ll + 2 * tB, 2 * q1, G, tag, abort);
+                if (needE) vE = ll_sum<MAXG>(ll + 2 * q, 2 * q1, G, tag, abort);
+            }
             if (lane < nseg && !last) {
                 const double2 bb = bqs[tA];
                 scal[warp * SEG_MAX + lane] = __ddiv_rn(__dmul_rn(alp[tA], __dsub_rn(bb.x, vA)), bb.y);
             }
-            if (nseg > 32 && 32 + lane < nseg && !last) {
-                const int tB = tb + 32 + lane;
+            if (needB && !last) {
                 const double2 bb = bqs[tB];
-                scal[warp * SEG_MAX + 32 + lane] = __ddiv_rn(__dmul_rn(alp[tB], __dsub_rn(bb.x, total(tB))), bb.y);
+                scal[warp * SEG_MAX + 32 + lane] = __ddiv_rn(__dmul_rn(alp[tB], __dsub_rn(bb.x, vB)), bb.y);
             }
-            if (want_check) err = (nseg < 32) ? __shfl_sync(0xffffffffu, vA, 31) : total(q);
+            if (want_check) err = (nseg < 32) ? __shfl_sync(0xffffffffu, vA, 31) : vE;
         }
         if (want_check) {
             ++checks;

@@ -202,3 +202,42 @@ def test_oracle_agreement_random_configs(gpu, oracle, systems):
             o = oracle.solve(s.A, s.b, s.x_star, variant="rkab", q=q, block_size=bs, base_seed=1)
             assert r.iterations == o["iterations"], (q, bs)
             assert rel_err(r.x, o["x"]) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("ctas", [32, 80, 112])
+def test_multi_cluster_matches_reference(gpu, c1_system, ctas):
+    """Several 16-CTA clusters exchanging cluster totals through tagged words
+    (kz_sync.cu): same iterates and stop decisions as the reference's c1 solve."""
+    from paper_2401_17474_b200 import DeviceSystem, solve_rka_seq
+
+    g = golden("solves.npz")
+    tag = "c1_rka64_s0"
+    with DeviceSystem(c1_system) as ds:
+        r = solve_rka_seq(ds, _cfg(variant="rka", q=64, base_seed=0, kernel="sync_cluster", ctas=ctas),
+                          checkpoint_every=1000)
+        assert r.gpu["kernel"] == "sync_cluster" and r.gpu["ctas"] == ctas
+        _check(r, g, tag)
+        cap = []
+        solve_rka_seq(ds, _cfg(variant="rka", q=64, base_seed=0, kernel="sync_cluster", ctas=ctas), capture=cap)
+        for j, b in enumerate(g[f"{tag}_ckpt"]):
+            assert rel_err(cap[1000 * (j + 1) - 1], b) <= PARITY_TOL, (ctas, j)
+
+
+@pytest.mark.parametrize("q,ctas", [(64, 112), (300, 96), (512, 0)])
+def test_multi_cluster_oracle_c2(gpu, oracle, c2_system, q, ctas):
+    """Long rows (80000 x 1000), q up to 512 (two scale blocks per warp), vs the oracle."""
+    from paper_2401_17474_b200 import DeviceSystem, solve_rka_seq
+
+    s = c2_system
+    o = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=q, base_seed=2, ckpt_every=250,
+                     nthreads=oracle.max_threads())
+    with DeviceSystem(s) as ds:
+        kernel = "sync_cluster" if ctas else "auto"
+        r = solve_rka_seq(ds, _cfg(variant="rka", q=q, base_seed=2, kernel=kernel, ctas=ctas))
+        assert ctas == 0 or r.gpu["ctas"] == ctas
+        assert r.iterations == o["iterations"] and r.error_evals == o["error_evals"]
+        assert rel_err(r.x, o["x"]) <= PARITY_TOL
+        cap = []
+        solve_rka_seq(ds, _cfg(variant="rka", q=q, base_seed=2, kernel=kernel, ctas=ctas), capture=cap)
+        for j, ck in enumerate(o["checkpoints"]):
+            assert rel_err(cap[250 * (j + 1) - 1], ck) <= PARITY_TOL, (q, j)
