@@ -845,9 +845,11 @@ void* rka_fn(int lg, int epl) {
 }
 
 size_t rka_smem(int64_t q, int box, int stages, int Pc) {
-    const int64_t q4 = (q + 3) & ~(int64_t)3, q1p = (q + 2) & ~(int64_t)1;
+    const int64_t q4 = (q + 3) & ~(int64_t)3;
+    const int64_t rpo = (((q + Pc - 1) / Pc) + 1) & ~(int64_t)1;
     const size_t stage = (size_t)q4 * box * sizeof(double) + (size_t)q4 * 32;
-    return 256 + (size_t)stages * stage + (size_t)(2 * Pc * q1p + RKA_NW * box + q4 + q) * sizeof(double);
+    return 256 + (size_t)stages * stage +
+           (size_t)(2 * Pc * rpo + 2 * q4 + 2 * Pc + 2 + rpo + RKA_NW * box + box + q) * sizeof(double);
 }
 
 typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -872,7 +874,7 @@ TmapEncodeFn tmap_encode() {
 
 // Tensor maps for the rka kernel: A as (columns = ld, rows = m) with a box of
 // `box` columns x 1 row (gather4 fetches 4 rows per instruction); the packed
-// (b_i, ||a_i||^2) pairs as (2, m) with a 2 x 1 box.
+// (b_i, ||a_i||^2, 1/||a_i||^2, 0) records as (4, m) with a 4 x 1 box.
 static int ensure_tmaps(kz_system* s, int box) {
     if (s->tm_box == box && s->tm_a == s->A.p && s->tm_b == s->bs2.p) return KZ_OK;
     TmapEncodeFn enc = tmap_encode();
@@ -888,9 +890,9 @@ static int ensure_tmaps(kz_system* s, int box) {
         if (r != CUDA_SUCCESS) return fail(KZ_ECUDA, "tensor map of A failed (%d)", (int)r);
     }
     {
-        const cuuint64_t dims[2] = {2, (cuuint64_t)s->m};
-        const cuuint64_t strides[1] = {2 * sizeof(double)};
-        const cuuint32_t bx[2] = {2, 1};
+        const cuuint64_t dims[2] = {4, (cuuint64_t)s->m};
+        const cuuint64_t strides[1] = {4 * sizeof(double)};
+        const cuuint32_t bx[2] = {4, 1};
         CUresult r = enc(&s->tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)s->bs2.p, dims, strides, bx, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -940,12 +942,7 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);
         if (const char* e = getenv("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
         if (stages < 2 || rka_smem(q, box, stages, Pc) > kSmemLimit) {
-            if (Pc > 2 && 2 * (size_t)Pc * (q + 2) * sizeof(double) > 32 * 1024) {
-                Pc /= 2;
-                G *= 2;
-            } else {
-                ++G;
-            }
+            ++G;  // thinner slices
             continue;
         }
         void* fn = rka_fn(lg, epl);
@@ -1077,7 +1074,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     // --- setup: row norms, sampler, packed (b, sq), streams, weights ---
     KZ_TRY(ensure_sampler(s, p->scheme, q, st));
     if (!s->bs2_valid) {
-        KZ_TRY(s->bs2.ensure(2 * (size_t)s->m));
+        KZ_TRY(s->bs2.ensure(4 * (size_t)s->m));
         pack_bs2_kernel<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->b.p, s->sq.p, s->m, s->bs2.p);
         KZ_TRY(check_launch("pack_bs2_kernel"));
         s->bs2_valid = true;
@@ -1110,6 +1107,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {
         if (bs != 1) return fail(KZ_EINVAL, "the sync kernels run RKA / RKAB with block_size 1 only");
         int rc = kern == KZ_KERNEL_SYNC_CLUSTER ? plan_rka(s, p, q, pl) : KZ_EINVAL;
+        if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && getenv("KZ_DEBUG_PLAN"))
+            fprintf(stderr, "[kz plan] rka kernel not used: %s\n", g_err.c_str());
         if (rc != KZ_OK) rc = plan_sync(s, p, q, kern == KZ_KERNEL_SYNC_CLUSTER, pl);
         if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && p->kernel == KZ_KERNEL_AUTO)
             rc = plan_sync(s, p, q, false, pl);
@@ -1160,8 +1159,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
     args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;
     if (phase_timing) {
-        KZ_TRY(s->dbg.ensure(32 * 64));
-        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 64 * sizeof(long long), st));
+        KZ_TRY(s->dbg.ensure(32 * 128));
+        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 128 * sizeof(long long), st));
         args.dbg = s->dbg.p;
     }
 
@@ -1298,8 +1297,9 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
                             "gap %.0f (n=%d, R=%d)\n", acc[0] / nrec, acc[1] / nrec, acc[2] / nrec, acc[3] / nrec,
                     acc[4] / nrec, acc[5] / nrec, acc[6] / nrec, nrec, pl.rows);
     } else if (phase_timing) {  // per-phase completion (max over warps) relative to the earliest warp start, CTA 0
-        std::vector<long long> h(32 * 64);
+        std::vector<long long> h(32 * 128);
         KZ_CUDA(cudaMemcpy(h.data(), s->dbg.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        const int SL = pl.tma ? 16 : 8;  // stamp slots per (iteration, warp)
         double acc[8] = {0}, span = 0;
         int nrec = 0;
         for (int k = 4; k < 31; ++k) {
@@ -1308,8 +1308,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             for (int ph = 0; ph < 8; ++ph) mx[ph] = -1;
             bool ok = true;
             for (int w = 0; w < 8; ++w) {
-                const long long* r = &h[(k * 8 + w) * 8];
-                const long long* rn = &h[((k + 1) * 8 + w) * 8];
+                const long long* r = &h[(k * 8 + w) * SL];
+                const long long* rn = &h[((k + 1) * 8 + w) * SL];
                 if (r[0] == 0 || rn[0] == 0) { ok = false; break; }
                 t0 = (t0 < 0 || r[0] < t0) ? r[0] : t0;
                 nxt = (nxt < 0 || rn[0] < nxt) ? rn[0] : nxt;
@@ -1324,6 +1324,29 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             fprintf(stderr, "[kz phase end, max over warps, cycles from start] top %.0f issued %.0f dots %.0f waited %.0f "
                             "err %.0f scales %.0f update %.0f | iteration %.0f (n=%d)\n", acc[0] / nrec, acc[1] / nrec,
                     acc[2] / nrec, acc[3] / nrec, acc[4] / nrec, acc[5] / nrec, acc[6] / nrec, span / nrec, nrec);
+        if (atoi(getenv("KZ_PHASE_TIMING")) >= 2) {  // per-warp mean stamps relative to the earliest warp start
+            double pw[8][16] = {{0}};
+            int nk = 0;
+            for (int k = 4; k < 31; ++k) {
+                long long t0 = -1;
+                for (int w = 0; w < 8; ++w) {
+                    const long long v = h[(k * 8 + w) * SL];
+                    if (v && (t0 < 0 || v < t0)) t0 = v;
+                }
+                if (t0 < 0) continue;
+                for (int w = 0; w < 8; ++w)
+                    for (int ph = 0; ph < SL; ++ph) {
+                        const long long v = h[(k * 8 + w) * SL + ph];
+                        pw[w][ph] += v ? (double)(v - t0) : 0.0;
+                    }
+                ++nk;
+            }
+            for (int w = 0; w < 8 && nk; ++w) {
+                fprintf(stderr, "[kz warp %d]", w);
+                for (int ph = 0; ph < SL; ++ph) fprintf(stderr, " %6.0f", pw[w][ph] / nk);
+                fprintf(stderr, "\n");
+            }
+        }
     }
     return KZ_OK;
 }

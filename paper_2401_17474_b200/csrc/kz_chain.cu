@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 const int64_t i = sm.win[(issued + lane) & (IDX_WINDOW - 1)];
                 mbar_arrive_expect_tx(&full[st], row_bytes + 16u);
                 bulk_g2s(sm.ring + (size_t)st * ldc, a.A + i * ld + cb, row_bytes, &full[st]);
-                bulk_g2s(sm.bsq + st, bs2 + i, 16u, &full[st]);
+                bulk_g2s(sm.bsq + st, bs2 + 2 * i, 16u, &full[st]);
             }
             issued += cnt;
             iss_stage += cnt;

@@ -22,7 +22,7 @@ struct SolveArgs {
     const double* A;       // m x ld, row-major, pitched
     const double* b;       // m
     const double* sq;      // m squared row norms (einsum order)
-    const double* bs2;     // m x 2 packed (b_i, sq_i)
+    const double* bs2;     // m x 4 packed (b_i, sq_i, RN(1/sq_i), 0)
     const double* xref;    // ld (zero padded)
     double* x;             // ld, the iterate (in/out)
     double* partial;       // non-null: one iteration, write sum_t v_t here instead of x

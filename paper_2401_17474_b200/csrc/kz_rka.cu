@@ -19,22 +19,24 @@
 //       1. dots: 8 rows per warp per round, LG lanes per row (NR = LG/4 rows
 //          per lane group, independent FMA chains), a transposed shuffle
 //          reduction (NR-1 + 2 shuffles per round);
-//       2. push: every row partial goes to all Pc CTAs of the cluster with
-//          st.async (completing the receiver's exchange mbarrier); warp 0 adds
-//          the slice's ||x - x_ref||^2 piece as entry q;
-//       3. wait on the local exchange mbarrier; 4 lanes per worker add the Pc
-//          partials with one fixed tree (bit-identical in every CTA).  With
-//          G > 1 the rank-0 CTA of each cluster publishes its cluster totals
-//          as tagged 64-bit words and every CTA adds the G cluster totals in
-//          cluster order;
-//       4. scale s_t = alpha_t (b_t - d_t) / ||a_t||^2; stop rule on entry q;
+//       2. reduce-scatter: worker t's partial goes to its owner, cluster rank
+//          t / RPO (16-byte st.async for row pairs, completing the owner's
+//          mbarrier); warp 0 sends the slice's ||x - x_ref||^2 piece as item q;
+//       3. the owner warp (7) adds the Pc partials of its items with one fixed
+//          tree, forms s_t = alpha_t (b_t - d_t) / ||a_t||^2 and broadcasts the
+//          scales (and the error total) to every CTA of the cluster -- two
+//          DSMEM hops carrying q values each instead of an all-to-all of q x Pc.
+//          With G > 1 clusters the owners first exchange their cluster totals
+//          as tagged 64-bit words (value halves + iteration tag, single-copy
+//          atomic; no grid barrier, no fence) and add them in cluster order;
+//       4. stop rule on the broadcast error total;
 //       5. average: each warp sums fl(x + fl(s_t a_t)) over its block; the 8
 //          per-warp sums meet in shared memory behind one named barrier and
 //          every warp forms x_{k+1} (fixed tree, / q) for its own lanes, so x
 //          never leaves registers.
-//   One named barrier per iteration; the exchange mbarrier orders everything
-//   else (a CTA's exchange completes only after every warp of every peer has
-//   pushed, i.e. finished the previous iteration).
+//   One named barrier per iteration; the two mbarriers order everything else
+//   (an owner's items complete only after every peer has finished the previous
+//   iteration).
 #include "kz_kernels.cuh"
 
 namespace kz {
@@ -63,21 +65,29 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int cwb = a.box;                               // >= cw, multiple of 4
     const int q4 = (q + 3) & ~3;
     const int q1 = q + 1, q1p = (q1 + 1) & ~1;
-    const int QB = (q + NW - 1) / NW;
+    const int RPO = (((q + Pc - 1) / Pc) + 1) & ~1;  // workers per owner, even; the error belongs to rank Pc-1
+    const int QB = (((q + NW - 1) / NW) + 1) & ~1;  // even: rows pair up into 16-byte pushes
     const int nwv = (q + QB - 1) / QB;  // warps owning at least one worker
     const unsigned rows_bytes = (unsigned)(q4 * cwb * 8);
-    const int stage_bytes = (int)rows_bytes + q4 * 32;  // rows, then (b, sq) pairs in 128-B groups of 4
+    const int stage_bytes = (int)rows_bytes + q4 * 32;  // rows, then 32-byte (b, sq, 1/sq, 0) records
 
     // shared memory carve (rka_smem() in kz_api.cu must match)
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw);  // D <= 8
     unsigned long long* empty = full + 8;                                       // D
-    unsigned long long* xbar = full + 16;                                       // 2
-    volatile int* halt = reinterpret_cast<volatile int*>(smem_raw + 160);
-    unsigned char* ring = smem_raw + 256;                                        // D x stage_bytes
-    double* inbuf = reinterpret_cast<double*>(ring + D * stage_bytes);  // 2 x Pc x q1p
-    double* upd = inbuf + 2 * Pc * q1p;                                          // NW x cwb
-    double* scal = upd + NW * cwb;                                               // q4
-    double* alp = scal + q4;                                                     // q
+    unsigned long long* xbar = full + 16;                                       // 2: partials at the owner
+    unsigned long long* sbar = full + 18;                                       // 2: scales everywhere
+    unsigned long long* ebin = full + 20;                                       // 2: error pieces at rank Pc-1
+    unsigned long long* ebar = full + 22;                                       // 2: error total everywhere
+    volatile int* halt = reinterpret_cast<volatile int*>(smem_raw + 192);
+    unsigned char* ring = smem_raw + 256;                                // D x stage_bytes
+    double* inbuf = reinterpret_cast<double*>(ring + D * stage_bytes);  // 2 x Pc x RPO (owner side)
+    double* scal = inbuf + 2 * Pc * RPO;                                 // 2 x q4 scales
+    double* ein = scal + 2 * q4;                                         // 2 x Pc error pieces (rank Pc-1)
+    double* errs = ein + 2 * Pc;                                         // 2 error totals
+    double* sout = errs + 2;                                             // RPO (owner staging)
+    double* upd = sout + RPO;                                            // NW x cwb
+    double* xrs = upd + NW * cwb;                                        // cwb: x_ref slice
+    double* alp = xrs + cwb;                                             // q
 
     if (tid == 0) {
         for (int i = 0; i < D; ++i) {
@@ -86,6 +96,12 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         }
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
+        mbar_init(&sbar[0], 1);
+        mbar_init(&sbar[1], 1);
+        mbar_init(&ebin[0], 1);
+        mbar_init(&ebin[1], 1);
+        mbar_init(&ebar[0], 1);
+        mbar_init(&ebar[1], 1);
         *halt = 0;
         fence_mbarrier_init_cluster();
     }
@@ -96,7 +112,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     if (warp == NW) {
         // ================= producer warp =================
         const int ng = q4 / 4;
-        const unsigned bytes = rows_bytes + (unsigned)q4 * 16u;  // gather4 of pairs lands 64 B per group
+        const unsigned bytes = rows_bytes + (unsigned)q4 * 32u;
         const unsigned ring_u = smem_u32(ring);
         int64_t it = 0;
         int s = 0;
@@ -140,99 +156,121 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     }
 
     // ================= compute warps =================
+    constexpr int OW = NW - 1;  // owner warp
     const int gl = lane % LG, grp = lane / LG;
-    double2 xv[EPL], xr[EPL];
+    double2 xv[EPL];
+    for (int j = tid; j < cwb; j += NW * 32) xrs[j] = j < wdt ? a.xref[c0 + j] : 0.0;
+    named_sync(CBAR, NW * 32);
     bool vld[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
         const int j = 2 * (gl + LG * e);
         vld[e] = j < wdt;
         xv[e] = vld[e] ? make_double2(__ldcg(a.x + c0 + j), __ldcg(a.x + c0 + j + 1)) : make_double2(0.0, 0.0);
-        xr[e] = vld[e] ? make_double2(a.xref[c0 + j], a.xref[c0 + j + 1]) : make_double2(0.0, 0.0);
     }
-    // ||x - x_ref||^2 over the slice (warp 0, lane group 0), pushed as entry q
-    auto slice_err = [&]() -> double {
-        double e2 = 0.0;
-        if (grp == 0) {
-#pragma unroll
-            for (int e = 0; e < EPL; ++e)
-                if (vld[e]) {
-                    const double d0 = xv[e].x - xr[e].x, d1 = xv[e].y - xr[e].y;
-                    e2 = fma(d0, d0, e2);
-                    e2 = fma(d1, d1, e2);
-                }
-        }
-        return warp_sum(e2);
-    };
-    double errp = (warp == 0) ? slice_err() : 0.0;
 
     // reduced-row bookkeeping: after the transposed reduction lane gl holds row ri
-    // of its group; lanes differing in the low two bits hold the same value
+    // of its group; lanes differing in the low two bits hold the same value and
+    // rows ri, ri ^ 1 sit on lanes gl, gl ^ 4
     int ri = 0;
 #pragma unroll
     for (int h = NR / 2, o = LG / 2; h >= 1; h >>= 1, o >>= 1)
         if (gl & o) ri += h;
-    const int rho = gl & 3;
-    unsigned rin[4], rbar[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int pk = rho + 4 * i;
-        rin[i] = mapa_u32(smem_u32(inbuf), (unsigned)(pk < Pc ? pk : 0));
-        rbar[i] = mapa_u32(smem_u32(xbar), (unsigned)(pk < Pc ? pk : 0));
-    }
-    const unsigned rin_e = mapa_u32(smem_u32(inbuf), (unsigned)(lane < Pc ? lane : 0));
-    const unsigned rbar_e = mapa_u32(smem_u32(xbar), (unsigned)(lane < Pc ? lane : 0));
+    const unsigned inbuf_u = smem_u32(inbuf), xbar_u = smem_u32(xbar), scal_u = smem_u32(scal),
+                   sbar_u = smem_u32(sbar), ein_u = smem_u32(ein), ebin_u = smem_u32(ebin),
+                   errs_u = smem_u32(errs), ebar_u = smem_u32(ebar);
 
     const int wb = warp * QB < q ? warp * QB : q;
     const int we = wb + QB < q ? wb + QB : q;
-    const int nb = we - wb;
-    const bool gh = nb > grp * NR;  // this lane group owns at least one worker
+    const int my_lo = cr * RPO < q ? cr * RPO : q;
+    const int n_own = (my_lo + RPO < q ? my_lo + RPO : q) - my_lo;  // workers this CTA owns
+    const int eown = Pc - 1;                                          // owner of the error total
+    const bool gh = we - wb > grp * NR;  // this lane group owns at least one worker
     const bool qpow2 = (q & (q - 1)) == 0;
-    const double invq = 1.0 / (double)q;
+    const double invq = 1.0 / (double)q;  // RN(1/q): exact for powers of two, Markstein otherwise
     const double qd = (double)q;
     const bool ckpt_on = a.ckpt_every > 0;
-    const unsigned xfer_bytes = (unsigned)(Pc * q1 * (int)sizeof(double));
     const int count = (int)a.count;
-    const int cnt2 = Pc >= 2 ? Pc / 2 : 1;  // partials per lane in the totals (2 lanes per worker)
+    const bool use_stop = opaque_i32(a.use_stop) != 0, final_check = opaque_i32(a.final_check) != 0;
+    const int cnt2 = Pc >= 2 ? Pc / 2 : 1;  // partials per lane in the owner's tree (2 lanes per item)
+    const int u = lane & 1;
+
+    // owner tree: item i's Pc partials (stride `stride`) added by lanes 2i, 2i+1 in one fixed order
+    auto owner_total = [&](const double* base, int stride, bool live) -> double {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int cc = u * cnt2 + k;
+            v[k] = (live && k < cnt2 && cc < Pc) ? base[cc * stride] : 0.0;
+        }
+        double tot = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+        tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+        return tot;
+    };
+
+    // per-lane constants: element offsets of the lane's rows in round 0 (later rounds
+    // add 8 rows), the round-0 reduce-scatter target, the owner's broadcast slots
+    // (opaque copies: keeps them in registers instead of re-deriving from the parameter bank)
+    int roff[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) roff[r] = opaque_i32((wb + grp * NR + r) * cwb + 2 * gl);
+    const int rstep = opaque_i32(8 * cwb);
+    const int t_push0 = wb + grp * NR + ri;
+    const int o_push0 = opaque_i32(t_push0 / RPO), s_push0 = opaque_i32(t_push0 - (t_push0 / RPO) * RPO);
+    int pcs = 0;
+    while ((1 << pcs) < Pc) ++pcs;  // Pc is a power of two
+    const bool pusher = (ri & 1) == 0 && (gl & 3) == 0;
 
     int st = 0;
     unsigned fph = 0;  // parity of stage st's current full phase
+    bool ready = false;  // stage st already awaited (prefetched wait)
     int done = 0;
     int conv = 0, checks = 0;
     double err_last = 0.0;
 
     for (int kk = 0;; ++kk) {
         const bool last = (kk == count);
-        const bool want_check = a.use_stop && (!last || a.final_check);
+        const bool want_check = use_stop && (!last || final_check);
         if (last && !want_check) break;
         const int par = kk & 1;
+        const unsigned bpar = (unsigned)((kk >> 1) & 1);
         const bool rec = TIMING && a.dbg != nullptr && c == 0 && lane == 0 && kk < 32;
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 0] = clock64();
-        if (tid == 0) mbar_arrive_expect_tx(&xbar[par], last ? (unsigned)(Pc * (int)sizeof(double)) : xfer_bytes);
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 0] = clock64();
+        if (tid == 0) {
+            if (!last) {
+                if (n_own > 0) mbar_arrive_expect_tx(&xbar[par], (unsigned)(n_own * Pc * (int)sizeof(double)));
+                mbar_arrive_expect_tx(&sbar[par], (unsigned)(q * (int)sizeof(double)));
+            }
+            if (want_check) {
+                if (cr == eown) mbar_arrive_expect_tx(&ebin[par], (unsigned)(Pc * (int)sizeof(double)));
+                mbar_arrive_expect_tx(&ebar[par], (unsigned)sizeof(double));
+            }
+        }
         const double* rows = reinterpret_cast<const double*>(ring + st * stage_bytes);
-        const double2* bsq = reinterpret_cast<const double2*>(ring + st * stage_bytes + rows_bytes);
-        if (!last) mbar_wait(&full[st], fph);
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 1] = clock64();
-        const unsigned my_off = (unsigned)(((par * Pc + cr) * q1p) * (int)sizeof(double));
-        // ---- 1-2. partial dots of this warp's rows, pushed to every CTA of the cluster --
+        const double* bsr = reinterpret_cast<const double*>(ring + st * stage_bytes + rows_bytes);
+        if (!last && !ready) mbar_wait(&full[st], fph);
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 1] = clock64();
+        // ---- 1-2. partial dots of this warp's rows -> their owners ------------------------
         if (!last) {
-            for (int rb = wb; rb < we; rb += 8) {
+            int o_push = o_push0, s_push = s_push0;  // owner, slot of round 0
+            for (int rb = wb, rofs = 0; rb < we; rb += 8, rofs += rstep) {
                 double acc[NR];
 #pragma unroll
                 for (int r = 0; r < NR; ++r) {
                     acc[r] = 0.0;
                     const int t = rb + grp * NR + r;
                     if (t < we) {
-                        const double* row = rows + t * cwb;
+                        const double* row = rows + roff[r] + rofs;
 #pragma unroll
                         for (int e = 0; e < EPL; ++e)
                             if (vld[e]) {
-                                const double2 rv = *reinterpret_cast<const double2*>(row + 2 * (gl + LG * e));
+                                const double2 rv = *reinterpret_cast<const double2*>(row + 2 * LG * e);
                                 acc[r] = fma(rv.x, xv[e].x, acc[r]);
                                 acc[r] = fma(rv.y, xv[e].y, acc[r]);
                             }
                     }
                 }
+                if (TIMING && rec && rb == wb) a.dbg[(kk * 8 + warp) * 16 + 14] = clock64() + (long long)(acc[0] * 0.0);
 #pragma unroll
                 for (int h = NR / 2, o = LG / 2; h >= 1; h >>= 1, o >>= 1) {
                     const bool up = (gl & o) != 0;
@@ -245,69 +283,120 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 }
                 acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
                 acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+                const double odd = __shfl_xor_sync(0xffffffffu, acc[0], 4);
+                if (TIMING && rec && rb == wb) a.dbg[(kk * 8 + warp) * 16 + 15] = clock64() + (long long)(odd * 0.0);
                 const int t = rb + grp * NR + ri;
-                if (t < we) {
-                    const unsigned off = my_off + (unsigned)(t * (int)sizeof(double));
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        if (rho + 4 * i < Pc) st_async_f64(rin[i] + off, acc[0], rbar[i] + 8u * par);
+                if (t < we && pusher) {
+                    const unsigned off = (unsigned)(((par * Pc + cr) * RPO + s_push) * (int)sizeof(double));
+                    const unsigned dst = mapa_u32(inbuf_u, (unsigned)o_push) + off;
+                    const unsigned bar = mapa_u32(xbar_u + 8u * par, (unsigned)o_push);
+                    if (t + 1 < we)
+                        st_async_v2_f64(dst, acc[0], odd, bar);
+                    else
+                        st_async_f64(dst, acc[0], bar);
                 }
+                if (rb + 8 < we)
+                    for (s_push += 8; s_push >= RPO; s_push -= RPO) ++o_push;  // next round: 8 rows on
             }
         }
-        if (warp == 0 && lane < Pc)
-            st_async_f64(rin_e + my_off + (unsigned)(q * (int)sizeof(double)), errp, rbar_e + 8u * par);
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 2] = clock64();
-        // ---- 3. exchange (the st.async data lands with the mbarrier's tx count) -----------
-        mbar_wait(&xbar[par], (unsigned)((kk >> 1) & 1));
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 3] = clock64();
-        // ---- 3-4. totals (2 lanes per worker), scales, stop rule -------------------------
-        double err = 0.0;
-        {
-            const double* ib = inbuf + par * Pc * q1p;
-            const int nbr = last ? 0 : nb;  // the final check exchanges only entry q
-            const int nitems = nbr + (want_check ? 1 : 0);
-            const int u = lane & 1;
-            double errv = 0.0;
-            for (int i0 = 0; i0 < nitems; i0 += 16) {
-                const int item = i0 + (lane >> 1);
-                const bool live = item < nitems;
-                const int t = item < nbr ? wb + item : q;
-                double v[8];
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 13] = clock64();
+        // ---- error piece of x_k (needed only at the end of the iteration) -----------------
+        if (want_check && warp == 0 && !(TIMING && (a.ablate & 1))) {
+            double e2 = 0.0;
+            if (grp == 0) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int cc = u * cnt2 + k;
-                    v[k] = (live && k < cnt2 && cc < Pc) ? ib[cc * q1p + t] : 0.0;
-                }
-                double tot = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-                tot += __shfl_xor_sync(0xffffffffu, tot, 1);
-                if (G > 1) {
-                    // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
-                    const unsigned tag = (unsigned)kk + 1u;
-                    unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * q1 * 2;
-                    if (cr == 0 && u == 0 && live && (item < nbr || warp == 0))
+                for (int e = 0; e < EPL; ++e)
+                    if (vld[e]) {
+                        const double2 xr = *reinterpret_cast<const double2*>(xrs + 2 * (gl + LG * e));
+                        const double d0 = xv[e].x - xr.x, d1 = xv[e].y - xr.y;
+                        e2 = fma(d0, d0, e2);
+                        e2 = fma(d1, d1, e2);
+                    }
+            }
+            e2 = warp_sum(e2);
+            if (lane == 0)
+                st_async_f64(mapa_u32(ein_u, (unsigned)eown) + (unsigned)((par * Pc + cr) * (int)sizeof(double)), e2,
+                             mapa_u32(ebin_u + 8u * par, (unsigned)eown));
+        } else if (want_check && warp == 0 && lane == 0) {
+            st_async_f64(mapa_u32(ein_u, (unsigned)eown) + (unsigned)((par * Pc + cr) * (int)sizeof(double)), 0.0,
+                         mapa_u32(ebin_u + 8u * par, (unsigned)eown));
+        }
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 2] = clock64();
+        // the next stage's rows are awaited now, while the exchange is in flight
+        ready = false;
+        if (warp != OW && kk + 1 < count) {
+            const int st1 = st + 1 == D ? 0 : st + 1;
+            mbar_wait(&full[st1], st + 1 == D ? fph ^ 1u : fph);
+            ready = true;
+        }
+        // ---- 3. owner: totals of its workers, scales, broadcast; then the error total -------
+        if (warp == OW) {
+            const unsigned tag = (unsigned)kk + 1u;
+            unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * q1 * 2;
+            if (!last && n_own > 0) {
+                mbar_wait(&xbar[par], bpar);
+                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 7] = clock64();
+                const double* ib = inbuf + par * Pc * RPO;
+                for (int i0 = 0; i0 < n_own; i0 += 16) {
+                    const int i = i0 + (lane >> 1);
+                    const bool live = i < n_own;
+                    const int t = my_lo + i;
+                    double tot = owner_total(ib + i, RPO, live);
+                    if (G > 1 && u == 0 && live) {
+                        // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
                         ll_store(ll + ((size_t)gid * q1 + t) * 2, tot, tag);
-                    if (u == 0 && live) tot = ll_sum<RKA_MAXG>(ll + 2 * t, 2 * q1, G, tag, &a.status->aborted);
-                    tot = __shfl_sync(0xffffffffu, tot, lane & ~1);
+                        tot = ll_sum<RKA_MAXG>(ll + 2 * t, 2 * q1, G, tag, &a.status->aborted);
+                    }
+                    if (live && u == 0) {
+                        const double* rec4 = bsr + 4 * t;  // (b, sq, 1/sq, 0)
+                        const double nume = __dmul_rn(alp[t], __dsub_rn(rec4[0], tot));
+                        sout[i] = div_rn_fast(nume, rec4[1], rec4[2]);
+                    }
                 }
-                if (live && u == 0 && item < nbr) {
-                    const double2 bb = bsq[((t >> 2) << 3) + (t & 3)];
-                    scal[t] = __ddiv_rn(__dmul_rn(alp[t], __dsub_rn(bb.x, tot)), bb.y);
+                __syncwarp();
+                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 8] = clock64();
+                // broadcast: worker pairs (i, i + 1) as 16-byte pushes to every CTA of the cluster
+                const int npair = (n_own + 1) / 2;
+                for (int k = lane; k < npair * Pc; k += 32) {
+                    const int pi = k >> pcs, peer = k & (Pc - 1);
+                    const int i = 2 * pi, t = my_lo + i;
+                    const unsigned dst =
+                        mapa_u32(scal_u, (unsigned)peer) + (unsigned)((par * q4 + t) * (int)sizeof(double));
+                    const unsigned bar = mapa_u32(sbar_u + 8u * par, (unsigned)peer);
+                    if (i + 1 < n_own)
+                        st_async_v2_f64(dst, sout[i], sout[i + 1], bar);
+                    else
+                        st_async_f64(dst, sout[i], bar);
                 }
-                if (item == nbr) errv = tot;
+                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 9] = clock64();
             }
-            if (want_check) err = __shfl_sync(0xffffffffu, errv, 2 * (nbr & 15));
+            if (want_check && cr == eown) {
+                mbar_wait(&ebin[par], bpar);
+                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 10] = clock64();
+                double tot = owner_total(ein + par * Pc, 1, lane < 2);
+                if (G > 1 && lane == 0) {
+                    ll_store(ll + ((size_t)gid * q1 + q) * 2, tot, tag);
+                    tot = ll_sum<RKA_MAXG>(ll + 2 * q, 2 * q1, G, tag, &a.status->aborted);
+                }
+                tot = __shfl_sync(0xffffffffu, tot, 0);
+                if (lane < Pc)
+                    st_async_f64(mapa_u32(errs_u, (unsigned)lane) + (unsigned)(par * (int)sizeof(double)), tot,
+                                 mapa_u32(ebar_u + 8u * par, (unsigned)lane));
+            }
         }
-        if (want_check) {
+        if (last) {  // final stop-rule evaluation only
+            mbar_wait(&ebar[par], bpar);
+            const double err = errs[par];
             ++checks;
             err_last = err;
-            if (err < a.eps) {
-                conv = 1;
-                break;
-            }
+            if (err < a.eps) conv = 1;
+            break;
         }
-        if (last) break;
-        __syncwarp();
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 4] = clock64();
+        // ---- 4. scales arrive ------------------------------------------------------------
+        mbar_wait(&sbar[par], bpar);
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 3] = clock64();
+        const double* sc = scal + par * q4;
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 4] = clock64();
         // ---- 5. average over this warp's workers -----------------------------------------
         double2 acc[EPL];
 #pragma unroll
@@ -317,13 +406,13 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             for (int r = 0; r < NR; ++r) {
                 const int t = rb + grp * NR + r;
                 if (t < we) {
-                    const double s = scal[t];
-                    const double* row = rows + t * cwb;
+                    const double s = sc[t];
+                    const double* row = rows + roff[r] + (rb - wb) * cwb;
                     const bool first = (r == 0) && (rb == wb);
 #pragma unroll
                     for (int e = 0; e < EPL; ++e)
                         if (vld[e]) {
-                            const double2 rv = *reinterpret_cast<const double2*>(row + 2 * (gl + LG * e));
+                            const double2 rv = *reinterpret_cast<const double2*>(row + 2 * LG * e);
                             const double v0 = __dadd_rn(xv[e].x, __dmul_rn(s, rv.x));
                             const double v1 = __dadd_rn(xv[e].y, __dmul_rn(s, rv.y));
                             acc[e].x = first ? v0 : __dadd_rn(acc[e].x, v0);
@@ -357,11 +446,13 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             for (int e = 0; e < EPL; ++e)
                 if (vld[e]) *reinterpret_cast<double2*>(upd + warp * cwb + 2 * (gl + LG * e)) = acc[e];
         }
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 5] = clock64();
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 5] = clock64();
         named_sync(CBAR, NW * 32);
         // ---- combine: every warp forms x_{k+1} for its own lanes (fixed tree over warps) --
+        double2 xn[EPL];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) {
+            xn[e] = xv[e];
             if (!vld[e]) continue;
             const int j = 2 * (gl + LG * e);
             double2 w[NW];
@@ -389,15 +480,30 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                         }
             }
             if (a.partial) {  // row-sharded step: un-normalised local sum
-                if (warp == 0 && grp == 0 && vld[e]) {
+                if (warp == 0 && grp == 0) {
                     __stcg(a.partial + c0 + j, w[0].x);
                     __stcg(a.partial + c0 + j + 1, w[0].y);
                 }
                 continue;
             }
-            xv[e].x = qpow2 ? __dmul_rn(w[0].x, invq) : __ddiv_rn(w[0].x, qd);
-            xv[e].y = qpow2 ? __dmul_rn(w[0].y, invq) : __ddiv_rn(w[0].y, qd);
+            xn[e].x = qpow2 ? __dmul_rn(w[0].x, invq) : div_rn_fast(w[0].x, qd, invq);
+            xn[e].y = qpow2 ? __dmul_rn(w[0].y, invq) : div_rn_fast(w[0].y, qd, invq);
         }
+        // ---- stop rule on x_k (its error total arrived while x_{k+1} was formed) ----------
+        if (want_check) {
+            if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 11] = clock64();
+            mbar_wait(&ebar[par], bpar);
+            if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 12] = clock64();
+            const double err = errs[par];
+            ++checks;
+            err_last = err;
+            if (err < a.eps) {
+                conv = 1;
+                break;  // x_k stands; x_{k+1} is discarded
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) xv[e] = xn[e];
         if (ckpt_on && warp == 0 && grp == 0) {
             const int64_t k = a.k0 + kk;
             if (((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap) {
@@ -411,8 +517,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     }
             }
         }
-        if (warp == 0) errp = slice_err();
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 8 + 6] = clock64();
+        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 6] = clock64();
         if (++st == D) {
             st = 0;
             fph ^= 1u;

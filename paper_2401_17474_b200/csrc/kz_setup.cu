@@ -222,9 +222,11 @@ __global__ void scale_copy_kernel(const double* __restrict__ S, double div, int6
 __global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __restrict__ sq, int64_t m,
                                 double* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) {
-        out[2 * i] = b[i];
-        out[2 * i + 1] = sq[i];
+    if (i < m) {  // 32-byte record (b_i, ||a_i||^2, RN(1 / ||a_i||^2), 0)
+        out[4 * i] = b[i];
+        out[4 * i + 1] = sq[i];
+        out[4 * i + 2] = sq[i] > 0.0 ? __drcp_rn(sq[i]) : 0.0;
+        out[4 * i + 3] = 0.0;
     }
 }
 

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
                     for (int p = 0; 2 * (my_p + p) < wdt; p += tpr) cp_async16(dst + t * rs + 2 * p, src + 2 * p);
                 }
             }
-            for (int t = tid; t < q; t += NT) cp_async16(bq + st * q + t, bs2 + ir[t]);
+            for (int t = tid; t < q; t += NT) cp_async16(bq + st * q + t, bs2 + 2 * ir[t]);
         }
         cp_async_commit();
     };
