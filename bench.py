@@ -373,6 +373,13 @@ def run_b200(args, name, rank, world, local_rank):
     peak, peak_src = read_peak()
     bytes_per_row = 8 * n
     achieved = rows * bytes_per_row / (kernel_ms / 1e3) / 1e9
+    traffic, traffic_note = None, None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):  # measured once with ncu --set full (never under this timing run)
+        tr = json.load(open(tpath)).get(name)
+        if tr:
+            traffic = tr["dram_bytes_per_launch"]
+            traffic_note = {k: tr[k] for k in ("launch", "algorithmic_bytes_per_launch", "source", "note")}
     value = world * rows / (t_ms / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -385,7 +392,8 @@ def run_b200(args, name, rank, world, local_rank):
                            "max": float(np.max(step_ms))},
         "iterations": iters,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src, "kernel": f"kz::sync/chain ({kernel_name})",
+                     "traffic": traffic, "traffic_detail": traffic_note, "peak_source": peak_src,
+                     "kernel": f"kz::rka/chain ({kernel_name})",
                      "algorithmic_bytes": "8*n per row projection"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_rows / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -440,7 +440,7 @@ static int ensure_sampler(kz_system* s, int scheme, int64_t q, cudaStream_t st) 
     KZ_TRY(s->len.ensure(q));
     KZ_CUDA(cudaMemcpyAsync(s->lo.p, lo.data(), q * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     KZ_CUDA(cudaMemcpyAsync(s->len.p, len.data(), q * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    cdf_scan_kernel<<<(unsigned)((nranges + 127) / 128), 128, 0, st>>>(s->sq.p, s->lo.p, s->len.p, nranges, s->cdf.p);
+    cdf_scan_kernel<<<(unsigned)nranges, CDF_SCAN_THREADS, 0, st>>>(s->sq.p, s->lo.p, s->len.p, nranges, s->cdf.p);
     KZ_TRY(check_launch("cdf_scan_kernel"));
     const int64_t maxlen = *std::max_element(len.begin(), len.end());
     dim3 grid((unsigned)std::min<int64_t>((maxlen + 255) / 256, 1024), (unsigned)nranges);
