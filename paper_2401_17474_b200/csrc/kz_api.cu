@@ -849,7 +849,7 @@ size_t rka_smem(int64_t q, int box, int stages, int Pc) {
     const int64_t rpo = (((q + Pc - 1) / Pc) + 1) & ~(int64_t)1;
     const size_t stage = (size_t)q4 * box * sizeof(double) + (size_t)q4 * 32;
     return 256 + (size_t)stages * stage +
-           (size_t)(2 * Pc * rpo + 2 * q4 + 2 * Pc + 2 + rpo + RKA_NW * box + box + q) * sizeof(double);
+           (size_t)(2 * Pc * rpo + 2 * q4 + 2 * Pc + 2 + rpo + RKA_NW * box + 2 * box + q) * sizeof(double);
 }
 
 typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -208,33 +208,40 @@ __device__ __forceinline__ double ll_value(unsigned long long w0, unsigned long 
     return __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
 }
 // Sum of G tagged values p[0], p[stride], ... in fixed order g = 0..G-1.
-// All G loads are in flight together; stragglers are re-polled.  A spin
-// beyond 2^22 polls sets *abort (reported to the host) instead of hanging, and
-// once *abort is set every other spinner gives up within 1024 polls.
+// Every round re-issues the loads of all slots still missing together (one L2
+// round trip per round, not one per straggler).  A spin beyond 2^22 rounds sets
+// *abort (reported to the host) instead of hanging, and once *abort is set
+// every other spinner gives up within 1024 rounds.
 template <int GMAX>
 __device__ __noinline__ double ll_sum(const unsigned long long* p, int stride, int G, unsigned tag, int* abort) {
     unsigned long long w0[GMAX], w1[GMAX];
 #pragma unroll
     for (int g = 0; g < GMAX; ++g)
         if (g < G) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+    unsigned spins = 0;
+    for (;;) {
+        bool all = true;
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g)
+            if (g < G && !ll_ok(w0[g], w1[g], tag)) all = false;
+        if (all) break;
+        ++spins;
+        if ((spins & 1023u) == 0 && *(volatile int*)abort) break;
+        if (spins > (1u << 22)) {
+            atomicExch(abort, 1);
+            break;
+        }
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g)
+            if (g < G && !ll_ok(w0[g], w1[g], tag)) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+    }
     double s = 0.0;
 #pragma unroll
-    for (int g = 0; g < GMAX; ++g) {
+    for (int g = 0; g < GMAX; ++g)
         if (g < G) {
-            unsigned spins = 0;
-            while (!ll_ok(w0[g], w1[g], tag)) {
-                ++spins;
-                if ((spins & 1023u) == 0 && *(volatile int*)abort) break;
-                if (spins > (1u << 22)) {
-                    atomicExch(abort, 1);
-                    break;
-                }
-                ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
-            }
             const double v = ll_value(w0[g], w1[g]);
             s = (g == 0) ? v : __dadd_rn(s, v);
         }
-    }
     return s;
 }
 

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     double* sout = errs + 2;                                             // RPO (owner staging)
     double* upd = sout + RPO;                                            // NW x cwb
     double* xrs = upd + NW * cwb;                                        // cwb: x_ref slice
-    double* alp = xrs + cwb;                                             // q
+    double* xs = xrs + cwb;                                              // cwb: x_{k+1} (split combine)
+    double* alp = xs + cwb;                                              // q
 
     if (tid == 0) {
         for (int i = 0; i < D; ++i) {
@@ -193,6 +194,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int count = (int)a.count;
     const bool use_stop = opaque_i32(a.use_stop) != 0, final_check = opaque_i32(a.final_check) != 0;
     const int cnt2 = Pc >= 2 ? Pc / 2 : 1;  // partials per lane in the owner's tree (2 lanes per item)
+    const bool split = TIMING && (a.ablate & 16) ? true : cwb >= 64;  // combine layout (see below)
+    const int ppw = ((wdt >> 1) + NW - 1) / NW;                      // column pairs per warp (split)
     const int u = lane & 1;
 
     // owner tree: item i's Pc partials (stride `stride`) added by lanes 2i, 2i+1 in one fixed order
@@ -448,13 +451,11 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         }
         if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 5] = clock64();
         named_sync(CBAR, NW * 32);
-        // ---- combine: every warp forms x_{k+1} for its own lanes (fixed tree over warps) --
-        double2 xn[EPL];
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-            xn[e] = xv[e];
-            if (!vld[e]) continue;
-            const int j = 2 * (gl + LG * e);
+        // ---- combine: x_{k+1} = (fixed tree over the warps' sums) / q ----------------------
+        // narrow slices: every warp forms its own lanes' columns (no second barrier);
+        // wide slices: warp w forms its share of the columns into xs, one more barrier,
+        // every lane reads its columns back (8x less shared-memory traffic)
+        auto combine_pair = [&](int j) -> double2 {
             double2 w[NW];
             if (nwv == NW) {
 #pragma unroll
@@ -479,15 +480,60 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                             w[i].y = __dadd_rn(w[i].y, w[i + h].y);
                         }
             }
-            if (a.partial) {  // row-sharded step: un-normalised local sum
-                if (warp == 0 && grp == 0) {
-                    __stcg(a.partial + c0 + j, w[0].x);
-                    __stcg(a.partial + c0 + j + 1, w[0].y);
+            return w[0];
+        };
+        auto scale_q = [&](double2 v) -> double2 {
+            return qpow2 ? make_double2(__dmul_rn(v.x, invq), __dmul_rn(v.y, invq))
+                         : make_double2(div_rn_fast(v.x, qd, invq), div_rn_fast(v.y, qd, invq));
+        };
+        double2 xn[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) xn[e] = xv[e];
+        const bool ck = ckpt_on && (((a.k0 + kk + 1) % a.ckpt_every) == 0) &&
+                        (((a.k0 + kk + 1) / a.ckpt_every) <= a.ckpt_cap);
+        const int64_t ck_slot = ck ? (a.k0 + kk + 1) / a.ckpt_every - 1 : 0;
+        if (split) {
+            const int np = wdt >> 1;
+            for (int pp = warp * ppw + lane; pp < (warp + 1) * ppw && pp < np; pp += 32) {
+                const int j = 2 * pp;
+                const double2 v = combine_pair(j);
+                if (a.partial) {  // row-sharded step: un-normalised local sum
+                    __stcg(a.partial + c0 + j, v.x);
+                    __stcg(a.partial + c0 + j + 1, v.y);
+                    continue;
                 }
-                continue;
+                const double2 x2 = scale_q(v);
+                *reinterpret_cast<double2*>(xs + j) = x2;
+                if (ck) {
+                    if (c0 + j < a.n) a.ckpt[ck_slot * a.n + c0 + j] = x2.x;
+                    if (c0 + j + 1 < a.n) a.ckpt[ck_slot * a.n + c0 + j + 1] = x2.y;
+                }
             }
-            xn[e].x = qpow2 ? __dmul_rn(w[0].x, invq) : div_rn_fast(w[0].x, qd, invq);
-            xn[e].y = qpow2 ? __dmul_rn(w[0].y, invq) : div_rn_fast(w[0].y, qd, invq);
+            named_sync(CBAR, NW * 32);
+            if (!a.partial) {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e)
+                    if (vld[e]) xn[e] = *reinterpret_cast<const double2*>(xs + 2 * (gl + LG * e));
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                if (!vld[e]) continue;
+                const int j = 2 * (gl + LG * e);
+                const double2 v = combine_pair(j);
+                if (a.partial) {
+                    if (warp == 0 && grp == 0) {
+                        __stcg(a.partial + c0 + j, v.x);
+                        __stcg(a.partial + c0 + j + 1, v.y);
+                    }
+                    continue;
+                }
+                xn[e] = scale_q(v);
+                if (ck && warp == 0 && grp == 0) {
+                    if (c0 + j < a.n) a.ckpt[ck_slot * a.n + c0 + j] = xn[e].x;
+                    if (c0 + j + 1 < a.n) a.ckpt[ck_slot * a.n + c0 + j + 1] = xn[e].y;
+                }
+            }
         }
         // ---- stop rule on x_k (its error total arrived while x_{k+1} was formed) ----------
         if (want_check) {
@@ -504,19 +550,6 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         }
 #pragma unroll
         for (int e = 0; e < EPL; ++e) xv[e] = xn[e];
-        if (ckpt_on && warp == 0 && grp == 0) {
-            const int64_t k = a.k0 + kk;
-            if (((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap) {
-                const int64_t slot = (k + 1) / a.ckpt_every - 1;
-#pragma unroll
-                for (int e = 0; e < EPL; ++e)
-                    if (vld[e]) {
-                        const int j = 2 * (gl + LG * e);
-                        if (c0 + j < a.n) a.ckpt[slot * a.n + c0 + j] = xv[e].x;
-                        if (c0 + j + 1 < a.n) a.ckpt[slot * a.n + c0 + j + 1] = xv[e].y;
-                    }
-            }
-        }
         if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 6] = clock64();
         if (++st == D) {
             st = 0;
