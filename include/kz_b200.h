@@ -43,7 +43,7 @@ enum kz_status {
     KZ_ENODEV = 6       /* no CUDA device                                                            */
 };
 
-enum kz_variant { KZ_RK = 0, KZ_RKA = 1, KZ_RKAB = 2 };          /* solvers.py:55 VARIANTS        */
+enum kz_variant { KZ_RK = 0, KZ_RKA = 1, KZ_RKAB = 2, KZ_CK = 3 };          /* solvers.py:55 VARIANTS        */
 enum kz_scheme { KZ_FULL_ACCESS = 0, KZ_DISTRIBUTED = 1 };        /* solvers.py:57 SAMPLING_SCHEMES */
 enum kz_kernel {                                                  /* engine selection (auto = 0)    */
     KZ_KERNEL_AUTO = 0,

@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libkz_oracle.so")
 _lib = None
 
-VARIANTS = {"rk": 0, "rka": 1, "rkab": 2}
+VARIANTS = {"rk": 0, "rka": 1, "rkab": 2, "ck": 3}
 SCHEMES = {"full_access": 0, "distributed": 1}
 
 OK, EINVAL, EDEGENERATE, EEMPTYRANGE, ENOMEM = range(5)

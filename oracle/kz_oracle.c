@@ -327,6 +327,7 @@ typedef struct {
     int64_t* rows;   /* q   (RKA row of each worker this iteration) */
     double* scales;  /* q                                            */
     double* vbuf;    /* q*n (RKAB private estimates)                 */
+    int64_t k;       /* iterations applied (CK row = k mod m)        */
 } run_t;
 
 /* Column range [c0,c1) of the averaging for thread `tid` of `nt`. */
@@ -377,6 +378,11 @@ static void worker_part(run_t* R, const double* x, int64_t t) {
 
 /* One iteration (advance) of the variant, serial. */
 static void advance_serial(run_t* R, double* x) {
+    if (R->variant == KZO_CK) { /* solvers.py:286-287: row k mod m */
+        kaczmarz_step(x, R->A, R->b, R->sq, R->n, R->k % R->m, R->alphas ? R->alphas[0] : 1.0);
+        ++R->k;
+        return;
+    }
     if (R->variant == KZO_RK) {
         int64_t i = sampler_draw(&R->samplers[0], &R->rngs[0]);
         kaczmarz_step(x, R->A, R->b, R->sq, R->n, i, R->alphas ? R->alphas[0] : 1.0);
@@ -462,9 +468,9 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
     memset(r, 0, sizeof(*r));
     r->bad_row = -1;
     if (m < 1 || n < 1 || p->q < 1 || p->block_size < 1 || !(p->epsilon > 0) ||
-        p->max_iterations < 1 || p->variant < KZO_RK || p->variant > KZO_RKAB)
+        p->max_iterations < 1 || p->variant < KZO_RK || p->variant > KZO_CK)
         return KZO_EINVAL;
-    if (p->variant == KZO_RK && p->q != 1) return KZO_EINVAL;
+    if ((p->variant == KZO_RK || p->variant == KZO_CK) && p->q != 1) return KZO_EINVAL;
     if (p->budget <= 0 && !x_ref) return KZO_EINVAL;
 
     run_t R;
@@ -499,8 +505,10 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
         rc = KZO_EDEGENERATE;
         goto done;
     }
-    rc = build_samplers(sq, m, p->scheme, R.q, cdf, R.samplers);
-    if (rc) goto done;
+    if (p->variant != KZO_CK) {
+        rc = build_samplers(sq, m, p->scheme, R.q, cdf, R.samplers);
+        if (rc) goto done;
+    }
     for (int64_t t = 0; t < R.q; ++t) worker_stream(p->base_seed, (uint64_t)t, &R.rngs[t]);
 
     double* x = x_out;
@@ -513,7 +521,7 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
     int converged = 0;
     int64_t evals = 0;
 
-    const int nt = (p->nthreads > 1 && p->variant != KZO_RK) ? p->nthreads : 1;
+    const int nt = (p->nthreads > 1 && p->variant != KZO_RK && p->variant != KZO_CK) ? p->nthreads : 1;
     if (nt <= 1) {
         for (;;) {
             if (use_stop) {

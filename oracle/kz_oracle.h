@@ -39,7 +39,7 @@ typedef struct {
     uint64_t inc_hi, inc_lo;
 } kzo_pcg64;
 
-enum { KZO_RK = 0, KZO_RKA = 1, KZO_RKAB = 2 };
+enum { KZO_RK = 0, KZO_RKA = 1, KZO_RKAB = 2, KZO_CK = 3 };
 enum { KZO_FULL_ACCESS = 0, KZO_DISTRIBUTED = 1 };
 
 enum {
@@ -51,7 +51,7 @@ enum {
 };
 
 typedef struct {
-    int32_t variant;          /* KZO_RK / KZO_RKA / KZO_RKAB                 */
+    int32_t variant;          /* KZO_RK / KZO_RKA / KZO_RKAB / KZO_CK        */
     int32_t scheme;           /* KZO_FULL_ACCESS / KZO_DISTRIBUTED           */
     int64_t q;                /* workers                                     */
     int64_t block_size;       /* RKAB chain length                           */

@@ -1055,7 +1055,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     r->final_residual = NAN;
     cudaStream_t st = (cudaStream_t)stream;
     // --- validation (SolverConfig.validate, solvers.py:85-101; _drive 200-214) ---
-    if (p->variant < KZ_RK || p->variant > KZ_RKAB) return fail(KZ_EINVAL, "unknown variant %d", p->variant);
+    if (p->variant < KZ_RK || p->variant > KZ_CK) return fail(KZ_EINVAL, "unknown variant %d", p->variant);
     if (p->q < 1) return fail(KZ_EINVAL, "q must be >= 1, got %lld", (long long)p->q);
     if (p->block_size < 1) return fail(KZ_EINVAL, "block_size must be >= 1, got %lld", (long long)p->block_size);
     if (!(p->epsilon > 0)) return fail(KZ_EINVAL, "epsilon must be > 0, got %g", p->epsilon);
@@ -1067,12 +1067,16 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     const bool stop_mode = !budget_mode && !trace_mode;
     if ((stop_mode || trace_mode) && !s->has_xref) return fail(KZ_EINVAL, "system carries no reference solution");
     if (trace_mode && !p->trace_host) return fail(KZ_EINVAL, "trace mode needs a trace buffer");
-    const int64_t q = p->variant == KZ_RK ? 1 : p->q;
+    const bool cyclic = p->variant == KZ_CK;  // solve_ck (solvers.py:271-291): row k mod m, no stream
+    const int64_t q = (p->variant == KZ_RK || cyclic) ? 1 : p->q;
     const int64_t bs = p->variant == KZ_RKAB ? p->block_size : 1;
     KZ_CUDA(cudaSetDevice(s->device));
 
     // --- setup: row norms, sampler, packed (b, sq), streams, weights ---
-    KZ_TRY(ensure_sampler(s, p->scheme, q, st));
+    if (cyclic)
+        KZ_TRY(ensure_norms(s, st));
+    else
+        KZ_TRY(ensure_sampler(s, p->scheme, q, st));
     if (!s->bs2_valid) {
         KZ_TRY(s->bs2.ensure(4 * (size_t)s->m));
         pack_bs2_kernel<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->b.p, s->sq.p, s->m, s->bs2.p);
@@ -1190,7 +1194,11 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         if (remaining <= 0 && !stop_mode) break;
         int64_t c = std::min<int64_t>(chunk, remaining);
         if (trace_mode) c = std::min<int64_t>(c, p->trace_step - (k % p->trace_step));
-        if (c > 0) {
+        if (c > 0 && cyclic) {
+            cyclic_rows_kernel<<<(unsigned)std::min<int64_t>((c + 255) / 256, 4096), 256, 0, st>>>(
+                s->idx.p, p->k_start + k, c, s->m);
+            KZ_TRY(check_launch("cyclic_rows_kernel"));
+        } else if (c > 0) {
             const int64_t count = c * bs;
             if (pl.kernel == KZ_KERNEL_CHAIN)
                 KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, (p->k_start + k) * bs, count, s->idx.p,

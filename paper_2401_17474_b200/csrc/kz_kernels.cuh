@@ -67,6 +67,7 @@ __global__ void rka_kernel(const __grid_constant__ SolveArgs a, const __grid_con
 
 __global__ void row_sqnorm_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
                                   double* __restrict__ sq, unsigned long long* __restrict__ first_zero);
+__global__ void cyclic_rows_kernel(int32_t* __restrict__ idx, int64_t k0, int64_t count, int64_t m);
 constexpr int CDF_SCAN_THREADS = 256;
 __global__ void cdf_scan_kernel(const double* __restrict__ sq, const int64_t* __restrict__ lo,
                                 const int64_t* __restrict__ len, int64_t nranges, double* __restrict__ cdf);

@@ -269,4 +269,10 @@ __global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v,
     }
 }
 
+// Cyclic Kaczmarz rows (solvers.py:286-287): idx[j] = (k0 + j) mod m.
+__global__ void cyclic_rows_kernel(int32_t* __restrict__ idx, int64_t k0, int64_t count, int64_t m) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x)
+        idx[j] = (int32_t)((k0 + j) % m);
+}
+
 }  // namespace kz

@@ -215,7 +215,7 @@ class DeviceSystem:
         """One iteration of this shard's workers from the resident x; writes the
         un-normalised worker sum S = sum_t v_t to `partial_ptr` (device)."""
         variant = cfg.variant
-        q = 1 if variant == "rk" else cfg.q
+        q = 1 if variant in ("rk", "ck") else cfg.q
         al = N.f64(np.ones(q) if alphas is None else alphas)
         p = N.Params()
         p.variant = N.VARIANT_IDS[variant]
@@ -337,7 +337,7 @@ def _uniform_alpha(alphas: np.ndarray) -> float:
 def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, trace_step=None, capture=None,
            lead_row: bool = False, checkpoint_every: int | None = None) -> RunReport:
     cfg.validate()
-    q = 1 if variant == "rk" else cfg.q
+    q = 1 if variant in ("rk", "ck") else cfg.q
     steps = cfg.block_size + (1 if lead_row else 0) if variant == "rkab" else 1
     alphas = N.f64(resolve_alphas(system, cfg, q))
     if budget is not None and budget < 1:
@@ -436,6 +436,13 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
     )
 
 
+def solve_ck(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
+             checkpoint_every=None) -> RunReport:
+    """Cyclic Kaczmarz: rows in order i = k mod m (solvers.py:271-291)."""
+    return _solve(system, cfg, "ck", x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture,
+                  checkpoint_every=checkpoint_every)
+
+
 def solve_rk(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
              checkpoint_every=None) -> RunReport:
     """Randomized Kaczmarz, worker stream 0 (solvers.py:294-310)."""
@@ -482,7 +489,8 @@ def run_solver(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step
             raise ValueError("cgls supports neither fixed-budget replay nor tracing")
         return _run_cgls(system, cfg, x_ref)
     if cfg.variant == "ck":
-        raise NotImplementedError("cyclic Kaczmarz (solvers.py:271-291) is outside the B200 hot path")
+        return solve_ck(system, cfg, x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture,
+                        checkpoint_every=checkpoint_every)
     if cfg.engine == "threads" and trace_step is not None:
         raise ValueError("tracing is supported by the sequential engine only")
     kw = dict(x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture, checkpoint_every=checkpoint_every)

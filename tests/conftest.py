@@ -46,6 +46,7 @@ def systems():
     out["c0"] = G.generate_mother(G.GeneratorConfig(m_max=2000, n_max=50, seed=0))
     out["s500"] = G.generate_mother(G.GeneratorConfig(m_max=500, n_max=20, seed=1))
     out["s2000"] = G.generate_mother(G.GeneratorConfig(m_max=2000, n_max=50, seed=7))
+    out["crop300x40"] = G.crop(out["s2000"], 300, 40)
     return out
 
 

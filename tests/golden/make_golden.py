@@ -170,5 +170,39 @@ def main():
     print("all done", time.time() - t0)
 
 
+def gen_ck():
+    """Cyclic Kaczmarz (solvers.py:271-291): rows i = k mod m, no stream."""
+    t0 = time.time()
+    c0 = system(2000, 50, 0)
+    s500 = system(500, 20, 1)
+    s2000 = system(2000, 50, 7)
+    crop = kb.crop(s2000, 300, 40)
+    out = {}
+
+    def record(tag, sys_, cfg, every, **kw):
+        cap = []
+        r = kb.run_solver(sys_, cfg, capture=cap, **kw)
+        out[f"{tag}_iterations"] = np.array(r.iterations)
+        out[f"{tag}_error_evals"] = np.array(r.error_evals)
+        out[f"{tag}_converged"] = np.array(r.converged)
+        out[f"{tag}_final_error_sq"] = np.array(r.final_error_sq)
+        out[f"{tag}_x"] = r.x.copy()
+        out[f"{tag}_every"] = np.array(every)
+        out[f"{tag}_ckpt"] = np.array(cap[every - 1::every]) if len(cap) >= every else np.zeros((0, sys_.n))
+        print(tag, r.iterations, r.converged, f"{time.time() - t0:.1f}s", flush=True)
+
+    record("c0_ck", c0, kb.SolverConfig(variant="ck"), 100)
+    record("s500_ck", s500, kb.SolverConfig(variant="ck"), 1)
+    record("s2000_ck_fixed", s2000, kb.SolverConfig(variant="ck", alpha_policy="fixed", alpha=1.5), 10)
+    record("crop300x40_ck", crop, kb.SolverConfig(variant="ck"), 10)
+    record("s500_ck_budget777", s500, kb.SolverConfig(variant="ck"), 1, budget=777)
+    record("c0_ck_max300", c0, kb.SolverConfig(variant="ck", max_iterations=300), 10)
+    save("ck.npz", **out)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "ck":
+        gen_ck()
+    else:
+        main()
+        gen_ck()

@@ -241,3 +241,26 @@ def test_multi_cluster_oracle_c2(gpu, oracle, c2_system, q, ctas):
         solve_rka_seq(ds, _cfg(variant="rka", q=q, base_seed=2, kernel=kernel, ctas=ctas), capture=cap)
         for j, ck in enumerate(o["checkpoints"]):
             assert rel_err(cap[250 * (j + 1) - 1], ck) <= PARITY_TOL, (q, j)
+
+
+CK_CASES = [("c0_ck", "c0", {}, {}), ("s500_ck", "s500", {}, {}),
+            ("s2000_ck_fixed", "s2000", dict(alpha_policy="fixed", alpha=1.5), {}),
+            ("crop300x40_ck", "crop300x40", {}, {}), ("s500_ck_budget777", "s500", {}, dict(budget=777)),
+            ("c0_ck_max300", "c0", dict(max_iterations=300), {})]
+
+
+@pytest.mark.parametrize("tag,sysname,cfgkw,kw", CK_CASES, ids=[c[0] for c in CK_CASES])
+def test_cyclic_kaczmarz_matches_reference(gpu, systems, tag, sysname, cfgkw, kw):
+    """solve_ck (solvers.py:271-291) through the B200 engine vs the reference's own run."""
+    from paper_2401_17474_b200 import run_solver
+
+    g = golden("ck.npz")
+    cap = []
+    r = run_solver(systems[sysname], _cfg(variant="ck", **cfgkw), capture=cap, **kw)
+    assert r.iterations == int(g[f"{tag}_iterations"])
+    assert r.error_evals == int(g[f"{tag}_error_evals"])
+    assert r.converged == bool(g[f"{tag}_converged"])
+    assert rel_err(r.x, g[f"{tag}_x"]) <= PARITY_TOL
+    every = int(g[f"{tag}_every"])
+    for j, ck in enumerate(g[f"{tag}_ckpt"]):
+        assert rel_err(cap[every * (j + 1) - 1], ck) <= PARITY_TOL, (tag, j)

@@ -105,3 +105,21 @@ def test_zero_row_is_degenerate(oracle):
     A = np.array([[1.0, 0.0], [0.0, 0.0], [0.0, 1.0]])
     with pytest.raises(ValueError, match="row 1"):
         oracle.solve(A, np.ones(3), np.zeros(2))
+
+
+def test_oracle_cyclic_kaczmarz_matches_reference(oracle, systems):
+    """The oracle's CK restatement against the reference's solve_ck fixtures (golden/ck.npz)."""
+    g = golden("ck.npz")
+    cases = [("c0_ck", "c0", {}, None), ("s500_ck", "s500", {}, None),
+             ("s2000_ck_fixed", "s2000", {"alphas": 1.5}, None), ("crop300x40_ck", "crop300x40", {}, None),
+             ("s500_ck_budget777", "s500", {}, 777), ("c0_ck_max300", "c0", {"max_iterations": 300}, None)]
+    for tag, name, kw, budget in cases:
+        s = systems[name]
+        every = int(g[f"{tag}_every"])
+        o = oracle.solve(s.A, s.b, s.x_star, variant="ck", budget=budget, ckpt_every=every, **kw)
+        assert o["iterations"] == int(g[f"{tag}_iterations"]), tag
+        assert o["error_evals"] == int(g[f"{tag}_error_evals"]), tag
+        assert o["converged"] == bool(g[f"{tag}_converged"]), tag
+        assert rel_err(o["x"], g[f"{tag}_x"]) <= PARITY_TOL, tag
+        for j, ck in enumerate(g[f"{tag}_ckpt"]):
+            assert rel_err(o["checkpoints"][j], ck) <= PARITY_TOL, (tag, j)
