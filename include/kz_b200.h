@@ -40,7 +40,8 @@ enum kz_status {
     KZ_EEMPTYRANGE = 3, /* EmptyRangeError (sampling.py:194-195, 213-218)                            */
     KZ_ENOMEM = 4,      /* device allocation failed                                                  */
     KZ_ECUDA = 5,       /* CUDA runtime / launch error                                               */
-    KZ_ENODEV = 6       /* no CUDA device                                                            */
+    KZ_ENODEV = 6,      /* no CUDA device                                                            */
+    KZ_ENOCONV = 7      /* ConvergenceError (cgls.py:71-75): iterate returned, tolerance not met     */
 };
 
 enum kz_variant { KZ_RK = 0, KZ_RKA = 1, KZ_RKAB = 2, KZ_CK = 3 };          /* solvers.py:55 VARIANTS        */
@@ -180,6 +181,14 @@ KZ_API int32_t kz_error_sq(kz_system* sys, double* err_host, void* stream);
 /* ---- norms used by traces and reports (solvers.py:174-179, 246) ---------- */
 /* ||A x - b||_2 and ||x - x_ref||_2 for a host x (n values). */
 KZ_API int32_t kz_norms(kz_system* sys, const double* x_host, double* residual, double* error, void* stream);
+
+/* CGLS on the resident matrix (replaces cgls.py:42-75 `cgls_solve`): x_out[n]
+ * = argmin ||A x - b|| with the reference's stop rule ||A^T(Ax-b)|| <= tol ||A^T b||
+ * and one restart.  b_host = NULL uses the system's b.  max_it <= 0 means
+ * 10 n + 100.  KZ_ENOCONV when the budget runs out (x_out holds the best
+ * iterate, like ConvergenceError.best_x). */
+KZ_API int32_t kz_cgls(kz_system* sys, const double* b_host, double tol, int64_t max_it, double* x_out,
+                       int64_t* iterations, void* stream);
 
 #ifdef __cplusplus
 }

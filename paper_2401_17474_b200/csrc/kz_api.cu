@@ -165,6 +165,7 @@ struct kz_system {
     DevBuf<SolveStatus> status;
     DevBuf<unsigned long long> zero_row;
     DevBuf<long long> dbg;
+    DevBuf<double> cg;  // CGLS work vectors (kz_cgls)
     SolveStatus* h_status = nullptr;  // pinned
     bool norms_valid = false;
     bool bs2_valid = false;
@@ -1358,3 +1359,112 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     }
     return KZ_OK;
 }
+
+// ---------------------------------------------------------------------------
+// CGLS on the resident matrix (cgls.py:42-75): x_LS of min ||A x - b|| with the
+// reference's stopping rule ||A^T (A x - b)|| <= tol ||A^T b|| and one restart.
+// ---------------------------------------------------------------------------
+extern "C" int32_t kz_cgls(kz_system* s, const double* b_host, double tol, int64_t max_it, double* x_out,
+                           int64_t* iterations, void* stream) {
+    if (!s || !x_out) return fail(KZ_EINVAL, "null argument");
+    if (!(tol > 0)) return fail(KZ_EINVAL, "tol must be > 0, got %g", tol);
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    const int64_t m = s->m, n = s->n, ld = s->ld;
+    if (max_it <= 0) max_it = 10 * n + 100;
+    const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>((int64_t)s->sms * 4, (m + 255) / 256));
+    const int64_t rpc = (m + nchunks - 1) / nchunks;
+    // layout: x | p | s (ld each) | r | t | b (m each) | partial (nchunks x ld) | scalars (8)
+    const size_t need = 3 * (size_t)ld + 3 * (size_t)m + (size_t)nchunks * ld + 8;
+    KZ_TRY(s->cg.ensure(need));
+    double* x = s->cg.p;
+    double* pv = x + ld;
+    double* sv = pv + ld;
+    double* r = sv + ld;
+    double* t = r + m;
+    double* bb = t + m;
+    double* part = bb + m;
+    double* scal = part + (size_t)nchunks * ld;  // [0] gamma, [1] delta, [2] gamma_new, [3] scratch
+    if (b_host)
+        KZ_CUDA(cudaMemcpyAsync(bb, b_host, m * sizeof(double), cudaMemcpyHostToDevice, st));
+    else
+        KZ_CUDA(cudaMemcpyAsync(bb, s->b.p, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    const unsigned rows_blocks = (unsigned)((m + 7) / 8);
+    const dim3 tgrid((unsigned)((n + 255) / 256), (unsigned)nchunks);
+    const unsigned eblocks = (unsigned)std::min<int64_t>(1024, (std::max(n, m) + 255) / 256);
+    auto gemv_t = [&](const double* vec, double* out) -> int {  // out = A^T vec
+        cg_gemv_t_partial_kernel<<<tgrid, 256, 0, st>>>(s->A.p, vec, m, n, ld, rpc, part);
+        KZ_TRY(check_launch("cg_gemv_t_partial_kernel"));
+        cg_gemv_t_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nchunks, n, ld, out);
+        return check_launch("cg_gemv_t_reduce_kernel");
+    };
+    auto dot = [&](const double* u, const double* v, int64_t len, int slot, double* host) -> int {
+        cg_dot_kernel<<<1, 1024, 0, st>>>(u, v, len, scal + slot);
+        KZ_TRY(check_launch("cg_dot_kernel"));
+        if (host) {
+            KZ_CUDA(cudaMemcpyAsync(host, scal + slot, sizeof(double), cudaMemcpyDeviceToHost, st));
+            KZ_CUDA(cudaStreamSynchronize(st));
+        }
+        return KZ_OK;
+    };
+    KZ_CUDA(cudaMemsetAsync(x, 0, ld * sizeof(double), st));
+    double ref2 = 0.0;
+    KZ_TRY(gemv_t(bb, sv));
+    KZ_TRY(dot(sv, sv, n, 3, &ref2));
+    const double ref = std::sqrt(ref2);
+    int64_t used = 0;
+    bool ok = ref == 0.0;
+    if (!ok) {
+        const double abs_tol = tol * ref;
+        for (int pass = 0; pass < 2; ++pass) {
+            cg_gemv_n_kernel<<<rows_blocks, 256, 0, st>>>(s->A.p, x, bb, m, n, ld, 1, r);  // r = b - A x
+            KZ_TRY(check_launch("cg_gemv_n_kernel"));
+            KZ_TRY(gemv_t(r, sv));
+            KZ_CUDA(cudaMemcpyAsync(pv, sv, ld * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            double gamma = 0.0;
+            KZ_TRY(dot(sv, sv, n, 0, &gamma));
+            int64_t it_used = max_it - used;
+            for (int64_t it = 1; it <= max_it - used; ++it) {
+                if (std::sqrt(gamma) <= abs_tol) {
+                    it_used = it - 1;
+                    break;
+                }
+                cg_gemv_n_kernel<<<rows_blocks, 256, 0, st>>>(s->A.p, pv, nullptr, m, n, ld, 0, t);  // t = A p
+                KZ_TRY(check_launch("cg_gemv_n_kernel"));
+                double delta = 0.0;
+                KZ_TRY(dot(t, t, m, 1, &delta));
+                if (delta == 0.0) {
+                    it_used = it - 1;
+                    break;
+                }
+                cg_update_xr_kernel<<<eblocks, 256, 0, st>>>(x, pv, r, t, scal, n, m);
+                KZ_TRY(check_launch("cg_update_xr_kernel"));
+                KZ_TRY(gemv_t(r, sv));
+                double gamma_new = 0.0;
+                KZ_TRY(dot(sv, sv, n, 2, &gamma_new));
+                cg_update_p_kernel<<<eblocks, 256, 0, st>>>(pv, sv, scal, n);
+                KZ_TRY(check_launch("cg_update_p_kernel"));
+                KZ_CUDA(cudaMemcpyAsync(scal, scal + 2, sizeof(double), cudaMemcpyDeviceToDevice, st));
+                gamma = gamma_new;
+            }
+            used += it_used;
+            // verify on a freshly computed normal-equations residual (cgls.py:66-68)
+            cg_gemv_n_kernel<<<rows_blocks, 256, 0, st>>>(s->A.p, x, bb, m, n, ld, 1, r);
+            KZ_TRY(check_launch("cg_gemv_n_kernel"));
+            KZ_TRY(gemv_t(r, sv));
+            double tr2 = 0.0;
+            KZ_TRY(dot(sv, sv, n, 3, &tr2));
+            if (std::sqrt(tr2) <= abs_tol) {
+                ok = true;
+                break;
+            }
+            if (used >= max_it) break;
+        }
+    }
+    KZ_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    if (iterations) *iterations = used;
+    if (!ok) return fail(KZ_ENOCONV, "CGLS did not reach tol=%g within %lld iterations", tol, (long long)max_it);
+    return KZ_OK;
+}
+

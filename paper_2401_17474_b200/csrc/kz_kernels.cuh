@@ -68,6 +68,21 @@ __global__ void rka_kernel(const __grid_constant__ SolveArgs a, const __grid_con
 __global__ void row_sqnorm_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
                                   double* __restrict__ sq, unsigned long long* __restrict__ first_zero);
 __global__ void cyclic_rows_kernel(int32_t* __restrict__ idx, int64_t k0, int64_t count, int64_t m);
+// CGLS (kz_cgls.cu)
+__global__ void cg_gemv_n_kernel(const double* __restrict__ A, const double* __restrict__ x,
+                                 const double* __restrict__ b, int64_t m, int64_t n, int64_t ld, int mode,
+                                 double* __restrict__ y);
+__global__ void cg_gemv_t_partial_kernel(const double* __restrict__ A, const double* __restrict__ r, int64_t m,
+                                         int64_t n, int64_t ld, int64_t rows_per_chunk, double* __restrict__ partial);
+__global__ void cg_gemv_t_reduce_kernel(const double* __restrict__ partial, int64_t nchunks, int64_t n, int64_t ld,
+                                        double* __restrict__ s);
+__global__ void cg_dot_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                              double* __restrict__ out);
+__global__ void cg_update_xr_kernel(double* __restrict__ x, const double* __restrict__ p, double* __restrict__ r,
+                                    const double* __restrict__ t, const double* __restrict__ scal, int64_t n,
+                                    int64_t m);
+__global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restrict__ s,
+                                   const double* __restrict__ scal, int64_t n);
 constexpr int CDF_SCAN_THREADS = 256;
 __global__ void cdf_scan_kernel(const double* __restrict__ sq, const int64_t* __restrict__ lo,
                                 const int64_t* __restrict__ len, int64_t nranges, double* __restrict__ cdf);

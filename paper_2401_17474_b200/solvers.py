@@ -253,6 +253,24 @@ class DeviceSystem:
         N.check(self._lib.kz_norms(self.handle, N.ptr(xv), C.byref(res), C.byref(err), None))
         return res.value, err.value
 
+    def cgls(self, b=None, tol: float = 1e-10, max_it: int | None = None) -> np.ndarray:
+        """x_LS = argmin ||A x - b|| on the device (cgls.py:42-75 `cgls_solve`); b defaults to the
+        system's right-hand side.  Raises ConvergenceError (best_x attached) like the reference."""
+        bv = None if b is None else N.f64(b)
+        if bv is not None and bv.shape != (self.m,):
+            raise DimensionMismatchError(f"b has shape {bv.shape}, expected ({self.m},)")
+        x = np.empty(self.n)
+        its = C.c_int64()
+        rc = self._lib.kz_cgls(self.handle, N.ptr(bv) if bv is not None else None, C.c_double(float(tol)),
+                               C.c_int64(int(max_it) if max_it is not None else 0), N.ptr(x), C.byref(its), None)
+        if rc == N.KZ_ENOCONV:
+            from .errors import ConvergenceError
+
+            raise ConvergenceError(self._lib.kz_last_error().decode(errors="replace"), best_x=x)
+        N.check(rc)
+        self.cgls_iterations = int(its.value)
+        return x
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             self._lib.kz_system_destroy(self.handle)
@@ -465,19 +483,27 @@ def solve_rkab_seq(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_
 
 
 def _run_cgls(system, cfg, x_ref):
-    """harness._run_cgls (harness.py:343-366): host CGLS, off the hot path."""
-    host = system.host if isinstance(system, DeviceSystem) else system
+    """harness._run_cgls (harness.py:343-366): CGLS on the device (kz_cgls)."""
     import time
 
-    t0 = time.perf_counter()
-    x = cgls_solve(host.A, host.b, tol=1e-10)
-    wall = time.perf_counter() - t0
-    if x_ref is None and (host.x_star is not None or host.x_ls is not None):
-        x_ref = host.x_ref()
-    err = float(np.dot(x - x_ref, x - x_ref)) if x_ref is not None else float("nan")
+    own = not isinstance(system, DeviceSystem)
+    ds = _pool_acquire(system, cfg.device) if own else system
+    try:
+        t0 = time.perf_counter()
+        x = ds.cgls(tol=1e-10)
+        wall = time.perf_counter() - t0
+        host = system if own else system.host
+        if x_ref is None and host is not None and (host.x_star is not None or host.x_ls is not None):
+            x_ref = host.x_ref()
+        if x_ref is not None:
+            ds.set_x_ref(x_ref)
+        res, err = ds.norms(x)
+    finally:
+        if own:
+            _pool_release(ds)
     return RunReport(variant="cgls", q=1, block_size=1, alpha_policy=cfg.alpha_policy, alpha=float("nan"),
-                     seed=cfg.base_seed, iterations=-1, converged=True, wall_time_s=wall, final_error_sq=err,
-                     final_residual=float(np.linalg.norm(host.A @ x - host.b)), x=x)
+                     seed=cfg.base_seed, iterations=-1, converged=True, wall_time_s=wall,
+                     final_error_sq=err * err if x_ref is not None else float("nan"), final_residual=res, x=x)
 
 
 def run_solver(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,

@@ -264,3 +264,35 @@ def test_cyclic_kaczmarz_matches_reference(gpu, systems, tag, sysname, cfgkw, kw
     every = int(g[f"{tag}_every"])
     for j, ck in enumerate(g[f"{tag}_ckpt"]):
         assert rel_err(cap[every * (j + 1) - 1], ck) <= PARITY_TOL, (tag, j)
+
+
+def test_device_cgls_matches_reference_xls(gpu, inc2000):
+    """kz_cgls (cgls.py:42-75 on the device) reproduces the reference's x_LS of the
+    inconsistent fixture system to rounding; the budget error mirrors ConvergenceError."""
+    from paper_2401_17474_b200 import DeviceSystem, errors, run_solver
+
+    g = golden("systems.npz")
+    with DeviceSystem(inc2000) as ds:
+        x = ds.cgls(tol=1e-12)
+        assert rel_err(x, g["inc2000_xls"]) <= 1e-9
+        # the reference's stop rule holds on a fresh residual
+        A, b = inc2000.A, inc2000.b
+        assert np.linalg.norm(A.T @ (A @ x - b)) <= 1e-12 * np.linalg.norm(A.T @ b) * 10
+        with pytest.raises(errors.ConvergenceError) as ei:
+            ds.cgls(tol=1e-14, max_it=2)
+        assert ei.value.best_x is not None and ei.value.best_x.shape == (A.shape[1],)
+    r = run_solver(inc2000, _cfg(variant="cgls"))
+    assert rel_err(r.x, g["inc2000_xls"]) <= 1e-7
+
+
+def test_device_cgls_c4_shape(gpu):
+    """c4 shape (80000 x 2000, b_LS = b + xi): device CGLS vs the host restatement."""
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, generate_mother
+    from paper_2401_17474_b200.sysgen import Prng, cgls_solve
+
+    s = generate_mother(GeneratorConfig(m_max=20000, n_max=800, seed=3))
+    b_ls = s.b + Prng(5, 3).standard_normal(s.A.shape[0])
+    x_host = cgls_solve(s.A, b_ls, tol=1e-12)
+    with DeviceSystem(s) as ds:
+        x_dev = ds.cgls(b=b_ls, tol=1e-12)
+    assert rel_err(x_dev, x_host) <= 1e-9
