@@ -286,6 +286,32 @@ def extra_workloads(device, peak, steps=3):
         measure("c4_rk_q1", ds, 2000, SolverConfig(variant="rk", device=device), 20000,
                 "c4 shape 80000x2000: RK (q=1), 20000 iterations per step")
         ds.close()
+        # c4 proper: inconsistent b_LS = b + xi (sysgen.py:175-176), x_LS by CGLS on the device,
+        # RKA horizons = mean of the last 10 trace records (harness.py:192-196), SURVEY 8(d) budgets
+        from paper_2401_17474_b200 import LinearSystem
+        from paper_2401_17474_b200.sysgen import TAG_NOISE, Prng
+
+        b_ls = s4.b + Prng(0, TAG_NOISE).standard_normal(size=s4.m)
+        inc = LinearSystem(A=s4.A, b=b_ls, x_star=None, x_ls=None, consistent=False, seed=0)
+        ds = DeviceSystem(inc, device=device)
+        t0 = time.perf_counter()
+        x_ls = ds.cgls(tol=1e-12)
+        cg_ms = (time.perf_counter() - t0) * 1e3
+        for q, budget in ((1, 120000), (64, 60000), (512, 48000)):
+            cfg = SolverConfig(variant="rka" if q > 1 else "rk", q=q, device=device, max_iterations=budget)
+            r = run_solver(ds, cfg, x_ref=x_ls, trace_step=1000)
+            tail = [t.error_norm for t in r.trace[-10:]]
+            h = float(np.mean(tail))
+            g = r.gpu
+            gbs = g["rows_projected"] * 8 * 2000 / (g["kernel_ms"] / 1e3) / 1e9
+            out.append({"workload": f"c4_horizon_q{q}", "desc": f"c4: 80000x2000 inconsistent (noise seed 0), "
+                        f"{'RK' if q == 1 else 'RKA'} q={q}, {budget} iterations, trace every 1000 vs CGLS x_LS",
+                        "rows_per_s": g["rows_projected"] / (g["loop_ms"] / 1e3), "ms_per_step": g["loop_ms"],
+                        "iterations": [r.iterations], "kernel": g["kernel"], "ctas": g["ctas"],
+                        "horizon_norm": h, "horizon_sq": h * h, "trace_records": len(r.trace),
+                        "cgls_ms": cg_ms, "cgls_iterations": ds.cgls_iterations,
+                        "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak}})
+        ds.close()
         s2 = generate_mother(GeneratorConfig(m_max=80000, n_max=1000, seed=0))
         ds = DeviceSystem(s2, device=device)
         measure("c2", ds, 1000, SolverConfig(variant="rkab", q=64, block_size=500, device=device), None,
