@@ -829,7 +829,7 @@ namespace {
 
 template <bool TM>
 void* rka_fn_t(int lg, int epl) {
-    if (lg == 8) return (void*)rka_kernel<8, 1, TM>;
+    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM> : (void*)rka_kernel<8, 1, TM>;
     if (lg == 16) return (void*)rka_kernel<16, 1, TM>;
     switch (epl) {
         case 1: return (void*)rka_kernel<32, 1, TM>;
@@ -936,8 +936,10 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
             continue;
         }
         const int npairs = box / 2;
-        const int lg = npairs <= 8 ? 8 : (npairs <= 16 ? 16 : 32);
-        const int epl = lg == 32 ? (npairs + 31) / 32 : 1;
+        int lg = npairs <= 8 ? 8 : (npairs <= 16 ? 16 : 32);
+        int epl = lg == 32 ? (npairs + 31) / 32 : 1;
+        if (const char* e = getenv("KZ_RKA_LG8"))  // experiment: 8 lanes per row, 2 pairs per lane
+            if (atoi(e) && npairs <= 16) lg = 8, epl = 2;
         const size_t stage = (size_t)((q + 3) & ~3) * box * sizeof(double) + (size_t)((q + 3) & ~3) * 32;
         const size_t fixed = rka_smem(q, box, 0, Pc);
         int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);

@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     }
 
     // ================= compute warps =================
-    constexpr int OW = NW - 1;  // owner warp
+    constexpr int OW = NW - 1;    // owner warp of the error total
+    constexpr int NOWN = 2;       // owner warps (NW - NOWN .. NW - 1) splitting the worker pairs
     const int gl = lane % LG, grp = lane / LG;
     double2 xv[EPL];
     for (int j = tid; j < cwb; j += NW * 32) xrs[j] = j < wdt ? a.xref[c0 + j] : 0.0;
@@ -194,17 +195,25 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int count = (int)a.count;
     const bool use_stop = opaque_i32(a.use_stop) != 0, final_check = opaque_i32(a.final_check) != 0;
     const int cnt2 = Pc >= 2 ? Pc / 2 : 1;  // partials per lane in the owner's tree (2 lanes per item)
-    const bool split = TIMING && (a.ablate & 16) ? true : cwb >= 64;  // combine layout (see below)
+    bool unit_alpha = true;
+    for (int t = 0; t < q; ++t) unit_alpha = unit_alpha && alp[t] == 1.0;
+    const bool split = TIMING && (a.ablate & 16) ? true : (cwb >= 64 || LG == 8);  // combine layout (see below)
     const int ppw = ((wdt >> 1) + NW - 1) / NW;                      // column pairs per warp (split)
     const int u = lane & 1;
 
     // owner tree: item i's Pc partials (stride `stride`) added by lanes 2i, 2i+1 in one fixed order
     auto owner_total = [&](const double* base, int stride, bool live) -> double {
         double v[8];
+        if (Pc == 16) {  // the common cluster: 8 partials per lane, no bounds
+            const double* bp = base + u * 8 * stride;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int cc = u * cnt2 + k;
-            v[k] = (live && k < cnt2 && cc < Pc) ? base[cc * stride] : 0.0;
+            for (int k = 0; k < 8; ++k) v[k] = live ? bp[k * stride] : 0.0;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int cc = u * cnt2 + k;
+                v[k] = (live && k < cnt2 && cc < Pc) ? base[cc * stride] : 0.0;
+            }
         }
         double tot = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         tot += __shfl_xor_sync(0xffffffffu, tot, 1);
@@ -327,24 +336,31 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 2] = clock64();
         // the next stage's rows are awaited now, while the exchange is in flight
         ready = false;
-        if (warp != OW && kk + 1 < count) {
+        if (warp < NW - NOWN && kk + 1 < count) {
             const int st1 = st + 1 == D ? 0 : st + 1;
             mbar_wait(&full[st1], st + 1 == D ? fph ^ 1u : fph);
             ready = true;
         }
         // ---- 3. owner: totals of its workers, scales, broadcast; then the error total -------
-        if (warp == OW) {
+        if (warp >= NW - NOWN) {
+            // NOWN owner warps: warp ow takes the worker pairs ow, ow + NOWN, ... of this CTA
+            const int ow = warp - (NW - NOWN);
             const unsigned tag = (unsigned)kk + 1u;
             unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * q1 * 2;
-            if (!last && n_own > 0) {
+            const int npair = (n_own + 1) / 2;
+            const int my_pairs = npair > ow ? (npair - ow + NOWN - 1) / NOWN : 0;
+            if (!last && my_pairs > 0) {
                 mbar_wait(&xbar[par], bpar);
                 if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 7] = clock64();
                 const double* ib = inbuf + par * Pc * RPO;
-                for (int i0 = 0; i0 < n_own; i0 += 16) {
-                    const int i = i0 + (lane >> 1);
-                    const bool live = i < n_own;
+                for (int l0 = 0; l0 < 2 * my_pairs; l0 += 16) {  // 16 items per pass, 2 lanes each
+                    const int li = l0 + (lane >> 1);
+                    const int i = 2 * (ow + NOWN * (li >> 1)) + (li & 1);
+                    const bool live = li < 2 * my_pairs && i < n_own;
                     const int t = my_lo + i;
                     double tot = owner_total(ib + i, RPO, live);
+                    if (TIMING && rec && warp == NW - NOWN && l0 == 0)
+                        a.dbg[(kk * 8 + warp) * 16 + 10] = clock64() + (long long)(tot * 0.0);
                     if (G > 1 && u == 0 && live) {
                         // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
                         ll_store(ll + ((size_t)gid * q1 + t) * 2, tot, tag);
@@ -352,16 +368,19 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     }
                     if (live && u == 0) {
                         const double* rec4 = bsr + 4 * t;  // (b, sq, 1/sq, 0)
-                        const double nume = __dmul_rn(alp[t], __dsub_rn(rec4[0], tot));
+                        const double d = __dsub_rn(rec4[0], tot);
+                        const double nume = unit_alpha ? d : __dmul_rn(alp[t], d);  // 1 * d == d exactly
                         sout[i] = div_rn_fast(nume, rec4[1], rec4[2]);
+                        if (TIMING && a.dbg != nullptr && c == 0 && lane == 0 && kk < 32 && warp == NW - NOWN &&
+                            l0 == 0)
+                            a.dbg[(kk * 8 + warp) * 16 + 11] = clock64() + (long long)(sout[i] * 0.0);
                     }
                 }
                 __syncwarp();
                 if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 8] = clock64();
-                // broadcast: worker pairs (i, i + 1) as 16-byte pushes to every CTA of the cluster
-                const int npair = (n_own + 1) / 2;
-                for (int k = lane; k < npair * Pc; k += 32) {
-                    const int pi = k >> pcs, peer = k & (Pc - 1);
+                // broadcast: this warp's worker pairs as 16-byte pushes to every CTA of the cluster
+                for (int k = lane; k < my_pairs * Pc; k += 32) {
+                    const int pi = ow + NOWN * (k >> pcs), peer = k & (Pc - 1);
                     const int i = 2 * pi, t = my_lo + i;
                     const unsigned dst =
                         mapa_u32(scal_u, (unsigned)peer) + (unsigned)((par * q4 + t) * (int)sizeof(double));
@@ -373,7 +392,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 }
                 if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 9] = clock64();
             }
-            if (want_check && cr == eown) {
+            if (warp == OW && want_check && cr == eown) {
                 mbar_wait(&ebin[par], bpar);
                 if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 10] = clock64();
                 double tot = owner_total(ein + par * Pc, 1, lane < 2);
@@ -580,6 +599,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
 template __global__ void rka_kernel<8, 1, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
 template __global__ void rka_kernel<8, 1, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<8, 2, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<8, 2, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
 template __global__ void rka_kernel<16, 1, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);

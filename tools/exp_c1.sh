@@ -1,4 +1,5 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-export KZ_PHASE_TIMING=1
-for A in 0 16; do echo "== c1 ablate=$A"; KZ_ABLATE=$A python tools/prof_case.py --workload c1 --budget 3000 --solves 1 2>&1 | grep -v "^system" | tail -2; done
+for L in 0 1; do echo "== LG8=$L"; KZ_RKA_LG8=$L python tools/prof_case.py --workload c1 --solves 2 2>&1 | tail -1; done
+export KZ_PHASE_TIMING=2
+KZ_RKA_LG8=1 python tools/prof_case.py --workload c1 --budget 3000 --solves 1 2>&1 | grep -v "^system" | tail -10

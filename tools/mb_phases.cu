@@ -133,6 +133,15 @@ __global__ void __launch_bounds__(256, 1) phase_kernel(long long* out, double* s
             mbar_wait(&mb[1], (unsigned)(it & 1));
         } else if (MODE == 12) {  // clock64 stamp to global
             if (lane == 0) sink[512 + warp] = (double)clock64();
+        } else if (MODE == 13) {  // the in-kernel probe: 16 dependent LDS then 32 dependent DADD/DMUL
+            int zi = ((int)xv.x) & 1;
+#pragma unroll
+            for (int zz = 0; zz < 16; ++zz) zi = (int)scal[zi] & 1;
+            double z = xv.y + zi;
+#pragma unroll
+            for (int zz = 0; zz < 32; ++zz) z = __dadd_rn(z, z * 1e-3);
+            xv.x += z * 1e-30;
+            xv.y = z;
         } else if (MODE == 5) {  // owner: 8 smem loads, tree, shfl, division
             double v[8];
 #pragma unroll
@@ -159,8 +168,8 @@ int main() {
     const int reps = 2000;
     const char* names[] = {"dots+reduce", "dots only", "avg+barrier+combine", "avg only", "warp_sum", "owner",
                            "named barrier", "sts+bar+lds8+tree", "ddiv", "shfl-add level", "try_wait done",
-                           "arrive+wait", "clock stamp"};
-    for (int mode = 0; mode < 13; ++mode) {
+                           "arrive+wait", "clock stamp", "probe 16 LDS + 32 DADD/DMUL"};
+    for (int mode = 0; mode < 14; ++mode) {
         for (int nw : {1, 8}) {
             switch (mode) {
                 case 0: phase_kernel<0><<<1, 32 * nw>>>(d_out, d_sink, reps); break;
@@ -176,6 +185,7 @@ int main() {
                 case 10: phase_kernel<10><<<1, 32 * nw>>>(d_out, d_sink, reps); break;
                 case 11: if (nw == 1) phase_kernel<11><<<1, 32>>>(d_out, d_sink, reps); break;
                 case 12: phase_kernel<12><<<1, 32 * nw>>>(d_out, d_sink, reps); break;
+                case 13: phase_kernel<13><<<1, 32 * nw>>>(d_out, d_sink, reps); break;
             }
             if ((mode == 2 || mode == 6 || mode == 7) && nw == 1) continue;
             if (mode == 11 && nw == 8) continue;
