@@ -59,37 +59,55 @@ struct ChainSmem {
 };
 
 // CTA-wide sums of NV per-thread values; every thread receives every total,
-// bit-identical.  Value-major transpose through shared memory: thread t
-// stores its NV partials at scr[i*T + t]; for each value, nw threads each add
-// 32 consecutive entries (4 interleaved accumulators, 16-byte loads), a fixed
-// xor tree joins the nw pieces, and the totals come back through `tot`.
-// Two CTA barriers; ~NV + 2*NV/nw... instructions per thread instead of 15*NV
-// for per-value shuffle trees.
+// bit-identical.  (1) Inside each warp a transposed shuffle reduction: the NV
+// values (padded to NP = 32 or 64) are halved across lanes at xor offsets
+// 16, 8, 4, 2, 1 -- a lane keeps one half and adds its partner's copy -- so
+// after NP - NP/32 shuffles lane l holds the warp sums of values
+// l * (NP/32) .. +NP/32 (no shared-memory traffic, 5 dependent levels).
+// (2) Those land in scr[warp][NP]; one barrier; thread v < NV adds the nw warp
+// sums in a fixed tree into tot[v]; one barrier; everyone reads tot.
 template <int NV>
 __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double* tot, int tid, int T, int nw) {
+    constexpr int NP = NV <= 32 ? 32 : 64;
+    static_assert(NV <= 64, "cta_reduce: at most 64 values");
+    const int lane = tid & 31, warp = tid >> 5;
+    if (NV <= 4) {  // few values: a butterfly per value (5 NV shuffles, no padding registers)
 #pragma unroll
-    for (int i = 0; i < NV; ++i) scr[i * T + tid] = v[i];
-    __syncthreads();
-    const int lg = 32 - __clz(nw - 1);  // W = 2^lg >= nw lanes per value (zero pieces pad)
-    const int W = 1 << lg;
-    for (int u0 = 0; u0 < NV * W; u0 += T) {
-        const int u = u0 + tid, i = u >> lg, part = u & (W - 1);
-        double sum = 0.0;
-        if (i < NV && part < nw) {
-            const double2* src = reinterpret_cast<const double2*>(scr + i * T + part * 32);
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int i = 0; i < NV; ++i) {
+            double x = v[i];
 #pragma unroll
-            for (int k = 0; k < 16; k += 2) {
-                const double2 x0 = src[k], x1 = src[k + 1];
-                a0 = __dadd_rn(a0, x0.x);
-                a1 = __dadd_rn(a1, x0.y);
-                a2 = __dadd_rn(a2, x1.x);
-                a3 = __dadd_rn(a3, x1.y);
-            }
-            sum = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (lane == i) scr[warp * NP + i] = x;
         }
-        for (int o = W >> 1; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o, W));
-        if (part == 0 && i < NV) tot[i] = sum;
+    } else {
+        double w[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) w[i] = i < NV ? v[i] : 0.0;
+#pragma unroll
+        for (int h = NP / 2, o = 16; o >= 1; h >>= 1, o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const double send = up ? w[i] : w[i + h];
+                const double keep = up ? w[i + h] : w[i];
+                w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        constexpr int PER = NP / 32;  // values per lane after the reduction: indices lane*PER + j
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (lane * PER + j < NV) scr[warp * NP + lane * PER + j] = w[j];
+    }
+    __syncthreads();
+    for (int u = tid; u < NV; u += T) {
+        double a[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) a[k] = k < nw ? scr[k * NP + u] : 0.0;
+#pragma unroll
+        for (int hh = 1; hh < 16; hh <<= 1)
+#pragma unroll
+            for (int k = 0; k + hh < 16; k += 2 * hh) a[k] = __dadd_rn(a[k], a[k + hh]);
+        tot[u] = a[0];
     }
     __syncthreads();
 #pragma unroll
