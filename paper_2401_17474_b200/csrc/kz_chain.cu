@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         if (rec) a.dbg[nblk * 8 + 0] = clock64();
         if (rec) a.dbg[nblk * 8 + 1] = clock64();
         int stg[R];
+        unsigned prs[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             int s0 = c_stage + r;
@@ -283,7 +284,17 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 pr ^= 1u;
             }
             stg[r] = s0;
-            if (r < Rp) mbar_wait(&full[s0], pr);  // row d + r landed
+            prs[r] = pr;
+        }
+        // rows d .. d + Rp - 1 landed: the R barrier probes go out together (one ~90-cycle
+        // round trip instead of R); only stragglers are re-polled
+        {
+            bool okr[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) okr[r] = r >= Rp || mbar_test(&full[stg[r]], prs[r]);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (!okr[r]) mbar_wait(&full[stg[r]], prs[r]);
         }
         if (rec) a.dbg[nblk * 8 + 2] = clock64();
         // rows -> registers (kept for the update), (b, sq) -> lane r

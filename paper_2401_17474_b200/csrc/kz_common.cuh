@@ -389,3 +389,20 @@ __device__ __forceinline__ int opaque_i32(int v) {
 }
 
 }  // namespace kz
+
+namespace kz {
+
+// Non-blocking probe of phase `parity` of a local mbarrier (returns at once).
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+    unsigned done;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+
+}  // namespace kz
