@@ -827,22 +827,25 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
 
 namespace {
 
-template <bool TM>
+template <bool TM, bool SR>
 void* rka_fn_t(int lg, int epl) {
-    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM> : (void*)rka_kernel<8, 1, TM>;
-    if (lg == 16) return (void*)rka_kernel<16, 1, TM>;
+    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM, SR> : (void*)rka_kernel<8, 1, TM, SR>;
+    if (lg == 16) return (void*)rka_kernel<16, 1, TM, SR>;
     switch (epl) {
-        case 1: return (void*)rka_kernel<32, 1, TM>;
-        case 2: return (void*)rka_kernel<32, 2, TM>;
-        case 3: return (void*)rka_kernel<32, 3, TM>;
-        case 4: return (void*)rka_kernel<32, 4, TM>;
+        case 1: return (void*)rka_kernel<32, 1, TM, SR>;
+        case 2: return (void*)rka_kernel<32, 2, TM, SR>;
+        case 3: return (void*)rka_kernel<32, 3, TM, SR>;
+        case 4: return (void*)rka_kernel<32, 4, TM, SR>;
         default: return nullptr;
     }
 }
 
-// the timing variant (per-phase clock stamps) only under KZ_PHASE_TIMING
-void* rka_fn(int lg, int epl) {
-    return getenv("KZ_PHASE_TIMING") ? rka_fn_t<true>(lg, epl) : rka_fn_t<false>(lg, epl);
+// the timing variant (per-phase clock stamps) only under KZ_PHASE_TIMING; SR = one
+// round of 8 rows per warp (q <= 64)
+void* rka_fn(int lg, int epl, bool sr) {
+    const bool tm = getenv("KZ_PHASE_TIMING") != nullptr;
+    if (tm) return sr ? rka_fn_t<true, true>(lg, epl) : rka_fn_t<true, false>(lg, epl);
+    return sr ? rka_fn_t<false, true>(lg, epl) : rka_fn_t<false, false>(lg, epl);
 }
 
 size_t rka_smem(int64_t q, int box, int stages, int Pc) {
@@ -948,7 +951,7 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
             ++G;  // thinner slices
             continue;
         }
-        void* fn = rka_fn(lg, epl);
+        void* fn = rka_fn(lg, epl, q <= 8 * RKA_NW);
         if (!fn) return fail(KZ_EINVAL, "no rka kernel for LG=%d EPL=%d", lg, epl);
         const size_t smem = rka_smem(q, box, stages, Pc);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1021,7 +1024,7 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
         cfg.attrs = attr2;
         cfg.numAttrs = na;
     } else if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER) {
-        fn = pl.tma ? rka_fn(pl.lg, pl.epl) : sync_fn(true, pl.lpr);
+        fn = pl.tma ? rka_fn(pl.lg, pl.epl, args.q <= 8 * RKA_NW) : sync_fn(true, pl.lpr);
         int na = 0;
         attr2[na].id = cudaLaunchAttributeClusterDimension;
         attr2[na].val.clusterDim.x = pl.cluster;

@@ -61,7 +61,7 @@ __global__ void sync_kernel(SolveArgs a);
 constexpr int RKA_NW = 8;                  // compute warps
 constexpr int RKA_NT = (RKA_NW + 1) * 32;  // + the producer warp
 constexpr int RKA_MAXG = 10;               // clusters exchanging through tagged words
-template <int LG, int EPL, bool TIMING>
+template <int LG, int EPL, bool TIMING, bool SR>
 __global__ void rka_kernel(const __grid_constant__ SolveArgs a, const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB);
 

@@ -46,7 +46,7 @@ constexpr int NW = RKA_NW;
 constexpr unsigned CBAR = 1;  // named barrier id of the compute warps
 }  // namespace
 
-template <int LG, int EPL, bool TIMING>
+template <int LG, int EPL, bool TIMING, bool SR>
 __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ SolveArgs a,
                                                         const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB) {
@@ -232,6 +232,12 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     int pcs = 0;
     while ((1 << pcs) < Pc) ++pcs;  // Pc is a power of two
     const bool pusher = (ri & 1) == 0 && (gl & 3) == 0;
+    int rok = 0;  // SR: bit r = row wb + grp NR + r exists
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+        if (wb + grp * NR + r < we) rok |= 1 << r;
+    rok = opaque_i32(rok);
+    const bool push_ok = pusher && t_push0 < we, push_pair = t_push0 + 1 < we;
 
     int st = 0;
     unsigned fph = 0;  // parity of stage st's current full phase
@@ -265,13 +271,14 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         // ---- 1-2. partial dots of this warp's rows -> their owners ------------------------
         if (!last) {
             int o_push = o_push0, s_push = s_push0;  // owner, slot of round 0
-            for (int rb = wb, rofs = 0; rb < we; rb += 8, rofs += rstep) {
+            // SR (q <= 64): exactly one round of 8 rows per warp, row predicates precomputed
+            for (int rb = wb, rofs = 0; SR ? rb == wb && wb < we : rb < we; rb += 8, rofs += rstep) {
                 double acc[NR];
 #pragma unroll
                 for (int r = 0; r < NR; ++r) {
                     acc[r] = 0.0;
                     const int t = rb + grp * NR + r;
-                    if (t < we) {
+                    if (SR ? ((rok >> r) & 1) != 0 : t < we) {
                         const double* row = rows + roff[r] + rofs;
 #pragma unroll
                         for (int e = 0; e < EPL; ++e)
@@ -298,16 +305,16 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 const double odd = __shfl_xor_sync(0xffffffffu, acc[0], 4);
                 if (TIMING && rec && rb == wb) a.dbg[(kk * 8 + warp) * 16 + 15] = clock64() + (long long)(odd * 0.0);
                 const int t = rb + grp * NR + ri;
-                if (t < we && pusher) {
+                if (SR ? push_ok : (t < we && pusher)) {
                     const unsigned off = (unsigned)(((par * Pc + cr) * RPO + s_push) * (int)sizeof(double));
                     const unsigned dst = mapa_u32(inbuf_u, (unsigned)o_push) + off;
                     const unsigned bar = mapa_u32(xbar_u + 8u * par, (unsigned)o_push);
-                    if (t + 1 < we)
+                    if (SR ? push_pair : t + 1 < we)
                         st_async_v2_f64(dst, acc[0], odd, bar);
                     else
                         st_async_f64(dst, acc[0], bar);
                 }
-                if (rb + 8 < we)
+                if (!SR && rb + 8 < we)
                     for (s_push += 8; s_push >= RPO; s_push -= RPO) ++o_push;  // next round: 8 rows on
             }
         }
@@ -423,11 +430,11 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         double2 acc[EPL];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) acc[e] = make_double2(0.0, 0.0);
-        for (int rb = wb; rb < we; rb += 8) {
+        for (int rb = wb; SR ? rb == wb && wb < we : rb < we; rb += 8) {
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
                 const int t = rb + grp * NR + r;
-                if (t < we) {
+                if (SR ? ((rok >> r) & 1) != 0 : t < we) {
                     const double s = sc[t];
                     const double* row = rows + roff[r] + (rb - wb) * cwb;
                     const bool first = (r == 0) && (rb == wb);
@@ -596,33 +603,61 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     }
 }
 
-template __global__ void rka_kernel<8, 1, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 1, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 1, true, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 2, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 2, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 2, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 2, true, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, true, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
 
 }  // namespace kz
