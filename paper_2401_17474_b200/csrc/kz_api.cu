@@ -921,9 +921,10 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         Pc = 1;
         while (2 * Pc <= p->ctas) Pc *= 2;
     } else {
-        // several clusters once a CTA would stage more than ~24 KB of rows per iteration
-        const double bytes = (double)q * (double)ld * sizeof(double);
-        G = (int)std::ceil(bytes / (16.0 * 24 * 1024));
+        // as few clusters as the 256-column TMA box and the shared-memory ring allow: every
+        // extra cluster adds a tagged-word round trip through L2 per iteration (measured:
+        // 80000 x 2000, q = 64: 1 cluster 2.54 us / iteration, 3 clusters 2.89 us)
+        G = 1;
     }
     if (const char* e = getenv("KZ_SYNC_CLUSTERS")) G = atoi(e);
     G = std::max<int>(G, (int)((ld + Pc * 256 - 1) / (Pc * 256)));
