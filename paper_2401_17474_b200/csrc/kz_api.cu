@@ -851,9 +851,11 @@ void* rka_fn(int lg, int epl, bool sr) {
 size_t rka_smem(int64_t q, int box, int stages, int Pc) {
     const int64_t q4 = (q + 3) & ~(int64_t)3;
     const int64_t rpo = (((q + Pc - 1) / Pc) + 1) & ~(int64_t)1;
-    const size_t stage = (size_t)q4 * box * sizeof(double) + (size_t)q4 * 32;
+    const int64_t rpo4 = (rpo + 3) & ~(int64_t)3;
+    const size_t stage = (size_t)q4 * box * sizeof(double) + (size_t)rpo4 * 32;
     return 256 + (size_t)stages * stage +
-           (size_t)(2 * Pc * rpo + 2 * q4 + 2 * Pc + 2 + rpo + RKA_NW * box + 2 * box + q) * sizeof(double);
+           (size_t)(2 * Pc * rpo + 2 * q4 + 2 * Pc + 2 + rpo + RKA_NW * box + 2 * box + q) * sizeof(double) +
+           (size_t)q * sizeof(int32_t);
 }
 
 typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -944,7 +946,7 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         int epl = lg == 32 ? (npairs + 31) / 32 : 1;
         if (const char* e = getenv("KZ_RKA_LG8"))  // experiment: 8 lanes per row, 2 pairs per lane
             if (atoi(e) && npairs <= 16) lg = 8, epl = 2;
-        const size_t stage = (size_t)((q + 3) & ~3) * box * sizeof(double) + (size_t)((q + 3) & ~3) * 32;
+        const size_t stage = rka_smem(q, box, 1, Pc) - rka_smem(q, box, 0, Pc);
         const size_t fixed = rka_smem(q, box, 0, Pc);
         int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);
         if (const char* e = getenv("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
@@ -1166,6 +1168,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.use_stop = stop_mode ? 1 : 0;
     args.stages = pl.stages;
     args.box = pl.box;
+    args.cpasync = 0;
     if (pl.tma) KZ_TRY(ensure_tmaps(s, pl.box));
     const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
     args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;

@@ -66,10 +66,13 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int q4 = (q + 3) & ~3;
     const int q1 = q + 1, q1p = (q1 + 1) & ~1;
     const int RPO = (((q + Pc - 1) / Pc) + 1) & ~1;  // workers per owner, even; the error belongs to rank Pc-1
+    const int my_lo = cr * RPO < q ? cr * RPO : q;
+    const int n_own = (my_lo + RPO < q ? my_lo + RPO : q) - my_lo;  // workers this CTA owns
     const int QB = (((q + NW - 1) / NW) + 1) & ~1;  // even: rows pair up into 16-byte pushes
     const int nwv = (q + QB - 1) / QB;  // warps owning at least one worker
     const unsigned rows_bytes = (unsigned)(q4 * cwb * 8);
-    const int stage_bytes = (int)rows_bytes + q4 * 32;  // rows, then 32-byte (b, sq, 1/sq, 0) records
+    const int RPO4 = (RPO + 3) & ~3;
+    const int stage_bytes = (int)rows_bytes + RPO4 * 32;  // rows, then the owned workers' (b, sq, 1/sq, 0)
 
     // shared memory carve (rka_smem() in kz_api.cu must match)
     unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw);  // D <= 8
@@ -112,8 +115,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
 
     if (warp == NW) {
         // ================= producer warp =================
-        const int ng = q4 / 4;
-        const unsigned bytes = rows_bytes + (unsigned)q4 * 32u;
+        const int ng = q4 / 4, nbg = (n_own + 3) / 4;
+        const unsigned bytes = rows_bytes + (unsigned)nbg * 128u;
         const unsigned ring_u = smem_u32(ring);
         int64_t it = 0;
         int s = 0;
@@ -126,20 +129,26 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 if (!ok) break;
             }
             if (*halt) break;
+            const unsigned dst = ring_u + (unsigned)(s * stage_bytes);
+            const int32_t* ix = a.idx + it * q;
             if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
             __syncwarp();
-            const unsigned dst = ring_u + (unsigned)(s * stage_bytes);
             const unsigned fb = smem_u32(&full[s]);
-            const int32_t* ix = a.idx + it * q;
-            for (int op = lane; op < 2 * ng; op += 32) {
-                const int i = op < ng ? op : op - ng;
+            // all q row slices; the (b, sq, 1/sq) records only of the workers this CTA owns
+            // (its owner warps are their only readers): q/4 + RPO/4 gathers per iteration
+            for (int op = lane; op < ng + nbg; op += 32) {
                 int r[4];
+                if (op < ng) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) r[u] = __ldg(ix + (4 * i + u < q ? 4 * i + u : q - 1));
-                if (op < ng)
-                    tma_gather4(dst + (unsigned)(i * 4 * cwb * 8), &tmA, c0, r[0], r[1], r[2], r[3], fb);
-                else
-                    tma_gather4(dst + rows_bytes + (unsigned)(i * 128), &tmB, 0, r[0], r[1], r[2], r[3], fb);
+                    for (int u = 0; u < 4; ++u) r[u] = __ldg(ix + (4 * op + u < q ? 4 * op + u : q - 1));
+                    tma_gather4(dst + (unsigned)(op * 4 * cwb * 8), &tmA, c0, r[0], r[1], r[2], r[3], fb);
+                } else {
+                    const int g = op - ng;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        r[u] = __ldg(ix + my_lo + (4 * g + u < n_own ? 4 * g + u : n_own - 1));
+                    tma_gather4(dst + rows_bytes + (unsigned)(g * 128), &tmB, 0, r[0], r[1], r[2], r[3], fb);
+                }
             }
             if (++s == D) s = 0;
         }
@@ -184,8 +193,6 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
 
     const int wb = warp * QB < q ? warp * QB : q;
     const int we = wb + QB < q ? wb + QB : q;
-    const int my_lo = cr * RPO < q ? cr * RPO : q;
-    const int n_own = (my_lo + RPO < q ? my_lo + RPO : q) - my_lo;  // workers this CTA owns
     const int eown = Pc - 1;                                          // owner of the error total
     const bool gh = we - wb > grp * NR;  // this lane group owns at least one worker
     const bool qpow2 = (q & (q - 1)) == 0;
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                         tot = ll_sum<RKA_MAXG>(ll + 2 * t, 2 * q1, G, tag, &a.status->aborted);
                     }
                     if (live && u == 0) {
-                        const double* rec4 = bsr + 4 * t;  // (b, sq, 1/sq, 0)
+                        const double* rec4 = bsr + 4 * i;  // (b, sq, 1/sq, 0) of owned worker i
                         const double d = __dsub_rn(rec4[0], tot);
                         const double nume = unit_alpha ? d : __dmul_rn(alp[t], d);  // 1 * d == d exactly
                         sout[i] = div_rn_fast(nume, rec4[1], rec4[2]);
