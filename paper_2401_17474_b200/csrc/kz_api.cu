@@ -703,7 +703,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     if (ep == 0 || T > chain_max_threads(ep) || (int64_t)ep * T < pairs)
         return fail(KZ_EINVAL, "n=%lld too large for the chain kernel", (long long)s->n);
     // rows per reduction: as many as registers allow (EP small) and the ring holds (> R rows)
-    int R = ep <= 2 ? 8 : (ep == 4 ? 4 : (ep == 8 ? 2 : 1));
+    int R = ep <= 4 ? 4 : (ep == 8 ? 2 : 1);  // R = 8 measured slower since the reduction got cheap
     if (C == 2) R = std::min(R, 4);
     if (const char* e = getenv("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
     const int64_t ldc = s->ld / C;

@@ -200,14 +200,22 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 stop = lim < win_next ? lim : win_next;
             }
             const int cnt = (int)(stop - issued);
-            // lane l of warp 0 issues row issued + l: arm its stage, then two bulk copies
-            if (warp == 0 && lane < cnt) {
-                int st = iss_stage + lane;
+            // row issued + j goes out from warp j % nw, lane j / nw: the per-row mbarrier and
+            // TMA issue costs (~200 cycles) spread over the warps instead of queueing in warp 0.
+            // Every warp tracks the same `issued`; only warp 0 rewrites the window, and only
+            // slots of rows already issued (see above), so these reads are safe.
+            const int jrow = lane * nw + warp;
+            if (jrow < cnt) {
+                const int lane_j = jrow;
+                int st = iss_stage + lane_j;
                 if (st >= D) st -= D;
-                const int64_t i = sm.win[(issued + lane) & (IDX_WINDOW - 1)];
-                mbar_arrive_expect_tx(&full[st], row_bytes + 16u);
+                const int64_t i = sm.win[(issued + lane_j) & (IDX_WINDOW - 1)];
+                // the (b, sq) pair by a 16-byte cp.async tracked on the same mbarrier: one TMA op
+                // per row instead of two (a bulk op costs ~60-110 cycles of TMA issue)
+                cp_async16(sm.bsq + st, bs2 + 2 * i);
+                cp_async_mbar_arrive(&full[st]);
+                mbar_arrive_expect_tx(&full[st], row_bytes);
                 bulk_g2s(sm.ring + (size_t)st * ldc, a.A + i * ld + cb, row_bytes, &full[st]);
-                bulk_g2s(sm.bsq + st, bs2 + 2 * i, 16u, &full[st]);
             }
             issued += cnt;
             iss_stage += cnt;

@@ -423,3 +423,13 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(unsigned long long* b
 }
 
 }  // namespace kz
+
+namespace kz {
+
+// Make a local mbarrier track this thread's prior cp.async copies: the pending
+// arrival count is raised now and dropped when the copies land (no .noinc).
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+}  // namespace kz
