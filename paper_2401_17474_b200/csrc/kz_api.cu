@@ -165,7 +165,8 @@ struct kz_system {
     DevBuf<SolveStatus> status;
     DevBuf<unsigned long long> zero_row;
     DevBuf<long long> dbg;
-    DevBuf<double> cg;  // CGLS work vectors (kz_cgls)
+    DevBuf<double> cg;     // CGLS work vectors (kz_cgls)
+    DevBuf<double> stage;  // dense host-upload staging (one 1-D copy, then a device repack)
     SolveStatus* h_status = nullptr;  // pinned
     bool norms_valid = false;
     bool bs2_valid = false;
@@ -238,8 +239,10 @@ extern "C" int32_t kz_system_create(int32_t device, int64_t m, int64_t n, kz_sys
 extern "C" int32_t kz_system_destroy(kz_system* s) {
     if (!s) return KZ_OK;
     cudaSetDevice(s->device);
-    for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas, &s->bs2})
+    for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas, &s->bs2,
+                    &s->cg, &s->stage})
         b->release();
+    s->dbg.release();
     s->lo.release();
     s->len.release();
     s->idx.release();
@@ -261,10 +264,23 @@ static int upload_common(kz_system* s, const double* A, int64_t lda, const doubl
                          cudaStream_t st, cudaMemcpyKind kind) {
     if (lda < s->n) return fail(KZ_EINVAL, "lda=%lld < n=%lld", (long long)lda, (long long)s->n);
     KZ_CUDA(cudaSetDevice(s->device));
-    KZ_CUDA(cudaMemcpy2DAsync(s->A.p, s->ld * sizeof(double), A, lda * sizeof(double), s->n * sizeof(double), s->m,
-                              kind, st));
-    if (s->ld > s->n)
-        KZ_CUDA(cudaMemset2DAsync(s->A.p + s->n, s->ld * sizeof(double), 0, (s->ld - s->n) * sizeof(double), s->m, st));
+    if (kind == cudaMemcpyHostToDevice && lda == s->n && s->ld > s->n) {
+        // dense host rows: one 1-D copy at full link speed into staging, then a device
+        // repack into the 128-byte row pitch (a pitched 2-D copy of ~4 KB rows runs far
+        // below the link rate)
+        KZ_TRY(s->stage.ensure((size_t)s->m * s->n));
+        KZ_CUDA(cudaMemcpyAsync(s->stage.p, A, (size_t)s->m * s->n * sizeof(double), kind, st));
+        const int64_t total = s->m * s->ld;
+        repack_rows_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)s->sms * 32), 256, 0, st>>>(
+            s->stage.p, s->m, s->n, s->ld, s->A.p);
+        KZ_TRY(check_launch("repack_rows_kernel"));
+    } else {
+        KZ_CUDA(cudaMemcpy2DAsync(s->A.p, s->ld * sizeof(double), A, lda * sizeof(double), s->n * sizeof(double),
+                                  s->m, kind, st));
+        if (s->ld > s->n)
+            KZ_CUDA(cudaMemset2DAsync(s->A.p + s->n, s->ld * sizeof(double), 0, (s->ld - s->n) * sizeof(double), s->m,
+                                      st));
+    }
     KZ_CUDA(cudaMemcpyAsync(s->b.p, b, s->m * sizeof(double), kind, st));
     if (xref) {
         KZ_CUDA(cudaMemcpyAsync(s->xref.p, xref, s->n * sizeof(double), kind, st));

@@ -84,6 +84,8 @@ __global__ void cg_update_xr_kernel(double* __restrict__ x, const double* __rest
                                     int64_t m);
 __global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restrict__ s,
                                    const double* __restrict__ scal, int64_t n);
+__global__ void repack_rows_kernel(const double* __restrict__ src, int64_t m, int64_t n, int64_t ld,
+                                   double* __restrict__ dst);
 constexpr int CDF_SCAN_THREADS = 256;
 __global__ void cdf_scan_kernel(const double* __restrict__ sq, const int64_t* __restrict__ lo,
                                 const int64_t* __restrict__ len, int64_t nranges, double* __restrict__ cdf);

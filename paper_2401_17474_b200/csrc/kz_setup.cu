@@ -275,4 +275,14 @@ __global__ void cyclic_rows_kernel(int32_t* __restrict__ idx, int64_t k0, int64_
         idx[j] = (int32_t)((k0 + j) % m);
 }
 
+// Dense rows (pitch n) -> pitched rows (pitch ld, zero padding).
+__global__ void repack_rows_kernel(const double* __restrict__ src, int64_t m, int64_t n, int64_t ld,
+                                   double* __restrict__ dst) {
+    const int64_t total = m * ld;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / ld, j = e - i * ld;
+        dst[e] = j < n ? src[i * n + j] : 0.0;
+    }
+}
+
 }  // namespace kz
