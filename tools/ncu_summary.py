@@ -12,6 +12,13 @@ METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "dram read"),
     ("dram__bytes_write.sum", "dram write"),
+    ("dram__bytes.sum.per_second", "dram bytes/s"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("LTS.TriageCompute.lts__average_t_sector_hit_rate_realtime.pct", "L2 hit rate %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
+    ("SM_B.TriageCompute.l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank confl."),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
