@@ -41,7 +41,8 @@ enum kz_status {
     KZ_ENOMEM = 4,      /* device allocation failed                                                  */
     KZ_ECUDA = 5,       /* CUDA runtime / launch error                                               */
     KZ_ENODEV = 6,      /* no CUDA device                                                            */
-    KZ_ENOCONV = 7      /* ConvergenceError (cgls.py:71-75): iterate returned, tolerance not met     */
+    KZ_ENOCONV = 7,     /* ConvergenceError (cgls.py:71-75): iterate returned, tolerance not met     */
+    KZ_ESPECTRAL = 8    /* SpectralConvergenceError (spectral.py:84-112)                             */
 };
 
 enum kz_variant { KZ_RK = 0, KZ_RKA = 1, KZ_RKAB = 2, KZ_CK = 3 };          /* solvers.py:55 VARIANTS        */
@@ -189,6 +190,14 @@ KZ_API int32_t kz_norms(kz_system* sys, const double* x_host, double* residual, 
  * iterate, like ConvergenceError.best_x). */
 KZ_API int32_t kz_cgls(kz_system* sys, const double* b_host, double tol, int64_t max_it, double* x_out,
                        int64_t* iterations, void* stream);
+
+/* Extreme eigenvalues of A_blk^T A_blk for the row block [row_lo, row_hi]
+ * (replaces spectral.py:66-121 `spectral_stats`): out[0] = sigma_max^2 by power
+ * iteration, out[1] = sigma_min^2 by inverse iteration with a matrix-free CG
+ * inner solve; v0/v1 are the normalised start vectors (n each).  KZ_ESPECTRAL
+ * maps to SpectralConvergenceError. */
+KZ_API int32_t kz_spectral(kz_system* sys, int64_t row_lo, int64_t row_hi, const double* v0_host,
+                           const double* v1_host, double tol, int64_t max_it, double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,7 @@ from .errors import DegenerateRowError, DimensionMismatchError, EmptyRangeError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkz_b200.so")
 
-KZ_OK, KZ_EINVAL, KZ_EDEGENERATE, KZ_EEMPTYRANGE, KZ_ENOMEM, KZ_ECUDA, KZ_ENODEV, KZ_ENOCONV = range(8)
+KZ_OK, KZ_EINVAL, KZ_EDEGENERATE, KZ_EEMPTYRANGE, KZ_ENOMEM, KZ_ECUDA, KZ_ENODEV, KZ_ENOCONV, KZ_ESPECTRAL = range(9)
 KERNELS = {"auto": 0, "chain": 1, "sync_cluster": 2, "sync_grid": 3}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 VARIANT_IDS = {"rk": 0, "rka": 1, "rkab": 2, "ck": 3}
@@ -32,7 +32,7 @@ EXPORTS = (
     "kz_generate_counter", "kz_system_download",
     "kz_row_norms", "kz_sampler_build", "kz_sampler_set_ranges", "kz_dump_rows", "kz_solve",
     "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
-    "kz_cgls",
+    "kz_cgls", "kz_spectral",
 )
 
 

@@ -1493,3 +1493,139 @@ extern "C" int32_t kz_cgls(kz_system* s, const double* b_host, double tol, int64
     return KZ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Extreme singular values of the row block [row_lo, row_hi] (spectral.py:66-121):
+// lambda_max by power iteration on A^T A, lambda_min by inverse iteration with a
+// matrix-free CG inner solve; the start vectors (Prng(0x5EED, 0/1), normalised)
+// come from the host.  out[0] = lambda_max, out[1] = lambda_min.
+// ---------------------------------------------------------------------------
+extern "C" int32_t kz_spectral(kz_system* s, int64_t row_lo, int64_t row_hi, const double* v0_host,
+                               const double* v1_host, double tol, int64_t max_it, double* out, void* stream) {
+    if (!s || !v0_host || !v1_host || !out) return fail(KZ_EINVAL, "null argument");
+    if (row_lo < 0 || row_hi >= s->m || row_hi < row_lo) return fail(KZ_EINVAL, "bad row range");
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    const int64_t m = row_hi - row_lo + 1, n = s->n, ld = s->ld;
+    const double* A = s->A.p + row_lo * ld;
+    const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>((int64_t)s->sms * 4, (m + 255) / 256));
+    const int64_t rpc = (m + nchunks - 1) / nchunks;
+    // v | w | y | r | p | mp (ld each) | t (m) | partial (nchunks x ld) | scalars (8)
+    const size_t need = 6 * (size_t)ld + (size_t)m + (size_t)nchunks * ld + 8;
+    KZ_TRY(s->cg.ensure(need));
+    double* v = s->cg.p;
+    double* w = v + ld;
+    double* y = w + ld;
+    double* r = y + ld;
+    double* p = r + ld;
+    double* mp = p + ld;
+    double* t = mp + ld;
+    double* part = t + m;
+    double* scal = part + (size_t)nchunks * ld;  // [0] rs, [1] denom, [2] rs_new, [3] scratch, [4] norm
+    const unsigned rows_blocks = (unsigned)((m + 7) / 8);
+    const dim3 tgrid((unsigned)((n + 255) / 256), (unsigned)nchunks);
+    const unsigned eblocks = (unsigned)std::min<int64_t>(1024, (n + 255) / 256);
+    auto Av = [&](const double* x, double* out_m) -> int {
+        cg_gemv_n_kernel<<<rows_blocks, 256, 0, st>>>(A, x, nullptr, m, n, ld, 0, out_m);
+        return check_launch("cg_gemv_n_kernel");
+    };
+    auto ATv = [&](const double* vec, double* out_n) -> int {
+        cg_gemv_t_partial_kernel<<<tgrid, 256, 0, st>>>(A, vec, m, n, ld, rpc, part);
+        KZ_TRY(check_launch("cg_gemv_t_partial_kernel"));
+        cg_gemv_t_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nchunks, n, ld, out_n);
+        return check_launch("cg_gemv_t_reduce_kernel");
+    };
+    auto dot = [&](const double* u, const double* x, int64_t len, int slot, double* host) -> int {
+        cg_dot_kernel<<<1, 1024, 0, st>>>(u, x, len, scal + slot);
+        KZ_TRY(check_launch("cg_dot_kernel"));
+        if (host) {
+            KZ_CUDA(cudaMemcpyAsync(host, scal + slot, sizeof(double), cudaMemcpyDeviceToHost, st));
+            KZ_CUDA(cudaStreamSynchronize(st));
+        }
+        return KZ_OK;
+    };
+    auto rayleigh = [&](const double* x, double* val) -> int {  // ||A x||^2
+        KZ_TRY(Av(x, t));
+        return dot(t, t, m, 3, val);
+    };
+    // ---- lambda_max: power iteration (spectral.py:75-95)
+    KZ_CUDA(cudaMemcpyAsync(v, v0_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    double lam = 0.0;
+    KZ_TRY(rayleigh(v, &lam));
+    bool ok = false;
+    for (int64_t it = 0; it < max_it; ++it) {
+        KZ_TRY(Av(v, t));
+        KZ_TRY(ATv(t, w));
+        double nw2 = 0.0;
+        KZ_TRY(dot(w, w, n, 4, &nw2));
+        const double nw = std::sqrt(nw2);
+        if (nw == 0.0) return fail(KZ_ESPECTRAL, "sigma_max: power iteration hit a null vector");
+        KZ_CUDA(cudaMemcpyAsync(scal + 4, &nw, sizeof(double), cudaMemcpyHostToDevice, st));
+        cg_scale_div_kernel<<<eblocks, 256, 0, st>>>(w, scal + 4, n, v);
+        KZ_TRY(check_launch("cg_scale_div_kernel"));
+        double lam_new = 0.0;
+        KZ_TRY(rayleigh(v, &lam_new));
+        const bool done = std::fabs(lam_new - lam) <= tol * lam_new;
+        lam = lam_new;
+        if (done) {
+            ok = true;
+            break;
+        }
+    }
+    if (!ok) return fail(KZ_ESPECTRAL, "sigma_max: power iteration did not converge");
+    out[0] = lam;
+    // ---- lambda_min: inverse iteration, CG on A^T A y = v (spectral.py:97-115, 36-57)
+    KZ_CUDA(cudaMemcpyAsync(v, v1_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    double theta = 0.0;
+    KZ_TRY(rayleigh(v, &theta));
+    const int64_t cg_max = 20 * n + 200;
+    ok = false;
+    for (int64_t it = 0; it < max_it; ++it) {
+        // y = 0, r = v, p = v, rs = <r, r>, stop = (tol ||v||)^2
+        KZ_CUDA(cudaMemsetAsync(y, 0, ld * sizeof(double), st));
+        KZ_CUDA(cudaMemcpyAsync(r, v, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        KZ_CUDA(cudaMemcpyAsync(p, v, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        double rs = 0.0;
+        KZ_TRY(dot(r, r, n, 0, &rs));
+        const double stop = (tol * std::sqrt(rs)) * (tol * std::sqrt(rs));
+        bool cg_ok = false;
+        for (int64_t k = 0; k < cg_max; ++k) {
+            if (rs <= stop) {
+                cg_ok = true;
+                break;
+            }
+            KZ_TRY(Av(p, t));
+            KZ_TRY(ATv(t, mp));
+            double den = 0.0;
+            KZ_TRY(dot(p, mp, n, 1, &den));
+            if (den <= 0.0) break;
+            cg_update_xr_kernel<<<eblocks, 256, 0, st>>>(y, p, r, mp, scal, n, n);  // alpha = rs / den
+            KZ_TRY(check_launch("cg_update_xr_kernel"));
+            double rs_new = 0.0;
+            KZ_TRY(dot(r, r, n, 2, &rs_new));
+            cg_update_p_kernel<<<eblocks, 256, 0, st>>>(p, r, scal, n);  // p = r + (rs_new / rs) p
+            KZ_TRY(check_launch("cg_update_p_kernel"));
+            KZ_CUDA(cudaMemcpyAsync(scal, scal + 2, sizeof(double), cudaMemcpyDeviceToDevice, st));
+            rs = rs_new;
+        }
+        if (!cg_ok && !(rs <= stop)) return fail(KZ_ESPECTRAL, "sigma_min: inner CG solve failed");
+        double ny2 = 0.0;
+        KZ_TRY(dot(y, y, n, 4, &ny2));
+        const double ny = std::sqrt(ny2);
+        if (ny == 0.0) return fail(KZ_ESPECTRAL, "sigma_min: inverse iteration collapsed");
+        KZ_CUDA(cudaMemcpyAsync(scal + 4, &ny, sizeof(double), cudaMemcpyHostToDevice, st));
+        cg_scale_div_kernel<<<eblocks, 256, 0, st>>>(y, scal + 4, n, v);
+        KZ_TRY(check_launch("cg_scale_div_kernel"));
+        double theta_new = 0.0;
+        KZ_TRY(rayleigh(v, &theta_new));
+        const bool done = it >= 2 && std::fabs(theta_new - theta) <= tol * theta_new;
+        theta = theta_new;
+        if (done) {
+            ok = true;
+            break;
+        }
+    }
+    if (!ok) return fail(KZ_ESPECTRAL, "sigma_min: inverse iteration did not converge");
+    out[1] = theta;
+    return KZ_OK;
+}
+

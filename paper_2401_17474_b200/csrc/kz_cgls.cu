@@ -80,6 +80,14 @@ __global__ void cg_update_xr_kernel(double* __restrict__ x, const double* __rest
     }
 }
 
+// v = w / nw  (numpy `w / nw`: correctly rounded division per element)
+__global__ void cg_scale_div_kernel(const double* __restrict__ w, const double* __restrict__ nw, int64_t n,
+                                    double* __restrict__ v) {
+    const double d = *nw;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        v[j] = __ddiv_rn(w[j], d);
+}
+
 // p = s + (gamma_new / gamma) p
 __global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restrict__ s,
                                    const double* __restrict__ scal, int64_t n) {

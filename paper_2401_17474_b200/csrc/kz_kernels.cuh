@@ -84,6 +84,8 @@ __global__ void cg_update_xr_kernel(double* __restrict__ x, const double* __rest
                                     int64_t m);
 __global__ void cg_update_p_kernel(double* __restrict__ p, const double* __restrict__ s,
                                    const double* __restrict__ scal, int64_t n);
+__global__ void cg_scale_div_kernel(const double* __restrict__ w, const double* __restrict__ nw, int64_t n,
+                                    double* __restrict__ v);
 __global__ void repack_rows_kernel(const double* __restrict__ src, int64_t m, int64_t n, int64_t ld,
                                    double* __restrict__ dst);
 constexpr int CDF_SCAN_THREADS = 256;

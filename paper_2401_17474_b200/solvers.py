@@ -23,7 +23,7 @@ import numpy as np
 from . import _native as N
 from .errors import DimensionMismatchError
 from .reports import RunReport, TraceRecord
-from .sysgen import LinearSystem, cgls_solve
+from .sysgen import LinearSystem, cgls_solve, partition_bounds
 
 VARIANTS = ("ck", "rk", "rka", "rkab", "cgls")
 ALPHA_POLICIES = ("unit", "fixed", "optimal_full", "optimal_partial")
@@ -271,6 +271,27 @@ class DeviceSystem:
         self.cgls_iterations = int(its.value)
         return x
 
+    def spectral(self, row_lo: int = 0, row_hi: int | None = None, tol: float = 1e-6, max_it: int = 5000):
+        """(lambda_max, lambda_min) of A_blk^T A_blk for rows [row_lo, row_hi] on the device
+        (spectral.py:66-121; start vectors Prng(0x5EED, 0/1) normalised on the host)."""
+        from .errors import SpectralConvergenceError
+        from .spectral import _START_SEED
+        from .sysgen import Prng
+
+        row_hi = self.m - 1 if row_hi is None else row_hi
+        v0 = Prng(_START_SEED, 0).standard_normal(self.n)
+        v0 /= np.linalg.norm(v0)
+        v1 = Prng(_START_SEED, 1).standard_normal(self.n)
+        v1 /= np.linalg.norm(v1)
+        out = np.empty(2)
+        rc = self._lib.kz_spectral(self.handle, C.c_int64(row_lo), C.c_int64(row_hi), N.ptr(v0), N.ptr(v1),
+                                   C.c_double(tol), C.c_int64(max_it), N.ptr(out), None)
+        if rc == N.KZ_ESPECTRAL:
+            msg = self._lib.kz_last_error().decode(errors="replace")
+            raise SpectralConvergenceError(msg.split(":")[0], msg)
+        N.check(rc)
+        return float(out[0]), float(out[1])
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             self._lib.kz_system_destroy(self.handle)
@@ -328,13 +349,37 @@ def release_pool() -> None:
 
 
 def resolve_alphas(system, cfg: SolverConfig, q: int | None = None) -> np.ndarray:
-    """Per-worker weights (solvers.py:148-159)."""
+    """Per-worker weights (solvers.py:148-159).  On a DeviceSystem the optimal_* policies
+    run their spectral estimates (spectral.py:66-156) on the device (kz_spectral)."""
     q = cfg.q if q is None else q
     if cfg.alpha_policy == "unit":
         return np.ones(q)
     if cfg.alpha_policy == "fixed":
         return np.full(q, float(cfg.alpha))
-    from .spectral import optimal_alpha, partial_alphas, spectral_stats  # host setup, off the hot path
+    from .spectral import SpectralStats, optimal_alpha, partial_alphas, spectral_stats  # setup, off the hot path
+
+    if isinstance(system, DeviceSystem):
+        sq = system.row_norms()
+
+        def stats(lo, hi):
+            lmax, lmin = system.spectral(lo, hi)
+            fro = float(sq[lo:hi + 1].sum())  # RowNormCache.frobenius_sq (linalg.py:88)
+            return SpectralStats(sigma_max=float(np.sqrt(lmax)), sigma_min=float(np.sqrt(lmin)),
+                                 s_min=lmin / fro, s_max=lmax / fro)
+
+        m, n = system.m, system.n
+        if cfg.alpha_policy == "optimal_full":
+            return np.full(q, optimal_alpha(stats(0, m - 1), q))
+        if q > m:
+            raise ValueError(f"q={q} exceeds row count m={m}")
+        out = np.empty(q)
+        for t in range(q):
+            lo, hi = partition_bounds(m, q, t)
+            if hi - lo + 1 < n:
+                raise DimensionMismatchError(f"worker {t} block has {hi - lo + 1} rows < {n} columns; "
+                                             f"its spectral estimate would be rank deficient")
+            out[t] = optimal_alpha(stats(lo, hi), q)
+        return out
     A = _host_matrix(system)
     if cfg.alpha_policy == "optimal_full":
         return np.full(q, optimal_alpha(spectral_stats(A), q))
@@ -357,7 +402,6 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
     cfg.validate()
     q = 1 if variant in ("rk", "ck") else cfg.q
     steps = cfg.block_size + (1 if lead_row else 0) if variant == "rkab" else 1
-    alphas = N.f64(resolve_alphas(system, cfg, q))
     if budget is not None and budget < 1:
         raise ValueError(f"fixed iteration budget must be >= 1, got {budget}")
     if budget is None and trace_step is not None and trace_step < 1:
@@ -366,6 +410,7 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
     own = not isinstance(system, DeviceSystem)
     ds = _pool_acquire(system, cfg.device) if own else system
     try:
+        alphas = N.f64(resolve_alphas(ds, cfg, q))  # optimal_* policies: spectral estimates on the device
         if x_ref is not None:
             ds.set_x_ref(x_ref)
         elif budget is None and not ds._xref_set:
