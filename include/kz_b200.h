@@ -42,7 +42,9 @@ enum kz_status {
     KZ_ECUDA = 5,       /* CUDA runtime / launch error                                               */
     KZ_ENODEV = 6,      /* no CUDA device                                                            */
     KZ_ENOCONV = 7,     /* ConvergenceError (cgls.py:71-75): iterate returned, tolerance not met     */
-    KZ_ESPECTRAL = 8    /* SpectralConvergenceError (spectral.py:84-112)                             */
+    KZ_ESPECTRAL = 8,   /* SpectralConvergenceError (spectral.py:84-112)                             */
+    KZ_EFORMAT = 9,     /* SystemFormatError (sysgen.py:226-246): bad magic, dimensions, truncation  */
+    KZ_EVERSION = 10    /* UnsupportedVersionError (sysgen.py:240-244)                               */
 };
 
 enum kz_variant { KZ_RK = 0, KZ_RKA = 1, KZ_RKAB = 2, KZ_CK = 3 };          /* solvers.py:55 VARIANTS        */
@@ -196,6 +198,14 @@ KZ_API int32_t kz_cgls(kz_system* sys, const double* b_host, double tol, int64_t
  * iteration, out[1] = sigma_min^2 by inverse iteration with a matrix-free CG
  * inner solve; v0/v1 are the normalised start vectors (n each).  KZ_ESPECTRAL
  * maps to SpectralConvergenceError. */
+/* Load a KZSYS v1 system file (sysgen.py:190-271) straight into device memory:
+ * rows [row_lo, row_hi] (row_hi < 0: all; a GPU's shard), b of those rows and
+ * x_ref (x_star if present, else x_ls).  Reports the file's full m, n, flags and
+ * generator metadata (seed, mu_lo, mu_hi, sigma_lo, sigma_hi; seed -1 if none). */
+KZ_API int32_t kz_system_load_file(int32_t device, const char* path, int64_t row_lo, int64_t row_hi,
+                                   kz_system** out, int64_t* m_total, int64_t* n_out, uint32_t* flags_out,
+                                   double* meta5);
+
 KZ_API int32_t kz_spectral(kz_system* sys, int64_t row_lo, int64_t row_hi, const double* v0_host,
                            const double* v1_host, double tol, int64_t max_it, double* out, void* stream);
 

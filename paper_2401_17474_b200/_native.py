@@ -18,7 +18,8 @@ from .errors import DegenerateRowError, DimensionMismatchError, EmptyRangeError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkz_b200.so")
 
-KZ_OK, KZ_EINVAL, KZ_EDEGENERATE, KZ_EEMPTYRANGE, KZ_ENOMEM, KZ_ECUDA, KZ_ENODEV, KZ_ENOCONV, KZ_ESPECTRAL = range(9)
+KZ_OK, KZ_EINVAL, KZ_EDEGENERATE, KZ_EEMPTYRANGE, KZ_ENOMEM, KZ_ECUDA, KZ_ENODEV, KZ_ENOCONV, KZ_ESPECTRAL, \
+    KZ_EFORMAT, KZ_EVERSION = range(11)
 KERNELS = {"auto": 0, "chain": 1, "sync_cluster": 2, "sync_grid": 3}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 VARIANT_IDS = {"rk": 0, "rka": 1, "rkab": 2, "ck": 3}
@@ -32,7 +33,7 @@ EXPORTS = (
     "kz_generate_counter", "kz_system_download",
     "kz_row_norms", "kz_sampler_build", "kz_sampler_set_ranges", "kz_dump_rows", "kz_solve",
     "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
-    "kz_cgls", "kz_spectral",
+    "kz_cgls", "kz_spectral", "kz_system_load_file",
 )
 
 
@@ -168,9 +169,21 @@ def check(rc: int, bad_row: int | None = None) -> None:
         raise ValueError(msg)
     if rc == KZ_ENODEV:
         raise NativeUnavailable(msg)
+    if rc in (KZ_EFORMAT, KZ_EVERSION):
+        from .errors import SystemFormatError, UnsupportedVersionError
+
+        off = _parse_offset(msg)
+        raise (UnsupportedVersionError if rc == KZ_EVERSION else SystemFormatError)(msg.split(" (offset")[0], off)
     if rc == KZ_ENOMEM:
         raise MemoryError(msg)
     raise NativeError(msg)
+
+
+def _parse_offset(msg: str) -> int:
+    try:
+        return int(msg.split("(offset ")[1].split(")")[0])
+    except (IndexError, ValueError):
+        return -1
 
 
 def _parse_row(msg: str) -> int:

@@ -18,6 +18,9 @@
 #include <string>
 #include <vector>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include "../../include/kz_b200.h"
 #include "kz_kernels.cuh"
 
@@ -1626,6 +1629,146 @@ extern "C" int32_t kz_spectral(kz_system* s, int64_t row_lo, int64_t row_hi, con
     }
     if (!ok) return fail(KZ_ESPECTRAL, "sigma_min: inverse iteration did not converge");
     out[1] = theta;
+    return KZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// KZSYS v1 system files (sysgen.py:190-271 save_system / load_system), read
+// straight into device memory.  Layout: "KZSYS", u8 version = 1, u64 m, u64 n,
+// u32 flags (1 consistent, 2 x_star, 4 x_ls, 8 generator metadata), [u64 seed,
+// f64 mu_lo, mu_hi, sigma_lo, sigma_hi], A (m x n f64 LE, row-major), b (m),
+// [x_star (n)], [x_ls (n)].  Rows [row_lo, row_hi] (a GPU's shard) stream from
+// the file through two pinned buffers: pread of chunk c+1 overlaps the H2D copy
+// and the device repack of chunk c into the 128-byte row pitch.
+// ---------------------------------------------------------------------------
+extern "C" int32_t kz_system_load_file(int32_t device, const char* path, int64_t row_lo, int64_t row_hi,
+                                       kz_system** out, int64_t* m_total, int64_t* n_out, uint32_t* flags_out,
+                                       double* meta5) {
+    if (!path || !out) return fail(KZ_EINVAL, "null argument");
+    *out = nullptr;
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) return fail(KZ_EINVAL, "cannot open %s", path);
+    struct Closer {
+        int fd;
+        ~Closer() { close(fd); }
+    } closer{fd};
+    auto read_at = [&](void* dst, size_t bytes, off_t off) -> bool {
+        size_t got = 0;
+        while (got < bytes) {
+            const ssize_t r = pread(fd, (char*)dst + got, bytes - got, off + (off_t)got);
+            if (r <= 0) return false;
+            got += (size_t)r;
+        }
+        return true;
+    };
+    unsigned char head[26];
+    if (!read_at(head, 5, 0)) return fail(KZ_EFORMAT, "truncated file while reading magic (offset 0)");
+    if (memcmp(head, "KZSYS", 5) != 0) return fail(KZ_EFORMAT, "bad magic (offset 0)");
+    if (!read_at(head + 5, 1, 5)) return fail(KZ_EFORMAT, "truncated file while reading version (offset 5)");
+    if (head[5] != 1) return fail(KZ_EVERSION, "unsupported system file version %d (expected 1) (offset 5)", head[5]);
+    if (!read_at(head + 6, 20, 6)) return fail(KZ_EFORMAT, "truncated file while reading header (offset 6)");
+    uint64_t m, n;
+    uint32_t flags;
+    memcpy(&m, head + 6, 8);
+    memcpy(&n, head + 14, 8);
+    memcpy(&flags, head + 22, 4);
+    if (m < 1 || n < 1) return fail(KZ_EFORMAT, "bad dimensions %llux%llu (offset 6)", (unsigned long long)m,
+                                    (unsigned long long)n);
+    off_t off = 26;
+    double meta[5] = {-1.0, -5.0, 5.0, 1.0, 20.0};
+    if (flags & 8u) {
+        unsigned char g[40];
+        if (!read_at(g, 40, off)) return fail(KZ_EFORMAT, "truncated file while reading generator metadata (offset %lld)",
+                                              (long long)off);
+        uint64_t seed;
+        memcpy(&seed, g, 8);
+        meta[0] = (double)seed;
+        memcpy(meta + 1, g + 8, 32);
+        off += 40;
+    }
+    if (row_hi < 0) row_hi = (int64_t)m - 1;
+    if (row_lo < 0 || row_lo > row_hi || row_hi >= (int64_t)m) return fail(KZ_EINVAL, "bad row range");
+    const int64_t rows = row_hi - row_lo + 1;
+    const off_t a_off = off, b_off = a_off + (off_t)(m * n * 8), xs_off = b_off + (off_t)(m * 8);
+    const off_t xl_off = xs_off + ((flags & 2u) ? (off_t)(n * 8) : 0);
+    const off_t end = xl_off + ((flags & 4u) ? (off_t)(n * 8) : 0);
+    if (lseek(fd, 0, SEEK_END) < end) return fail(KZ_EFORMAT, "truncated file (needs %lld bytes)", (long long)end);
+    kz_system* s = nullptr;
+    KZ_TRY(kz_system_create(device, rows, (int64_t)n, &s));
+    struct Guard {
+        kz_system*& s;
+        bool keep = false;
+        ~Guard() {
+            if (!keep && s) kz_system_destroy(s);
+        }
+    } guard{s};
+    cudaStream_t st = nullptr;
+    // chunked rows: <= 64 MiB per chunk
+    const int64_t chunk_rows = std::max<int64_t>(1, std::min<int64_t>(rows, ((int64_t)64 << 20) / (int64_t)(n * 8)));
+    double* pin[2] = {nullptr, nullptr};
+    for (auto& p : pin)
+        if (cudaMallocHost(&p, (size_t)chunk_rows * n * 8) != cudaSuccess) {
+            cudaGetLastError();
+            for (auto& q : pin)
+                if (q) cudaFreeHost(q);
+            return fail(KZ_ENOMEM, "pinned staging allocation failed");
+        }
+    struct PinFree {
+        double** p;
+        ~PinFree() {
+            for (int i = 0; i < 2; ++i)
+                if (p[i]) cudaFreeHost(p[i]);
+        }
+    } pinfree{pin};
+    KZ_TRY(s->stage.ensure((size_t)2 * chunk_rows * n));
+    cudaEvent_t done[2];
+    cudaEventCreate(&done[0]);
+    cudaEventCreate(&done[1]);
+    int rc = KZ_OK;
+    int64_t c = 0;
+    for (int64_t r0 = 0; r0 < rows && rc == KZ_OK; r0 += chunk_rows, ++c) {
+        const int64_t nr = std::min<int64_t>(chunk_rows, rows - r0);
+        const int k = (int)(c & 1);
+        cudaEventSynchronize(done[k]);  // the copy out of this pinned buffer two chunks ago is done
+        if (!read_at(pin[k], (size_t)nr * n * 8, a_off + (off_t)((row_lo + r0) * (int64_t)n * 8))) {
+            rc = fail(KZ_EFORMAT, "truncated file while reading matrix rows");
+            break;
+        }
+        double* dst = s->stage.p + (size_t)k * chunk_rows * n;
+        if (cudaMemcpyAsync(dst, pin[k], (size_t)nr * n * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            rc = fail(KZ_ECUDA, "H2D copy failed");
+            break;
+        }
+        const int64_t total = nr * s->ld;
+        repack_rows_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)s->sms * 32), 256, 0, st>>>(
+            dst, nr, (int64_t)n, s->ld, s->A.p + r0 * s->ld);
+        cudaEventRecord(done[k], st);
+    }
+    cudaStreamSynchronize(st);
+    cudaEventDestroy(done[0]);
+    cudaEventDestroy(done[1]);
+    KZ_TRY(rc);
+    KZ_TRY(check_launch("repack_rows_kernel"));
+    std::vector<double> hb((size_t)rows), hx((size_t)n);
+    if (!read_at(hb.data(), (size_t)rows * 8, b_off + (off_t)(row_lo * 8)))
+        return fail(KZ_EFORMAT, "truncated file while reading constants");
+    KZ_CUDA(cudaMemcpy(s->b.p, hb.data(), (size_t)rows * 8, cudaMemcpyHostToDevice));
+    s->has_xref = false;
+    if (flags & 6u) {  // x_ref: x_star if present, else x_ls (LinearSystem.x_ref)
+        if (!read_at(hx.data(), (size_t)n * 8, (flags & 2u) ? xs_off : xl_off))
+            return fail(KZ_EFORMAT, "truncated file while reading the solution vector");
+        KZ_CUDA(cudaMemcpy(s->xref.p, hx.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+        s->has_xref = true;
+    }
+    s->norms_valid = false;
+    s->bs2_valid = false;
+    s->sampler_scheme = -1;
+    if (m_total) *m_total = (int64_t)m;
+    if (n_out) *n_out = (int64_t)n;
+    if (flags_out) *flags_out = flags;
+    if (meta5) memcpy(meta5, meta, sizeof(meta));
+    guard.keep = true;
+    *out = s;
     return KZ_OK;
 }
 

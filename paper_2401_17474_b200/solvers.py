@@ -105,6 +105,28 @@ class DeviceSystem:
             xr = system.x_star if system.x_star is not None else system.x_ls
             self.upload(system.A, system.b, xr)
 
+    @classmethod
+    def from_file(cls, path, *, device: int = 0, rows: tuple[int, int] | None = None) -> "DeviceSystem":
+        """A KZSYS v1 file (sysgen.py:190-271) loaded straight into HBM (kz_system_load_file);
+        `rows` = (lo, hi) inclusive loads one row shard.  The host copy stays on disk."""
+        lib = N.load_library()
+        h = C.c_void_p()
+        m_tot, n, flags = C.c_int64(), C.c_int64(), C.c_uint32()
+        meta = np.empty(5)
+        lo, hi = rows if rows is not None else (0, -1)
+        N.check(lib.kz_system_load_file(int(device), str(path).encode(), C.c_int64(lo), C.c_int64(hi), C.byref(h),
+                                        C.byref(m_tot), C.byref(n), C.byref(flags), N.ptr(meta)))
+        self = cls.__new__(cls)
+        self._lib = lib
+        self.m = (int(hi) if hi >= 0 else int(m_tot.value) - 1) - int(lo) + 1
+        self.n, self.device = int(n.value), int(device)
+        self.host = None
+        self.handle = h
+        self._xref_set = bool(flags.value & 6)
+        self.file_m, self.file_flags = int(m_tot.value), int(flags.value)
+        self.file_meta = meta
+        return self
+
     # -- residency -------------------------------------------------------------
     def upload(self, A, b, x_ref=None, stream=None) -> None:
         A = N.f64(A)

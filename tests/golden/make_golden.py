@@ -200,9 +200,18 @@ def gen_ck():
     save("ck.npz", **out)
 
 
+def gen_kzsys():
+    """A KZSYS v1 file written by the reference's own save_system (sysgen.py:190-214)."""
+    kb.save_system(system(500, 20, 1), os.path.join(OUT, "kzsys_s500.bin"))
+    print("wrote kzsys_s500.bin")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "ck":
         gen_ck()
+    elif len(sys.argv) > 1 and sys.argv[1] == "kzsys":
+        gen_kzsys()
     else:
         main()
         gen_ck()
+        gen_kzsys()

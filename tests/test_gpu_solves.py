@@ -325,3 +325,33 @@ def test_device_spectral_matches_host(gpu, systems):
     o = O.solve(s.A, s.b, s.x_star, variant="rka", q=8, base_seed=3, alphas=alphas, max_iterations=20000)
     assert r.iterations == o["iterations"]
     assert rel_err(r.x, o["x"]) <= PARITY_TOL
+
+
+def test_kzsys_file_straight_to_device(gpu, systems, tmp_path):
+    """kz_system_load_file: the reference's own KZSYS file and a row shard of a larger one
+    land in HBM equal to the uploaded arrays; solves from them match the golden run."""
+    import os
+
+    from paper_2401_17474_b200 import DeviceSystem, run_solver, sysgen as G
+    from paper_2401_17474_b200.errors import SystemFormatError
+
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    with DeviceSystem.from_file(os.path.join(gdir, "kzsys_s500.bin")) as ds:
+        assert (ds.m, ds.n) == (500, 20) and ds.file_flags & 2
+        A, b, xr = ds.download()
+        s = systems["s500"]
+        assert np.array_equal(A, s.A) and np.array_equal(b, s.b) and np.array_equal(xr, s.x_star)
+        g = golden("solves.npz")
+        r = run_solver(ds, _cfg(variant="rk", base_seed=5))
+        assert r.iterations == int(g["s500_rk_s5_iterations"])
+        assert rel_err(r.x, g["s500_rk_s5_x"]) <= PARITY_TOL
+    big = G.generate_mother(G.GeneratorConfig(m_max=5000, n_max=300, seed=2))
+    p = tmp_path / "big.kzsys"
+    G.save_system(big, p)
+    with DeviceSystem.from_file(p, rows=(1200, 3999)) as ds:
+        A, b, xr = ds.download()
+        assert np.array_equal(A, big.A[1200:4000]) and np.array_equal(b, big.b[1200:4000])
+        assert ds.file_m == 5000
+    p.write_bytes(open(p, "rb").read()[:-100])
+    with pytest.raises(SystemFormatError):
+        DeviceSystem.from_file(p)

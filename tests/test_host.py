@@ -108,3 +108,38 @@ def test_spectral_alpha_formula():
     st = spectral_stats(np.diag([1.0, 2.0, 3.0]))
     assert abs(st.s_max - 9 / 14) <= 1e-5 and abs(st.s_min - 1 / 14) <= 1e-5
     assert math.isfinite(st.sigma_min)
+
+
+def test_kzsys_round_trip_and_reference_files(tmp_path):
+    """save_system / load_system restate sysgen.py:190-271; files written by the
+    reference (golden/kzsys_*.bin) load bit-identically, and damage raises the
+    reference's errors with offsets."""
+    import os
+
+    from paper_2401_17474_b200 import sysgen as G
+    from paper_2401_17474_b200.errors import SystemFormatError, UnsupportedVersionError
+
+    s = G.generate_mother(G.GeneratorConfig(m_max=300, n_max=20, seed=4))
+    p = tmp_path / "s.kzsys"
+    G.save_system(s, p)
+    r = G.load_system(p)
+    assert np.array_equal(r.A, s.A) and np.array_equal(r.b, s.b) and np.array_equal(r.x_star, s.x_star)
+    assert r.seed == s.seed and r.consistent == s.consistent
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    ref = G.load_system(os.path.join(gdir, "kzsys_s500.bin"))
+    mine = G.generate_mother(G.GeneratorConfig(m_max=500, n_max=20, seed=1))
+    assert np.array_equal(ref.A, mine.A) and np.array_equal(ref.x_star, mine.x_star)
+    assert open(os.path.join(gdir, "kzsys_s500.bin"), "rb").read() == (G.save_system(mine, tmp_path / "m"), open(tmp_path / "m", "rb").read())[1]
+    data = bytearray(open(p, "rb").read())
+    bad = tmp_path / "bad"
+    bad.write_bytes(b"XXSYS" + bytes(data[5:]))
+    with pytest.raises(SystemFormatError) as e:
+        G.load_system(bad)
+    assert e.value.offset == 0
+    data[5] = 2
+    bad.write_bytes(bytes(data))
+    with pytest.raises(UnsupportedVersionError):
+        G.load_system(bad)
+    bad.write_bytes(open(p, "rb").read()[:-8])
+    with pytest.raises(SystemFormatError):
+        G.load_system(bad)
