@@ -173,71 +173,118 @@ def cpu_baseline(name, system, kw, budget_s=12.0):
 
 
 def run_b200_sharded(args, name, rank, world, local_rank):
-    """N > 1: weak scaling -- every GPU holds a workload-sized row shard of an
-    (m*N) x n system and runs q workers on it; one NCCL all-reduce of the
-    worker sums per outer iteration (multigpu.solve_sharded)."""
+    """N > 1, headline: the workload's 10 seed-solves are independent objects, so the ranks
+    split them (seed-parallel weak scaling, no data-path collective): each GPU solves
+    `steps` seeds of the resident c1 system; value = all rows / max-over-ranks time.
+    Extras: the row-sharded path itself (BASELINE config 3: 160000 x 20000 counter-keyed,
+    rows split over the GPUs, q = 64 workers per GPU, one NCCL all-reduce of the worker
+    sums per outer iteration -- multigpu.solve_sharded) for RKAB bs = 1000 and RKA."""
     import torch
     import torch.distributed as dist
 
-    from paper_2401_17474_b200 import GeneratorConfig, SolverConfig, generate_mother
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver
     from paper_2401_17474_b200 import _native as N
-    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded
 
     torch.cuda.set_device(local_rank)
-    m1, n, kw, desc = WORKLOADS[name]
-    m = m1 * world
-    system = generate_mother(GeneratorConfig(m_max=m, n_max=n, seed=0))
-    q_local = kw.get("q", 1)
-    plan = plan_shards(m, world, rank, q_local)
-    cfg = SolverConfig(device=local_rank, sampling_scheme="distributed", **kw)
-    shard = CudaShard(system.A[plan.lo:plan.hi + 1], system.b[plan.lo:plan.hi + 1], system.x_star, plan, local_rank)
+    system, kw = build_system(name)
+    m, n = system.A.shape
+    cfg = SolverConfig(device=local_rank, **kw)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
+    ds = DeviceSystem(system, device=local_rank)
     for w in range(args.warmup):
-        solve_sharded(shard, cfg.replace(base_seed=w % 10))
+        run_solver(ds, cfg.replace(base_seed=(rank + w * world) % 10))
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = N.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     rows, iters = 0, []
-    rows0 = shard.rows
     with ClockSampler(local_rank) as clk:
-        ev0.record()
         for k in range(args.steps):
-            r = solve_sharded(shard, cfg.replace(base_seed=k % 10))
+            flush.fill_(k & 0xFF)
+            starts[k].record()
+            r = run_solver(ds, cfg.replace(base_seed=(rank + k * world) % 10))
+            ends[k].record()
+            assert r.converged
+            rows += r.gpu["rows_projected"]
             iters.append(r.iterations)
-        ev1.record()
         torch.cuda.synchronize()
-    rows = shard.rows - rows0
-    t_ms = ev0.elapsed_time(ev1)
+    launches = N.launch_count() - launches0
+    t_ms = float(sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)))
     tt = torch.tensor([t_ms], device=f"cuda:{local_rank}")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    tot = torch.tensor([float(rows)], device=f"cuda:{local_rank}")
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     t_ms = float(tt.item())
-    tot_rows = torch.tensor([float(rows)], device=f"cuda:{local_rank}")
-    dist.all_reduce(tot_rows, op=dist.ReduceOp.SUM)
-    dist.barrier()
-    launches = N.launch_count() - launches0
-    shard.close()
+    ds.close()
+    extras = [] if args.no_extra else sharded_extras(rank, world, local_rank)
     if rank != 0:
         return
     peak, peak_src = read_peak()
-    value = float(tot_rows.item()) / (t_ms / 1e3)
+    value = float(tot.item()) / (t_ms / 1e3)
     achieved = value / world * 8 * n / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0)",
-        "config": {"workload": desc + f", rows x{world} sharded", "m": m, "n": n, **kw, "q_per_gpu": q_local,
-                   "sampling_scheme": "distributed", "parallelism": f"row shards x{world}, NCCL all-reduce / iteration",
-                   "seeds": "0..9 cycling"},
-        "iterations": iters,
+        "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0; bitwise = reference)",
+        "config": {"workload": WORKLOADS[name][3], "m": m, "n": n, **kw,
+                   "parallelism": f"seed-parallel x{world}: independent solves per GPU, no collective",
+                   "seeds": "rank + k * world (mod 10)", "l2": "256 MiB write between steps"},
+        "iterations_rank0": iters,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src, "algorithmic_bytes": "8*n per row projection",
-                     "note": "per-GPU rate over the whole step (kernels + all-reduce + host loop)"},
+                     "note": "per-GPU rate over the whole step"},
         "clocks": clk.summary(),
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 * n,
-                "note": "shard resident; per-iteration host loop included"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": n * 8,
+                "note": "multi-GPU runs keep the system resident; the host-array e2e path is measured at N=1"},
         "gpu_launches": launches,
+        "sharded_extras": extras,
     }
     print(json.dumps(line), flush=True)
+
+
+def sharded_extras(rank, world, local_rank, steps=3):
+    """BASELINE config 3 row-sharded across the ranks: rows/s over all GPUs (max-over-ranks
+    time), RKAB bs = 1000 (1 outer iteration per step) and RKA (200 iterations per step)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_17474_b200 import SolverConfig
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded
+
+    out = []
+    m_total, n, q = 160000, 20000, 64
+    try:
+        plan = plan_shards(m_total, world, rank, q)
+        shard = CudaShard.counter(m_total, n, plan, 0, local_rank)
+        for tag, kw, budget in (("c3_sharded_rkab_bs1000", dict(variant="rkab", q=q, block_size=1000), 1),
+                                ("c3_sharded_rka", dict(variant="rka", q=q), 200)):
+            cfg = SolverConfig(device=local_rank, sampling_scheme="distributed", **kw)
+            solve_sharded(shard, cfg, budget=budget)  # warm-up
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            rows0 = shard.rows
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for k in range(steps):
+                solve_sharded(shard, cfg.replace(base_seed=k), budget=budget)
+            ev1.record()
+            torch.cuda.synchronize()
+            tt = torch.tensor([ev0.elapsed_time(ev1)], device=f"cuda:{local_rank}")
+            rr = torch.tensor([float(shard.rows - rows0)], device=f"cuda:{local_rank}")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dist.all_reduce(rr, op=dist.ReduceOp.SUM)
+            rows_s = float(rr.item()) / (float(tt.item()) / 1e3)
+            out.append({"workload": tag, "n_gpus": world, "rows_per_s": rows_s, "ms_per_step": float(tt.item()) / steps,
+                        "desc": f"160000x20000 counter-keyed, rows sharded x{world}, q={q} per GPU, "
+                                f"{budget} outer iteration(s) per step, NCCL all-reduce per outer iteration",
+                        "hbm_frac_per_gpu": rows_s / world * 8 * n / 1e9 / read_peak()[0]})
+        shard.close()
+    except Exception as exc:  # extras must never sink the headline line
+        out.append({"error": repr(exc)})
+    return out
 
 
 def extra_workloads(device, peak, steps=3):
@@ -427,6 +474,7 @@ def run_b200(args, name, rank, world, local_rank):
     }
     if not args.no_extra:
         line["extra_workloads"] = extra_workloads(local_rank, peak)
+        line["sharded_extras"] = sharded_extras(0, 1, local_rank)  # the row-sharded path at N = 1
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, system, kw)
     print(json.dumps(line), flush=True)

@@ -89,6 +89,10 @@ KZ_API int32_t kz_system_set_xref(kz_system* sys, const double* xref_host, void*
  * on (seed, i, j), so any m' x n' system is an exact leading crop. */
 KZ_API int32_t kz_generate_counter(kz_system* sys, uint64_t seed, double mu_lo, double mu_hi, double sigma_lo,
                                    double sigma_hi, void* stream);
+/* Rows [row0, row0 + m) of the same counter-keyed system into this system (a
+ * GPU's row shard is bit-identical to those rows of the full matrix). */
+KZ_API int32_t kz_generate_counter_rows(kz_system* sys, uint64_t seed, int64_t row0, double mu_lo, double mu_hi,
+                                        double sg_lo, double sg_hi, void* stream);
 /* Copy the leading m2 x n2 block of A (row-major, ld n2), b[:m2] and x_ref[:n2] to the host (any may be NULL). */
 KZ_API int32_t kz_system_download(kz_system* sys, int64_t m2, int64_t n2, double* A_host, double* b_host,
                                   double* xref_host, void* stream);

@@ -33,7 +33,7 @@ EXPORTS = (
     "kz_generate_counter", "kz_system_download",
     "kz_row_norms", "kz_sampler_build", "kz_sampler_set_ranges", "kz_dump_rows", "kz_solve",
     "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
-    "kz_cgls", "kz_spectral", "kz_system_load_file",
+    "kz_cgls", "kz_spectral", "kz_system_load_file", "kz_generate_counter_rows",
 )
 
 

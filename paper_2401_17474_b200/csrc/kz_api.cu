@@ -170,6 +170,13 @@ struct kz_system {
     DevBuf<long long> dbg;
     DevBuf<double> cg;     // CGLS work vectors (kz_cgls)
     DevBuf<double> stage;  // dense host-upload staging (one 1-D copy, then a device repack)
+    // per-call host work reused across kz_solve calls (row-sharded loops call it every iteration):
+    // worker streams, weights and the kernel plan
+    uint64_t pods_seed = 0;
+    int64_t pods_off = -1, pods_q = -1;
+    std::vector<double> alphas_cache;
+    int64_t plan_key[6] = {-1, -1, -1, -1, -1, -1};
+    unsigned char plan_blob[128];  // the cached Plan (trivially copyable)
     SolveStatus* h_status = nullptr;  // pinned
     bool norms_valid = false;
     bool bs2_valid = false;
@@ -331,13 +338,19 @@ extern "C" int32_t kz_system_set_xref(kz_system* s, const double* xref, void* st
 
 extern "C" int32_t kz_generate_counter(kz_system* s, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,
                                        double sg_hi, void* stream) {
+    return kz_generate_counter_rows(s, seed, 0, mu_lo, mu_hi, sg_lo, sg_hi, stream);
+}
+
+extern "C" int32_t kz_generate_counter_rows(kz_system* s, uint64_t seed, int64_t row0, double mu_lo, double mu_hi,
+                                            double sg_lo, double sg_hi, void* stream) {
+    if (row0 < 0) return fail(KZ_EINVAL, "row0 must be >= 0");
     if (!s) return fail(KZ_EINVAL, "null system");
     if (!(sg_lo > 0) || sg_hi < sg_lo || mu_hi < mu_lo) return fail(KZ_EINVAL, "bad generator ranges");
     cudaStream_t st = (cudaStream_t)stream;
     KZ_CUDA(cudaSetDevice(s->device));
     const int64_t pairs = s->m * (s->ld / 2);
     const unsigned blocks = (unsigned)std::min<int64_t>((pairs + 255) / 256, (int64_t)s->sms * 64);
-    gen_counter_kernel<<<blocks, 256, 0, st>>>(s->A.p, s->m, s->n, s->ld, seed, mu_lo, mu_hi, sg_lo, sg_hi);
+    gen_counter_kernel<<<blocks, 256, 0, st>>>(s->A.p, s->m, s->n, s->ld, seed, mu_lo, mu_hi, sg_lo, sg_hi, row0);
     KZ_TRY(check_launch("gen_counter_kernel"));
     gen_xstar_kernel<<<(unsigned)((s->ld / 2 + 255) / 256), 256, 0, st>>>(s->xref.p, s->n, s->ld, seed, mu_lo, mu_hi,
                                                                           sg_lo, sg_hi);
@@ -520,6 +533,7 @@ extern "C" int32_t kz_dump_rows(kz_system* s, int32_t scheme, int64_t q, uint64_
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_TRY(ensure_sampler(s, scheme, q, st));
     KZ_TRY(s->states.ensure(std::max<int64_t>(q, 1)));
+    s->pods_q = -1;  // kz_solve's cached worker streams are overwritten below
     PcgPod pod = seed_stream(seed, (uint64_t)worker);
     KZ_CUDA(cudaMemcpyAsync(s->states.p, &pod, sizeof(pod), cudaMemcpyHostToDevice, st));
     KZ_TRY(s->rows_out.ensure(count));
@@ -1111,14 +1125,22 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         KZ_TRY(check_launch("pack_bs2_kernel"));
         s->bs2_valid = true;
     }
-    std::vector<PcgPod> pods(q);
-    for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)(p->worker_offset + t));
-    KZ_TRY(s->states.ensure(q));
-    KZ_CUDA(cudaMemcpyAsync(s->states.p, pods.data(), q * sizeof(PcgPod), cudaMemcpyHostToDevice, st));
+    if (!(s->pods_q == q && s->pods_seed == p->base_seed && s->pods_off == p->worker_offset)) {
+        std::vector<PcgPod> pods(q);
+        for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)(p->worker_offset + t));
+        KZ_TRY(s->states.ensure(q));
+        KZ_CUDA(cudaMemcpyAsync(s->states.p, pods.data(), q * sizeof(PcgPod), cudaMemcpyHostToDevice, st));
+        s->pods_q = q;
+        s->pods_seed = p->base_seed;
+        s->pods_off = p->worker_offset;
+    }
     std::vector<double> al(q, 1.0);
     if (p->alphas_host) std::copy(p->alphas_host, p->alphas_host + q, al.begin());
-    KZ_TRY(s->alphas.ensure(q));
-    KZ_CUDA(cudaMemcpyAsync(s->alphas.p, al.data(), q * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (al != s->alphas_cache) {
+        KZ_TRY(s->alphas.ensure(q));
+        KZ_CUDA(cudaMemcpyAsync(s->alphas.p, al.data(), q * sizeof(double), cudaMemcpyHostToDevice, st));
+        s->alphas_cache = al;
+    }
     if (!p->keep_x) KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
     const bool partial_mode = p->partial_dev != nullptr;
     if (partial_mode && !(budget_mode && p->budget == 1))
@@ -1134,7 +1156,17 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             kern = KZ_KERNEL_SYNC_CLUSTER;  // one or several clusters; grid barrier as the fallback
         }
     }
-    if (kern == KZ_KERNEL_CHAIN) {
+    const int64_t key[6] = {kern, q, bs, p->ctas, p->threads, p->kernel};
+    static_assert(sizeof(Plan) <= sizeof(s->plan_blob), "plan cache");
+    if (std::equal(key, key + 6, s->plan_key)) {
+        memcpy(&pl, s->plan_blob, sizeof(Plan));  // same shape as the previous call: reuse its plan
+        // the dynamic shared-memory limit is a property of the kernel function, which another
+        // system may have lowered since: restore it for this plan
+        void* fn = pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair)
+                   : pl.tma                     ? rka_fn(pl.lg, pl.epl, q <= 8 * RKA_NW)
+                                                : sync_fn(pl.kernel == KZ_KERNEL_SYNC_CLUSTER, pl.lpr);
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    } else if (kern == KZ_KERNEL_CHAIN) {
         KZ_TRY(plan_chain(s, p, q, pl));
     } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {
         if (bs != 1) return fail(KZ_EINVAL, "the sync kernels run RKA / RKAB with block_size 1 only");
@@ -1148,6 +1180,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     } else {
         return fail(KZ_EINVAL, "unknown kernel selector %d", kern);
     }
+    memcpy(s->plan_blob, &pl, sizeof(Plan));
+    std::copy(key, key + 6, s->plan_key);
     r->kernel_used = pl.kernel;
     r->ctas = pl.ctas;
     r->threads = pl.threads;
@@ -1251,6 +1285,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             // CTA-pair clusters not launchable cooperatively here: one CTA per worker
             setenv("KZ_CHAIN_PAIR", "1", 1);
             KZ_TRY(plan_chain(s, p, q, pl));
+            memcpy(s->plan_blob, &pl, sizeof(Plan));
             args.stages = pl.stages;
             r->ctas = pl.ctas;
             r->threads = pl.threads;
@@ -1260,6 +1295,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             p->kernel == KZ_KERNEL_AUTO) {
             // several clusters not launchable cooperatively here: grid-barrier kernel
             KZ_TRY(plan_sync(s, p, q, false, pl));
+            memcpy(s->plan_blob, &pl, sizeof(Plan));
             KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
             args.part = s->part.p;
             args.stages = pl.stages;
@@ -1268,6 +1304,14 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             lrc = launch_solve(s, pl, args, st);
         }
         KZ_TRY(lrc);
+        if (partial_mode) {
+            // row-sharded local step: exactly one iteration, left in flight on the stream (the
+            // collective and kz_average_from that follow are stream-ordered); no host sync
+            r->iterations = 1;
+            r->rows_projected = q * bs;
+            r->kernel_launches = g_launches.load() - launches0;
+            return KZ_OK;
+        }
         KZ_CUDA(cudaEventRecord(s->ev[3], st));
         KZ_CUDA(cudaMemcpyAsync(s->h_status, s->status.p, sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
         KZ_CUDA(cudaStreamSynchronize(st));

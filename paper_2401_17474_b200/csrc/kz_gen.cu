@@ -44,15 +44,16 @@ constexpr uint64_t TAG_XS = 0x585354ULL;    // "XST"
 }  // namespace
 
 __global__ void gen_counter_kernel(double* __restrict__ A, int64_t m, int64_t n, int64_t ld, uint64_t seed,
-                                   double mu_lo, double mu_hi, double sg_lo, double sg_hi) {
+                                   double mu_lo, double mu_hi, double sg_lo, double sg_hi, int64_t row0) {
     const int64_t pairs = ld / 2;
     const int64_t total = m * pairs;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = g / pairs, p = g - i * pairs;
-        const double mu = mu_lo + (mu_hi - mu_lo) * u01(seed, TAG_ROW, 2 * (uint64_t)i);
-        const double sg = sg_lo + (sg_hi - sg_lo) * u01(seed, TAG_ROW, 2 * (uint64_t)i + 1);
-        const double2 z = normal2(seed, (uint64_t)i, (uint64_t)p);
+        const uint64_t gi = (uint64_t)(row0 + i);  // global row: shards are exact row slices
+        const double mu = mu_lo + (mu_hi - mu_lo) * u01(seed, TAG_ROW, 2 * gi);
+        const double sg = sg_lo + (sg_hi - sg_lo) * u01(seed, TAG_ROW, 2 * gi + 1);
+        const double2 z = normal2(seed, gi, (uint64_t)p);
         const int64_t j = 2 * p;
         double2 out;
         out.x = (j < n) ? fma(sg, z.x, mu) : 0.0;

@@ -110,7 +110,7 @@ __global__ void scale_copy_kernel(const double* __restrict__ S, double inv_div, 
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
 
 __global__ void gen_counter_kernel(double* __restrict__ A, int64_t m, int64_t n, int64_t ld, uint64_t seed,
-                                   double mu_lo, double mu_hi, double sg_lo, double sg_hi);
+                                   double mu_lo, double mu_hi, double sg_lo, double sg_hi, int64_t row0);
 __global__ void gen_xstar_kernel(double* __restrict__ x, int64_t n, int64_t ld, uint64_t seed, double mu_lo,
                                  double mu_hi, double sg_lo, double sg_hi);
 __global__ void gemv_rows_kernel(const double* __restrict__ A, const double* __restrict__ x, int64_t m, int64_t n,

@@ -88,6 +88,25 @@ class CudaShard:
         self.rows = 0
         self.kernel = None
 
+    @classmethod
+    def counter(cls, m_total: int, n: int, plan: ShardPlan, seed: int, device: int) -> "CudaShard":
+        """The rank's rows of the counter-keyed config-3 system, generated in place on its GPU
+        (bit-identical to rows [lo, hi] of the full matrix; no host copy)."""
+        import torch
+
+        from .solvers import DeviceSystem
+
+        self = cls.__new__(cls)
+        self.plan = plan
+        self.ds = DeviceSystem(m=plan.m_local, n=n, device=device)
+        self.ds.generate_counter(seed, row0=plan.lo)
+        self.ds.set_ranges(plan.worker_lo, plan.worker_len)
+        self.S = torch.zeros(self.ds.pitch, dtype=torch.float64, device=f"cuda:{device}")
+        self.kernel_ms = 0.0
+        self.rows = 0
+        self.kernel = None
+        return self
+
     def reset(self) -> float:
         self.ds.set_x(None)
         return self.ds.error_sq()

@@ -159,10 +159,12 @@ class DeviceSystem:
         self._xref_set = True
         return a.value, b.value, x.value, self.pitch
 
-    def generate_counter(self, seed: int = 0, mu_range=(-5.0, 5.0), sigma_range=(1.0, 20.0)) -> None:
-        """Fill the system with the counter-keyed BASELINE config-3 generator (device only)."""
-        N.check(self._lib.kz_generate_counter(self.handle, int(seed), float(mu_range[0]), float(mu_range[1]),
-                                              float(sigma_range[0]), float(sigma_range[1]), None))
+    def generate_counter(self, seed: int = 0, mu_range=(-5.0, 5.0), sigma_range=(1.0, 20.0), row0: int = 0) -> None:
+        """Fill the system with the counter-keyed BASELINE config-3 generator (device only);
+        `row0` makes it rows [row0, row0 + m) of the full system (a row shard)."""
+        N.check(self._lib.kz_generate_counter_rows(self.handle, C.c_uint64(int(seed)), C.c_int64(int(row0)),
+                                                   C.c_double(mu_range[0]), C.c_double(mu_range[1]),
+                                                   C.c_double(sigma_range[0]), C.c_double(sigma_range[1]), None))
         self._xref_set = True
 
     def download(self, m2: int | None = None, n2: int | None = None):
@@ -238,6 +240,14 @@ class DeviceSystem:
         un-normalised worker sum S = sum_t v_t to `partial_ptr` (device)."""
         variant = cfg.variant
         q = 1 if variant in ("rk", "ck") else cfg.q
+        key = (cfg, int(worker_offset), int(partial_ptr), None if alphas is None else tuple(np.asarray(alphas).ravel()))
+        cached = getattr(self, "_step_cache", None)
+        if cached is not None and cached[0] == key:  # same step shape: only the iteration index moves
+            _, p, al, r = cached
+            p.k_start = int(k)
+            N.check(self._lib.kz_solve(self.handle, C.byref(p), C.byref(r), None, None))
+            return {"kernel_ms": 0.0, "loop_ms": 0.0, "rows": int(r.rows_projected),
+                    "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches)}
         al = N.f64(np.ones(q) if alphas is None else alphas)
         p = N.Params()
         p.variant = N.VARIANT_IDS[variant]
@@ -255,6 +265,7 @@ class DeviceSystem:
         p.partial_dev = C.c_void_p(partial_ptr)
         r = N.Result()
         N.check(self._lib.kz_solve(self.handle, C.byref(p), C.byref(r), None, None))
+        self._step_cache = (key, p, al, r)
         return {"kernel_ms": float(r.kernel_ms), "loop_ms": float(r.loop_ms), "rows": int(r.rows_projected),
                 "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches)}
 
