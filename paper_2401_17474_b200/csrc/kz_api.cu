@@ -1221,7 +1221,6 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.use_stop = stop_mode ? 1 : 0;
     args.stages = pl.stages;
     args.box = pl.box;
-    args.cpasync = 0;
     if (pl.tma) KZ_TRY(ensure_tmaps(s, pl.box));
     const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
     args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;

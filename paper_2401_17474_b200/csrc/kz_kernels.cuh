@@ -44,7 +44,6 @@ struct SolveArgs {
     long long* dbg;        // optional phase timestamps (KZ_PHASE_TIMING=1)
     int ablate;            // debug: bit mask of phases to skip (KZ_ABLATE), timing experiments only
     int box;               // rka kernel: TMA box width (columns of the row slice)
-    int cpasync;           // rka kernel: stage rows with cp.async (many narrow rows) instead of TMA gather4
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
