@@ -407,22 +407,6 @@ __device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned pari
 
 }  // namespace kz
 
-namespace kz {
-
-// 16-byte cp.async with zero fill (src_size 0 => 16 zero bytes, no global read).
-__device__ __forceinline__ void cp_async16_zfill(unsigned dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-                 : "memory");
-}
-
-// Arrive on a local mbarrier once all of this thread's prior cp.async copies have
-// landed (the arrival is not counted in advance: init the barrier with one
-// expected arrival per participating thread).
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(unsigned long long* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-}  // namespace kz
 
 namespace kz {
 
