@@ -65,3 +65,17 @@ def test_emulated_ranks_one_gpu(gpu, oracle, world, variant, bs):
     o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=world * q_local, block_size=bs, base_seed=7,
                      scheme="distributed", budget=budget)
     assert rel_err(xs[0], o["x"]) <= PARITY_TOL
+
+
+def test_counter_shard_is_exact_row_slice(gpu):
+    """kz_generate_counter_rows: a shard generated in place equals those rows of the
+    full counter-keyed matrix (so row-sharded config-3 runs need no host copy)."""
+    from paper_2401_17474_b200 import DeviceSystem
+
+    with DeviceSystem(m=3000, n=700) as full:
+        full.generate_counter(7)
+        A, b, xr = full.download()
+    with DeviceSystem(m=1000, n=700) as part:
+        part.generate_counter(7, row0=1500)
+        A2, b2, xr2 = part.download()
+    assert np.array_equal(A2, A[1500:2500]) and np.array_equal(b2, b[1500:2500]) and np.array_equal(xr2, xr)
