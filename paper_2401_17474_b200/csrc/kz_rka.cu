@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         const unsigned bpar = (unsigned)((kk >> 1) & 1);
         const bool rec = TIMING && a.dbg != nullptr && c == 0 && lane == 0 && kk < 32;
         if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 0] = clock64();
-        if (tid == 0) {
+        if (tid == 32) {  // warp 1: not on the producer warp's scheduler (warps 0, 4, 8 share one)
             if (!last) {
                 if (n_own > 0) mbar_arrive_expect_tx(&xbar[par], (unsigned)(n_own * Pc * (int)sizeof(double)));
                 mbar_arrive_expect_tx(&sbar[par], (unsigned)(q * (int)sizeof(double)));
