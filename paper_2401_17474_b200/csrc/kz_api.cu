@@ -689,6 +689,7 @@ void* chain_fn(int ep, int R, int C) {
         case 10801: return (void*)chain_kernel<8, 1, 1>;
         case 10802: return (void*)chain_kernel<8, 2, 1>;
         case 11601: return (void*)chain_kernel<16, 1, 1>;
+        case 20104: return (void*)chain_kernel<1, 4, 2>;
         case 20204: return (void*)chain_kernel<2, 4, 2>;
         case 20402: return (void*)chain_kernel<4, 2, 2>;
         case 20404: return (void*)chain_kernel<4, 4, 2>;
@@ -714,7 +715,7 @@ constexpr int MAXG_CLUSTERS = 10;  // = MAXG in kz_sync.cu
 static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     // a worker is one CTA, or a CTA pair (thread-block cluster of 2, each CTA
     // half the columns) when the rows are long and the pairs fit the SMs
-    int C = (s->ld >= 2048 && 2 * q <= s->sms) ? 2 : 1;
+    int C = (s->ld >= 1024 && 2 * q <= s->sms) ? 2 : 1;  // measured: pairs win from n ~ 1000 (c2, c4 RK)
     if (const char* e = getenv("KZ_CHAIN_PAIR")) C = atoi(e) == 2 && 2 * q <= s->sms ? 2 : 1;
     const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };

@@ -542,6 +542,7 @@ KZ_CHAIN(4, 4, 1)
 KZ_CHAIN(8, 1, 1)
 KZ_CHAIN(8, 2, 1)
 KZ_CHAIN(16, 1, 1)
+KZ_CHAIN(1, 4, 2)
 KZ_CHAIN(2, 4, 2)
 KZ_CHAIN(4, 2, 2)
 KZ_CHAIN(4, 4, 2)
