@@ -177,6 +177,7 @@ struct kz_system {
     std::vector<double> alphas_cache;
     int64_t plan_key[6] = {-1, -1, -1, -1, -1, -1};
     unsigned char plan_blob[128];  // the cached Plan (trivially copyable)
+    bool no_pairs = false;         // CTA-pair clusters not launchable cooperatively on this device
     SolveStatus* h_status = nullptr;  // pinned
     bool norms_valid = false;
     bool bs2_valid = false;
@@ -715,7 +716,7 @@ constexpr int MAXG_CLUSTERS = 10;  // = MAXG in kz_sync.cu
 static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     // a worker is one CTA, or a CTA pair (thread-block cluster of 2, each CTA
     // half the columns) when the rows are long and the pairs fit the SMs
-    int C = (s->ld >= 1024 && 2 * q <= s->sms) ? 2 : 1;  // measured: pairs win from n ~ 1000 (c2, c4 RK)
+    int C = (s->ld >= 1024 && 2 * q <= s->sms && !s->no_pairs) ? 2 : 1;  // measured: pairs win from n ~ 1000
     if (const char* e = getenv("KZ_CHAIN_PAIR")) C = atoi(e) == 2 && 2 * q <= s->sms ? 2 : 1;
     const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
@@ -1283,7 +1284,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         int lrc = launch_solve(s, pl, args, st);
         if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && k == 0) {
             // CTA-pair clusters not launchable cooperatively here: one CTA per worker
-            setenv("KZ_CHAIN_PAIR", "1", 1);
+            s->no_pairs = true;  // remembered for this system (no process-wide side effects)
             KZ_TRY(plan_chain(s, p, q, pl));
             memcpy(s->plan_blob, &pl, sizeof(Plan));
             args.stages = pl.stages;
