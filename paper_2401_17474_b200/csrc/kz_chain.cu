@@ -412,7 +412,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                         if (slot < a.ckpt_cap) {
 #pragma unroll
                             for (int p = 0; p < EP; ++p) {
-                                const int64_t col = cb + 2 * ((int64_t)p * T + tid);
+                                const int64_t lc = 2 * ((int64_t)p * T + tid);
+                                const int64_t col = cb + lc;
+                                if (lc >= ldc) continue;  // lanes past this CTA's slice own nothing
                                 if (col < a.n) a.ckpt[slot * a.n + col] = v[2 * p];
                                 if (col + 1 < a.n) a.ckpt[slot * a.n + col + 1] = v[2 * p + 1];
                             }

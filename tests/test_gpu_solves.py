@@ -355,3 +355,25 @@ def test_kzsys_file_straight_to_device(gpu, systems, tmp_path):
     p.write_bytes(open(p, "rb").read()[:-100])
     with pytest.raises(SystemFormatError):
         DeviceSystem.from_file(p)
+
+
+def test_chain_cta_pairs_match_oracle(gpu, oracle):
+    """Rows of n >= 1024 run on CTA pairs (thread-block clusters of 2, DSMEM join per row
+    block): RK and RKAB against the oracle, checkpoints every 500 rows / 2 outer iterations."""
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, generate_mother, solve_rk, solve_rkab_seq
+
+    s = generate_mother(GeneratorConfig(m_max=12000, n_max=1500, seed=6))
+    with DeviceSystem(s) as ds:
+        cap = []
+        r = solve_rk(ds, _cfg(variant="rk", base_seed=2), budget=3000, capture=cap)
+        assert r.gpu["ctas"] == 2, r.gpu
+        o = oracle.solve(s.A, s.b, s.x_star, variant="rk", base_seed=2, budget=3000, ckpt_every=500)
+        for j, ck in enumerate(o["checkpoints"]):
+            assert rel_err(cap[500 * (j + 1) - 1], ck) <= PARITY_TOL, ("rk", j)
+        cap = []
+        r = solve_rkab_seq(ds, _cfg(variant="rkab", q=8, block_size=60, base_seed=4), budget=12, capture=cap)
+        assert r.gpu["ctas"] == 16, r.gpu
+        o = oracle.solve(s.A, s.b, s.x_star, variant="rkab", q=8, block_size=60, base_seed=4, budget=12,
+                         ckpt_every=2)
+        for j, ck in enumerate(o["checkpoints"]):
+            assert rel_err(cap[2 * (j + 1) - 1], ck) <= PARITY_TOL, ("rkab", j)
