@@ -250,17 +250,26 @@ def sharded_extras(rank, world, local_rank, steps=3):
     import torch.distributed as dist
 
     from paper_2401_17474_b200 import SolverConfig
-    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded
+    from paper_2401_17474_b200.multigpu import CudaShard, ShardComm, plan_shards, solve_sharded, solve_sharded_native
 
     out = []
     m_total, n, q = 160000, 20000, 64
     try:
         plan = plan_shards(m_total, world, rank, q)
         shard = CudaShard.counter(m_total, n, plan, 0, local_rank)
-        for tag, kw, budget in (("c3_sharded_rkab_bs1000", dict(variant="rkab", q=q, block_size=1000), 1),
-                                ("c3_sharded_rka", dict(variant="rka", q=q), 200)):
+        comm = ShardComm(local_rank, world, rank) if world > 1 else None
+        cases = (("c3_sharded_rkab_bs1000", dict(variant="rkab", q=q, block_size=1000), 1, True),
+                 ("c3_sharded_rka", dict(variant="rka", q=q), 200, True),
+                 ("c3_sharded_rka_host_loop", dict(variant="rka", q=q), 200, False))
+        for tag, kw, budget, native in cases:
             cfg = SolverConfig(device=local_rank, sampling_scheme="distributed", **kw)
-            solve_sharded(shard, cfg, budget=budget)  # warm-up
+
+            def run(c):
+                if native:
+                    return solve_sharded_native(shard, c, budget=budget, comm=comm)
+                return solve_sharded(shard, c, budget=budget)
+
+            run(cfg)  # warm-up
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
@@ -268,7 +277,7 @@ def sharded_extras(rank, world, local_rank, steps=3):
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record()
             for k in range(steps):
-                solve_sharded(shard, cfg.replace(base_seed=k), budget=budget)
+                run(cfg.replace(base_seed=k))
             ev1.record()
             torch.cuda.synchronize()
             tt = torch.tensor([ev0.elapsed_time(ev1)], device=f"cuda:{local_rank}")
@@ -279,9 +288,13 @@ def sharded_extras(rank, world, local_rank, steps=3):
             rows_s = float(rr.item()) / (float(tt.item()) / 1e3)
             out.append({"workload": tag, "n_gpus": world, "rows_per_s": rows_s, "ms_per_step": float(tt.item()) / steps,
                         "desc": f"160000x20000 counter-keyed, rows sharded x{world}, q={q} per GPU, "
-                                f"{budget} outer iteration(s) per step, NCCL all-reduce per outer iteration",
+                                f"{budget} outer iteration(s) per step, NCCL all-reduce per outer iteration, "
+                                + ("native loop (kz_solve_sharded: no host sync per iteration)" if native
+                                   else "host-driven loop (multigpu.solve_sharded)"),
                         "hbm_frac_per_gpu": rows_s / world * 8 * n / 1e9 / read_peak()[0]})
         shard.close()
+        if comm is not None:
+            comm.close()
     except Exception as exc:  # extras must never sink the headline line
         out.append({"error": repr(exc)})
     return out

@@ -213,6 +213,32 @@ KZ_API int32_t kz_system_load_file(int32_t device, const char* path, int64_t row
 KZ_API int32_t kz_spectral(kz_system* sys, int64_t row_lo, int64_t row_hi, const double* v0_host,
                            const double* v1_host, double tol, int64_t max_it, double* out, void* stream);
 
+/* ---- row-sharded multi-GPU solve (replaces distributed.py:282-363
+ * solve_rka_dist / solve_rkab_dist / run_distributed_solve and the
+ * SimTransport.allreduce_sum of distributed.py:119-148) ----------------------
+ * One process per GPU.  Rank 0 draws an id with kz_comm_unique_id, the caller
+ * broadcasts its KZ_COMM_ID_BYTES bytes (e.g. torch.distributed), and every
+ * rank creates its communicator (NCCL over NVLink / NVSwitch; libnccl.so.2 is
+ * loaded at first use -- the process's own copy when one is loaded). */
+typedef struct kz_comm kz_comm;
+#define KZ_COMM_ID_BYTES 128
+KZ_API int32_t kz_comm_unique_id(uint8_t* id_out);
+KZ_API int32_t kz_comm_create(int32_t device, const uint8_t* id, int32_t world, int32_t rank, kz_comm** out);
+KZ_API int32_t kz_comm_destroy(kz_comm* comm);
+/* The whole _drive loop (solvers.py:182-263) of one rank's row shard, natively:
+ * per outer iteration the local step writes the rank's worker sum S_g, S is
+ * all-reduced in place over `comm` (NULL: a single rank), and x = S / (q *
+ * world) with ||x - x_ref||^2 and the stop rule evaluated on the device.  No
+ * host synchronisation per iteration: a device stop flag turns every launch
+ * after convergence into a no-op and the host reads the per-iteration errors
+ * once per chunk.  Every rank computes bit-identical x and errors, so all stop
+ * together (distributed.py:233-235).  params: variant RKA or RKAB, scheme
+ * KZ_SCHEME_RANGES (kz_sampler_set_ranges with the rank's worker blocks),
+ * worker_offset = rank * q, stop or budget mode (no trace / checkpoints);
+ * partial_dev is ignored.  result->rows_projected counts this rank's rows. */
+KZ_API int32_t kz_solve_sharded(kz_system* shard, kz_comm* comm, const kz_params* params, kz_result* result,
+                                double* x_host, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,8 +18,11 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
 #include <fcntl.h>
 #include <unistd.h>
+
+#include <nccl.h>  // types only: the library is dlopen'ed (the process's already-loaded libnccl.so.2 if any)
 
 #include "../../include/kz_b200.h"
 #include "kz_kernels.cuh"
@@ -170,6 +173,11 @@ struct kz_system {
     DevBuf<long long> dbg;
     DevBuf<double> cg;     // CGLS work vectors (kz_cgls)
     DevBuf<double> stage;  // dense host-upload staging (one 1-D copy, then a device repack)
+    DevBuf<unsigned long long> ll;  // rka kernel: tagged words of the cross-cluster exchange
+    unsigned tag_seq = 0;           // next free tag range of `ll`
+    DevBuf<double> S;               // kz_solve_sharded: the rank's worker sum (all-reduced in place)
+    DevBuf<double> errs;            // kz_solve_sharded: ||x_k - x_ref||^2 per iteration of a chunk
+    DevBuf<int> halt;               // kz_solve_sharded: device stop flag (k + 1 of the stop, 0 = running)
     // per-call host work reused across kz_solve calls (row-sharded loops call it every iteration):
     // worker streams, weights and the kernel plan
     uint64_t pods_seed = 0;
@@ -251,8 +259,10 @@ extern "C" int32_t kz_system_destroy(kz_system* s) {
     if (!s) return KZ_OK;
     cudaSetDevice(s->device);
     for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas, &s->bs2,
-                    &s->cg, &s->stage})
+                    &s->cg, &s->stage, &s->S, &s->errs})
         b->release();
+    s->ll.release();
+    s->halt.release();
     s->dbg.release();
     s->lo.release();
     s->len.release();
@@ -1092,12 +1102,22 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
     return KZ_OK;
 }
 
-extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, double* x_host, void* stream) {
-    if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
-    memset(r, 0, sizeof(*r));
-    r->final_error_sq = NAN;
-    r->final_residual = NAN;
-    cudaStream_t st = (cudaStream_t)stream;
+namespace {
+// Everything a solve needs between setup and its iteration loop (kz_solve, kz_solve_sharded).
+struct SolveCtx {
+    bool sharded = false;  // kz_solve_sharded: partial steps driven per iteration by the native loop
+    int64_t q = 1, bs = 1;
+    bool budget_mode = false, trace_mode = false, stop_mode = false, cyclic = false, partial_mode = false;
+    Plan pl;
+    SolveArgs args = {};
+    int64_t n_ck_cap = 0, chunk_cap = 1;
+    bool phase_timing = false;
+};
+}  // namespace
+
+// Validation, cached setup (norms, sampler, packed records, worker streams,
+// weights), kernel plan, scratch and the kernel arguments.
+static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStream_t st, SolveCtx& cx) {
     // --- validation (SolverConfig.validate, solvers.py:85-101; _drive 200-214) ---
     if (p->variant < KZ_RK || p->variant > KZ_CK) return fail(KZ_EINVAL, "unknown variant %d", p->variant);
     if (p->q < 1) return fail(KZ_EINVAL, "q must be >= 1, got %lld", (long long)p->q);
@@ -1145,7 +1165,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     }
     if (!p->keep_x) KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
     const bool partial_mode = p->partial_dev != nullptr;
-    if (partial_mode && !(budget_mode && p->budget == 1))
+    if (partial_mode && !cx.sharded && !(budget_mode && p->budget == 1))
         return fail(KZ_EINVAL, "partial (row-sharded) steps run exactly one iteration: set budget = 1");
 
     // --- kernel plan ---
@@ -1195,6 +1215,17 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     KZ_TRY(s->idx.ensure(std::min<int64_t>(idx_cap, chunk_cap * draws_per_iter)));
     if (pl.kernel == KZ_KERNEL_CHAIN && q > 1) KZ_TRY(s->V.ensure((size_t)q * s->ld));
     KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
+    if (pl.tma && pl.ctas > pl.cluster) {
+        // tagged words of the rka kernel's cluster exchange: a buffer of their own, zeroed once;
+        // every launch draws a fresh tag range (tag_base), so stale words never match
+        const size_t words = 4 * (size_t)(pl.ctas / pl.cluster) * (q + 1);
+        if (s->ll.cap < words) {
+            KZ_TRY(s->ll.ensure(words));
+            KZ_CUDA(cudaMemsetAsync(s->ll.p, 0, s->ll.cap * sizeof(unsigned long long), st));
+            s->tag_seq = 0;
+        }
+        KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
+    }
     const int64_t n_ck_cap = p->ckpt_every > 0 ? std::max<int64_t>(0, p->ckpt_capacity) : 0;
     if (n_ck_cap > 0) KZ_TRY(s->ckpt.ensure((size_t)n_ck_cap * s->n));
 
@@ -1209,7 +1240,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     args.V = s->V.p;
     args.idx = s->idx.p;
     args.alphas = s->alphas.p;
-    args.part = s->part.p;
+    args.part = (pl.tma && pl.ctas > pl.cluster) ? reinterpret_cast<double*>(s->ll.p) : s->part.p;
     args.barrier = s->barrier.p;
     args.status = s->status.p;
     args.ckpt = s->ckpt.p;
@@ -1231,6 +1262,80 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 128 * sizeof(long long), st));
         args.dbg = s->dbg.p;
     }
+
+    cx.q = q;
+    cx.bs = bs;
+    cx.budget_mode = budget_mode;
+    cx.trace_mode = trace_mode;
+    cx.stop_mode = stop_mode;
+    cx.cyclic = cyclic;
+    cx.partial_mode = partial_mode;
+    cx.pl = pl;
+    cx.args = args;
+    cx.n_ck_cap = n_ck_cap;
+    cx.chunk_cap = chunk_cap;
+    cx.phase_timing = phase_timing;
+    return KZ_OK;
+}
+
+// One launch of the planned solve kernel over args.count iterations, with the
+// plan fallbacks a first launch may need (CTA pairs / several clusters not
+// launchable cooperatively on this device).
+static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx& cx, bool first, cudaStream_t st) {
+    Plan& pl = cx.pl;
+    SolveArgs& args = cx.args;
+    const int64_t q = cx.q;
+    if (!pl.tma) KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
+    if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER && !pl.tma && pl.ctas > pl.cluster) {  // sync kernel: tags restart at 1
+        KZ_CUDA(cudaMemsetAsync(s->part.p, 0, 4 * (size_t)(pl.ctas / pl.cluster) * (q + 1) * sizeof(double), st));
+        KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
+    }
+    if (pl.tma) {
+        args.tag_base = s->tag_seq;
+        s->tag_seq += (unsigned)args.count + 2u;
+    }
+    int lrc = launch_solve(s, pl, args, st);
+    if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && first) {
+        // CTA-pair clusters not launchable cooperatively here: one CTA per worker
+        s->no_pairs = true;  // remembered for this system (no process-wide side effects)
+        KZ_TRY(plan_chain(s, p, q, pl));
+        memcpy(s->plan_blob, &pl, sizeof(Plan));
+        args.stages = pl.stages;
+        r->ctas = pl.ctas;
+        r->threads = pl.threads;
+        if (pl.ctas > 1) KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
+        lrc = launch_solve(s, pl, args, st);
+    }
+    if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_SYNC_CLUSTER && pl.ctas > pl.cluster && first &&
+        p->kernel == KZ_KERNEL_AUTO) {
+        // several clusters not launchable cooperatively here: grid-barrier kernel
+        KZ_TRY(plan_sync(s, p, q, false, pl));
+        memcpy(s->plan_blob, &pl, sizeof(Plan));
+        KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
+        args.part = s->part.p;
+        args.stages = pl.stages;
+        r->kernel_used = pl.kernel;
+        r->ctas = pl.ctas;
+        KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
+        lrc = launch_solve(s, pl, args, st);
+    }
+    return lrc;
+}
+
+extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, double* x_host, void* stream) {
+    if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
+    memset(r, 0, sizeof(*r));
+    r->final_error_sq = NAN;
+    r->final_residual = NAN;
+    cudaStream_t st = (cudaStream_t)stream;
+    SolveCtx cx;
+    KZ_TRY(solve_setup(s, p, r, st, cx));
+    const int64_t q = cx.q, bs = cx.bs;
+    const bool budget_mode = cx.budget_mode, trace_mode = cx.trace_mode, stop_mode = cx.stop_mode,
+               cyclic = cx.cyclic, partial_mode = cx.partial_mode, phase_timing = cx.phase_timing;
+    const int64_t n_ck_cap = cx.n_ck_cap, chunk_cap = cx.chunk_cap;
+    Plan& pl = cx.pl;
+    SolveArgs& args = cx.args;
 
     const int64_t limit = budget_mode ? p->budget : p->max_iterations;
     int64_t k = 0, evals = 0;
@@ -1275,36 +1380,8 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         args.count = c;
         args.idx_stride = c * bs;
         args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
-        KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
-        if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER && pl.ctas > pl.cluster) {  // tags restart at 1 per launch
-            KZ_CUDA(cudaMemsetAsync(s->part.p, 0, 4 * (size_t)(pl.ctas / pl.cluster) * (q + 1) * sizeof(double), st));
-            KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
-        }
         KZ_CUDA(cudaEventRecord(s->ev[2], st));
-        int lrc = launch_solve(s, pl, args, st);
-        if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && k == 0) {
-            // CTA-pair clusters not launchable cooperatively here: one CTA per worker
-            s->no_pairs = true;  // remembered for this system (no process-wide side effects)
-            KZ_TRY(plan_chain(s, p, q, pl));
-            memcpy(s->plan_blob, &pl, sizeof(Plan));
-            args.stages = pl.stages;
-            r->ctas = pl.ctas;
-            r->threads = pl.threads;
-            lrc = launch_solve(s, pl, args, st);
-        }
-        if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_SYNC_CLUSTER && pl.ctas > pl.cluster && k == 0 &&
-            p->kernel == KZ_KERNEL_AUTO) {
-            // several clusters not launchable cooperatively here: grid-barrier kernel
-            KZ_TRY(plan_sync(s, p, q, false, pl));
-            memcpy(s->plan_blob, &pl, sizeof(Plan));
-            KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
-            args.part = s->part.p;
-            args.stages = pl.stages;
-            r->kernel_used = pl.kernel;
-            r->ctas = pl.ctas;
-            lrc = launch_solve(s, pl, args, st);
-        }
-        KZ_TRY(lrc);
+        KZ_TRY(launch_step(s, p, r, cx, k == 0, st));
         if (partial_mode) {
             // row-sharded local step: exactly one iteration, left in flight on the stream (the
             // collective and kz_average_from that follow are stream-ordered); no host sync
@@ -1817,3 +1894,224 @@ extern "C" int32_t kz_system_load_file(int32_t device, const char* path, int64_t
     return KZ_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Row-sharded multi-GPU solve (distributed.py:282-363 generalised to q workers
+// per rank; BASELINE config 3).  One process per GPU; the ranks' worker sums
+// are all-reduced in place by NCCL over NVLink on the solve stream.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+int nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok ? KZ_OK : fail(KZ_ENODEV, "%s", g_nccl.why.c_str());
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        g_nccl.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+        return fail(KZ_ENODEV, "%s", g_nccl.why.c_str());
+    }
+    g_nccl.get_unique_id = (decltype(g_nccl.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    g_nccl.comm_init_rank = (decltype(g_nccl.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    g_nccl.all_reduce = (decltype(g_nccl.all_reduce))dlsym(h, "ncclAllReduce");
+    g_nccl.comm_destroy = (decltype(g_nccl.comm_destroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.error_string = (decltype(g_nccl.error_string))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.all_reduce || !g_nccl.comm_destroy ||
+        !g_nccl.error_string) {
+        g_nccl.why = "libnccl.so.2 lacks the NCCL 2 entry points";
+        return fail(KZ_ENODEV, "%s", g_nccl.why.c_str());
+    }
+    g_nccl.ok = true;
+    return KZ_OK;
+}
+
+#define KZ_NCCL(call)                                                                                   \
+    do {                                                                                                \
+        ncclResult_t r_ = (call);                                                                       \
+        if (r_ != ncclSuccess) return fail(KZ_ECUDA, "%s failed: %s", #call, g_nccl.error_string(r_)); \
+    } while (0)
+}  // namespace
+
+struct kz_comm {
+    int device = 0, world = 1, rank = 0;
+    ncclComm_t nccl = nullptr;
+};
+
+extern "C" int32_t kz_comm_unique_id(uint8_t* id_out) {
+    if (!id_out) return fail(KZ_EINVAL, "null argument");
+    static_assert(sizeof(ncclUniqueId) == KZ_COMM_ID_BYTES, "NCCL unique id size");
+    KZ_TRY(nccl_load());
+    ncclUniqueId id;
+    KZ_NCCL(g_nccl.get_unique_id(&id));
+    memcpy(id_out, &id, sizeof(id));
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_comm_create(int32_t device, const uint8_t* id, int32_t world, int32_t rank, kz_comm** out) {
+    if (!id || !out) return fail(KZ_EINVAL, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(KZ_EINVAL, "rank %d out of range for world %d", rank, world);
+    *out = nullptr;
+    KZ_TRY(nccl_load());
+    KZ_CUDA(cudaSetDevice(device));
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    kz_comm* c = new kz_comm;
+    c->device = device;
+    c->world = world;
+    c->rank = rank;
+    ncclResult_t r = g_nccl.comm_init_rank(&c->nccl, world, uid, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(KZ_ECUDA, "ncclCommInitRank failed: %s", g_nccl.error_string(r));
+    }
+    *out = c;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_comm_destroy(kz_comm* c) {
+    if (!c) return KZ_OK;
+    if (c->nccl && g_nccl.ok) {
+        cudaSetDevice(c->device);
+        g_nccl.comm_destroy(c->nccl);
+    }
+    delete c;
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params* p, kz_result* r, double* x_host,
+                                    void* stream) {
+    if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
+    memset(r, 0, sizeof(*r));
+    r->final_error_sq = NAN;
+    r->final_residual = NAN;
+    if (p->variant != KZ_RKA && p->variant != KZ_RKAB)
+        return fail(KZ_EINVAL, "row-sharded solves run RKA or RKAB (variant %d)", p->variant);
+    if (p->trace_step > 0 || p->ckpt_every > 0)
+        return fail(KZ_EINVAL, "row-sharded solves have no trace or checkpoint mode");
+    if (comm && comm->device != s->device)
+        return fail(KZ_EINVAL, "communicator on device %d, shard on device %d", comm->device, s->device);
+    const int world = comm ? comm->world : 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_TRY(s->S.ensure(s->ld));
+    KZ_CUDA(cudaMemsetAsync(s->S.p, 0, s->ld * sizeof(double), st));  // the padded tail stays zero
+    kz_params pp = *p;
+    pp.partial_dev = s->S.p;
+    SolveCtx cx;
+    cx.sharded = true;
+    KZ_TRY(solve_setup(s, &pp, r, st, cx));
+    SolveArgs& args = cx.args;
+    args.use_stop = 0;  // the stop rule runs on the averaged x, after the collective
+    args.final_check = 0;
+    args.count = 1;
+    const bool stop_mode = cx.stop_mode, chain = cx.pl.kernel == KZ_KERNEL_CHAIN;
+    const int64_t q = cx.q, bs = cx.bs, Q = q * world;
+    const int64_t limit = cx.budget_mode ? p->budget : p->max_iterations;
+    const int64_t chunk_max = std::min<int64_t>(cx.chunk_cap, 1024);
+    KZ_TRY(s->errs.ensure(chunk_max + 1));
+    KZ_TRY(s->halt.ensure(1));
+    KZ_CUDA(cudaMemsetAsync(s->halt.p, 0, sizeof(int), st));
+    args.halt = s->halt.p;
+    std::vector<double> herr(chunk_max + 1);
+    int hhalt = 0;
+    int32_t* const idx0 = s->idx.p;
+    const long long launches0 = g_launches.load();
+
+    int64_t k = 0, evals = 0;
+    bool converged = false;
+    double err = NAN;
+    if (stop_mode) {  // _drive's check before iteration 0 (x_0 = 0 or the kept iterate)
+        KZ_TRY(error_sq_dev(s, &err, st));
+        evals = 1;
+        converged = err < p->epsilon;
+    }
+    KZ_CUDA(cudaEventRecord(s->ev[0], st));
+    // rka kernel: x_k = S / Q, the stop rule and the halt flag live in the step kernel itself (one
+    // kernel + one collective per outer iteration); chain kernel (RKAB): separate average kernel
+    const bool fused = cx.pl.tma;
+    if (fused) {
+        args.use_stop = stop_mode ? 1 : 0;
+        args.x_div = (double)Q;
+    }
+    int64_t chunk = stop_mode ? 64 : chunk_max;
+    while (!converged && k < limit) {
+        const int64_t c = std::min<int64_t>(chunk, limit - k);
+        // row draws of the whole chunk: one sampler launch (x-independent)
+        const int64_t count = c * bs;
+        if (chain)
+            KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, (p->k_start + k) * bs, count, idx0, count, 1,
+                                  st));
+        else
+            KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, (p->k_start + k) * bs, count, idx0, 1, q, st));
+        for (int64_t i = 0; i < c; ++i) {
+            args.k0 = k + i;
+            args.idx = chain ? idx0 + i * bs : idx0 + i * q;
+            args.idx_stride = chain ? count : q;
+            if (fused) args.x_sum = (k + i == 0) ? nullptr : s->S.p;  // x_0 is the resident iterate
+            KZ_TRY(launch_step(s, &pp, r, cx, k + i == 0, st));
+            if (comm)
+                KZ_NCCL(g_nccl.all_reduce(s->S.p, s->S.p, (size_t)s->ld, ncclFloat64, ncclSum, comm->nccl, st));
+            if (!fused) {
+                shard_average_kernel<<<1, 1024, 0, st>>>(s->S.p, (double)Q, s->n, s->ld, s->xref.p, s->x.p,
+                                                         p->epsilon, stop_mode ? 1 : 0, k + i + 1, s->errs.p + i,
+                                                         s->halt.p);
+                KZ_TRY(check_launch("shard_average_kernel"));
+            }
+        }
+        const bool last_chunk = k + c >= limit;
+        if (fused && last_chunk) {  // x_K = S / Q and the check before iteration K
+            shard_average_kernel<<<1, 1024, 0, st>>>(s->S.p, (double)Q, s->n, s->ld, s->xref.p, s->x.p, p->epsilon,
+                                                     stop_mode ? 1 : 0, k + c, s->errs.p + c - 1, s->halt.p);
+            KZ_TRY(check_launch("shard_average_kernel"));
+        }
+        // one host synchronisation per chunk: the errors, the stop flag and the kernel status
+        KZ_CUDA(cudaMemcpyAsync(herr.data(), s->errs.p, c * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaMemcpyAsync(&hhalt, s->halt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaMemcpyAsync(s->h_status, s->status.p, sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        if (cx.pl.tma && cx.pl.ctas > cx.pl.cluster && s->h_status->aborted)
+            return fail(KZ_ECUDA, "cross-cluster exchange timed out (clusters not co-resident)");
+        if (hhalt != 0) {  // x_{hhalt - 1} met the rule; the launches after it were no-ops
+            const int64_t ks = hhalt - 1;
+            // the stopping kernel's own error total, or the average kernel's
+            err = (fused && ks < k + c) ? s->h_status->err : herr[ks - k - 1];
+            k = ks;
+            evals = k + 1;
+            converged = true;
+            break;
+        }
+        k += c;
+        if (!fused || last_chunk) err = herr[c - 1];
+        if (stop_mode) evals = k + 1;
+        chunk = std::min<int64_t>(chunk_max, chunk * 2);
+    }
+    KZ_CUDA(cudaEventRecord(s->ev[1], st));
+    KZ_CUDA(cudaEventSynchronize(s->ev[1]));
+    float loop_ms = 0.f;
+    cudaEventElapsedTime(&loop_ms, s->ev[0], s->ev[1]);
+    r->iterations = k;
+    r->converged = converged ? 1 : 0;
+    r->error_evals = stop_mode ? evals : 0;
+    r->final_error_sq = stop_mode ? err : NAN;
+    r->rows_projected = k * q * bs;  // this rank's projections
+    r->loop_ms = loop_ms;
+    r->kernel_ms = loop_ms;  // steps, collectives and averages interleave on one stream
+    r->kernel_used = cx.pl.kernel;
+    r->ctas = cx.pl.ctas;
+    r->threads = cx.pl.threads;
+    if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    r->kernel_launches = g_launches.load() - launches0;
+    return KZ_OK;
+}

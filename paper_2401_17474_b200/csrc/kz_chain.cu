@@ -131,6 +131,7 @@ struct ChainMaxThreads {
 template <int EP, int R, int C>
 __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     const int D = a.stages;
     const int64_t ld = a.ld, q = a.q, bs = a.bs;

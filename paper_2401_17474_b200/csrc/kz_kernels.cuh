@@ -44,6 +44,12 @@ struct SolveArgs {
     long long* dbg;        // optional phase timestamps (KZ_PHASE_TIMING=1)
     int ablate;            // debug: bit mask of phases to skip (KZ_ABLATE), timing experiments only
     int box;               // rka kernel: TMA box width (columns of the row slice)
+    int* halt;             // optional: nonzero = the solve already stopped, the launch is a no-op
+                           // (device-side stop flag of the row-sharded driver, kz_solve_sharded);
+                           // the rka kernel raises it (stop iteration + 1) when its stop rule fires
+    unsigned tag_base;     // rka kernel: tags of this launch's tagged words are tag_base + 1 ...
+    const double* x_sum;   // rka kernel, optional: x_k = x_sum / x_div (the all-reduced worker sum of the
+    double x_div;          // previous row-sharded step) instead of x; x_k is written back to x
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
@@ -107,6 +113,10 @@ __global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __re
                                 double* __restrict__ out);
 __global__ void scale_copy_kernel(const double* __restrict__ S, double inv_div, int64_t n, double* __restrict__ x);
 __global__ void sum_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out);
+__global__ void shard_average_kernel(const double* __restrict__ S, double Q, int64_t n, int64_t ld,
+                                     const double* __restrict__ xref, double* __restrict__ x, double eps,
+                                     int use_stop, int64_t k_next, double* __restrict__ err_out,
+                                     int* __restrict__ halt);
 
 __global__ void gen_counter_kernel(double* __restrict__ A, int64_t m, int64_t n, int64_t ld, uint64_t seed,
                                    double mu_lo, double mu_hi, double sg_lo, double sg_hi, int64_t row0);

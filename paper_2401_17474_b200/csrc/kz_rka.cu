@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     constexpr int NR = LG / 4;  // rows per lane group per round (8 rows per warp per round)
     static_assert(LG == 8 || LG == 16 || LG == 32, "lane group");
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = a.stages;
     const int ld = (int)a.ld, q = (int)a.q;
@@ -177,7 +178,13 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     for (int e = 0; e < EPL; ++e) {
         const int j = 2 * (gl + LG * e);
         vld[e] = j < wdt;
-        xv[e] = vld[e] ? make_double2(__ldcg(a.x + c0 + j), __ldcg(a.x + c0 + j + 1)) : make_double2(0.0, 0.0);
+        if (!vld[e])
+            xv[e] = make_double2(0.0, 0.0);
+        else if (a.x_sum)  // row-sharded step: x_k from the all-reduced sum (kz_average_from's division)
+            xv[e] = make_double2(__ddiv_rn(__ldcg(a.x_sum + c0 + j), a.x_div),
+                                 __ddiv_rn(__ldcg(a.x_sum + c0 + j + 1), a.x_div));
+        else
+            xv[e] = make_double2(__ldcg(a.x + c0 + j), __ldcg(a.x + c0 + j + 1));
     }
 
     // reduced-row bookkeeping: after the transposed reduction lane gl holds row ri
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         if (warp >= NW - NOWN) {
             // NOWN owner warps: warp ow takes the worker pairs ow, ow + NOWN, ... of this CTA
             const int ow = warp - (NW - NOWN);
-            const unsigned tag = (unsigned)kk + 1u;
+            const unsigned tag = a.tag_base + (unsigned)kk + 1u;  // unique per launch: no reset of the words
             unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * q1 * 2;
             const int npair = (n_own + 1) / 2;
             const int my_pairs = npair > ow ? (npair - ow + NOWN - 1) / NOWN : 0;
@@ -591,7 +598,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         done = kk + 1;
     }
     if (tid == 0) *halt = 1;
-    if (!a.partial && warp == 0 && grp == 0) {
+    if (warp == 0 && grp == 0) {  // partial steps too: x_k (from x_sum) is the resident iterate
 #pragma unroll
         for (int e = 0; e < EPL; ++e)
             if (vld[e]) {
@@ -607,6 +614,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         a.status->converged = conv;
         a.status->checks = checks;
         a.status->err = err_last;
+        if (conv && a.halt != nullptr) *a.halt = (int)(a.k0 + done + 1);  // later launches become no-ops
     }
 }
 

@@ -269,6 +269,41 @@ __global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v,
     }
 }
 
+// Closing half of one row-sharded iteration on the device (distributed.py:296-301, solvers.py:137):
+// x = S / Q, then ||x - x_ref||^2 in exactly diff_sq_kernel + sum_kernel's order (so the native loop
+// and the host-driven one agree bitwise), written to *err_out.  In stop mode err < eps raises the halt
+// flag (halt = k_next + 1: x_{k_next} met the rule): every later launch of the stream that reads the
+// flag is a no-op, so x_{k_next} stands (_drive's check before iteration k, solvers.py:229-243).
+__global__ void __launch_bounds__(1024) shard_average_kernel(const double* __restrict__ S, double Q, int64_t n,
+                                                             int64_t ld, const double* __restrict__ xref,
+                                                             double* __restrict__ x, double eps, int use_stop,
+                                                             int64_t k_next, double* __restrict__ err_out,
+                                                             int* __restrict__ halt) {
+    if (*(volatile int*)halt != 0) return;  // stopped earlier: uniform over the block
+    __shared__ double part[32];
+    double s = 0.0;
+#pragma unroll 4
+    for (int64_t j = threadIdx.x; j < ld; j += blockDim.x) {
+        const double v = __ddiv_rn(S[j], Q);
+        x[j] = v;
+        if (j < n) {
+            const double d = __dsub_rn(v, xref[j]);
+            s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) {
+            *err_out = t;
+            if (use_stop && t < eps) *halt = (int)(k_next + 1);
+        }
+    }
+}
+
 // Cyclic Kaczmarz rows (solvers.py:286-287): idx[j] = (k0 + j) mod m.
 __global__ void cyclic_rows_kernel(int32_t* __restrict__ idx, int64_t k0, int64_t count, int64_t m) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x)

@@ -50,6 +50,7 @@ constexpr int MAXG = 10;          // clusters exchanging through tagged global w
 template <bool CLUSTER, int LPR>
 __global__ void __launch_bounds__(NT) sync_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = a.stages;
     const int ld = (int)a.ld, q = (int)a.q;

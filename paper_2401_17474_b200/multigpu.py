@@ -128,6 +128,64 @@ class CudaShard:
         self.ds.close()
 
 
+class ShardComm:
+    """The ranks' NCCL communicator for the native sharded loop (kz_comm_*): rank 0 draws
+    the unique id, torch.distributed broadcasts its bytes, every rank joins."""
+
+    def __init__(self, device: int, world: int, rank: int, group=None):
+        import ctypes as C
+
+        from . import _native as N
+
+        self._lib = N.load_library()
+        obj = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(N.COMM_ID_BYTES)
+            N.check(self._lib.kz_comm_unique_id(buf))
+            obj = [bytes(buf.raw)]
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.broadcast_object_list(obj, src=0, group=group)
+        h = C.c_void_p()
+        N.check(self._lib.kz_comm_create(int(device), obj[0], int(world), int(rank), C.byref(h)))
+        self.handle, self.world, self.rank = h, world, rank
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.kz_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_sharded_native(shard: "CudaShard", cfg, *, budget: int | None = None, comm: ShardComm | None = None
+                         ) -> RunReport:
+    """The same protocol as :func:`solve_sharded`, run by the library (kz_solve_sharded): the
+    local steps, NCCL all-reduces and averages of a chunk of outer iterations are enqueued on
+    one stream without a host round trip; a device stop flag freezes x at the stopping
+    iteration.  Bitwise the same x, errors and iteration counts as the host-driven loop."""
+    plan = shard.plan
+    if comm is None and plan.world > 1:
+        raise ValueError("a multi-rank sharded solve needs a ShardComm")
+    t0 = time.perf_counter()
+    r = shard.ds.solve_sharded(cfg, worker_offset=plan.worker_offset, comm=comm, budget=budget)
+    wall = time.perf_counter() - t0
+    shard.rows += r["rows"]
+    shard.kernel_ms += r["loop_ms"]
+    shard.kernel = r["kernel"]
+    return RunReport(variant=cfg.variant, q=plan.q_total, block_size=cfg.block_size if cfg.variant == "rkab" else 1,
+                     alpha_policy=cfg.alpha_policy, alpha=1.0, seed=cfg.base_seed, iterations=r["iterations"],
+                     converged=r["converged"], wall_time_s=wall, final_error_sq=r["final_error_sq"],
+                     final_residual=float("nan"), error_evals=r["error_evals"], x=r["x"],
+                     gpu={"world": plan.world, "q_local": plan.q_local, "shard": (plan.lo, plan.hi),
+                          "native": True, "loop_ms": r["loop_ms"], "launches": r["launches"]})
+
+
 def solve_sharded(shard, cfg, *, budget: int | None = None, group=None) -> RunReport:
     """The _drive protocol (solvers.py:182-263) over row shards with one
     all-reduce-sum per outer iteration.  ``shard`` provides reset/step/finish/x

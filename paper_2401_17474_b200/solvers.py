@@ -269,6 +269,39 @@ class DeviceSystem:
         return {"kernel_ms": float(r.kernel_ms), "loop_ms": float(r.loop_ms), "rows": int(r.rows_projected),
                 "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches)}
 
+    def solve_sharded(self, cfg: "SolverConfig", *, worker_offset: int, comm=None, budget: int | None = None,
+                      alphas=None) -> dict:
+        """The whole row-sharded _drive loop of this shard natively (kz_solve_sharded): per outer
+        iteration the local step, an in-place all-reduce of the worker sum over ``comm`` (a
+        :class:`ShardComm`; None = one rank) and x = S / (q * world) with the stop rule on the
+        device.  Worker ranges come from :meth:`set_ranges`."""
+        variant = cfg.variant
+        if variant not in ("rka", "rkab"):
+            raise ValueError(f"row-sharded solves run rka or rkab, not {variant!r}")
+        al = N.f64(np.ones(cfg.q) if alphas is None else alphas)
+        p = N.Params()
+        p.variant = N.VARIANT_IDS[variant]
+        p.scheme = N.SCHEME_IDS["ranges"]
+        p.q = cfg.q
+        p.block_size = cfg.block_size if variant == "rkab" else 1
+        p.alphas_host = N.ptr(al)
+        p.base_seed = int(cfg.base_seed)
+        p.epsilon = float(cfg.epsilon)
+        p.max_iterations = int(cfg.max_iterations)
+        p.budget = 0 if budget is None else int(budget)
+        p.kernel = N.KERNELS[cfg.kernel]
+        p.threads, p.ctas = int(cfg.threads), int(cfg.ctas)
+        p.worker_offset = int(worker_offset)
+        r = N.Result()
+        x = np.empty(self.n, dtype=np.float64)
+        N.check(self._lib.kz_solve_sharded(self.handle, None if comm is None else comm.handle, C.byref(p),
+                                           C.byref(r), N.ptr(x), None))
+        return {"iterations": int(r.iterations), "converged": bool(r.converged),
+                "final_error_sq": float(r.final_error_sq), "error_evals": int(r.error_evals), "x": x,
+                "rows": int(r.rows_projected), "loop_ms": float(r.loop_ms),
+                "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches),
+                "ctas": int(r.ctas), "threads": int(r.threads)}
+
     def set_x(self, x=None) -> None:
         """Overwrite the resident iterate (None = zeros)."""
         xv = None if x is None else N.f64(x)

@@ -79,3 +79,79 @@ def test_counter_shard_is_exact_row_slice(gpu):
         part.generate_counter(7, row0=1500)
         A2, b2, xr2 = part.download()
     assert np.array_equal(A2, A[1500:2500]) and np.array_equal(b2, b[1500:2500]) and np.array_equal(xr2, xr)
+
+
+def _native_vs_host(s, variant, q, bs, seed, budget=None, comm=None, kernel="auto"):
+    from paper_2401_17474_b200 import SolverConfig
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded, solve_sharded_native
+
+    plan = plan_shards(s.m, 1, 0, q)
+    shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
+    cfg = SolverConfig(variant=variant, q=q, block_size=bs, base_seed=seed, sampling_scheme="distributed",
+                       kernel=kernel)
+    rn = solve_sharded_native(shard, cfg, budget=budget, comm=comm)
+    rh = solve_sharded(shard, cfg, budget=budget)
+    rn2 = solve_sharded_native(shard, cfg, budget=budget, comm=comm)  # a second solve on the same shard
+    shard.close()
+    return rn, rh, rn2
+
+
+@pytest.mark.parametrize("variant,q,bs", [("rka", 8, 1), ("rkab", 4, 6)])
+def test_native_sharded_loop_world1(gpu, oracle, variant, q, bs):
+    """kz_solve_sharded (device stop flag, one host sync per chunk) against the host-driven
+    loop (bitwise: same kernels, same collective, same average) and the oracle."""
+    s = _system()
+    rn, rh, rn2 = _native_vs_host(s, variant, q, bs, seed=2)
+    o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=q, block_size=bs, base_seed=2, scheme="distributed")
+    for r in (rn, rn2):
+        assert r.converged and r.iterations == rh.iterations == o["iterations"]
+        assert r.error_evals == rh.error_evals == o["error_evals"]
+        # the rka step kernel checks x_k with its own (cluster-tree) error sum: same value to rounding
+        assert abs(r.final_error_sq - rh.final_error_sq) <= 1e-12 * rh.final_error_sq
+        assert np.array_equal(r.x, rh.x)
+    assert rel_err(rn.x, o["x"]) <= PARITY_TOL
+
+
+def test_native_sharded_budget_multi_cluster(gpu, oracle):
+    """Budget mode on rows wide enough for several rka clusters (tagged-word exchange with
+    per-launch tag ranges, one launch per outer iteration)."""
+    from paper_2401_17474_b200 import GeneratorConfig, generate_mother
+
+    s = generate_mother(GeneratorConfig(m_max=5000, n_max=4500, seed=3))
+    rn, rh, rn2 = _native_vs_host(s, "rka", 16, 1, seed=4, budget=37)
+    assert rn.iterations == rh.iterations == 37 and rn.error_evals == 0
+    assert np.array_equal(rn.x, rh.x) and np.array_equal(rn2.x, rh.x)
+    o = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=16, base_seed=4, scheme="distributed", budget=37)
+    assert rel_err(rn.x, o["x"]) <= PARITY_TOL
+
+
+def test_native_sharded_max_iterations(gpu, oracle):
+    """Stop mode that runs out of iterations: not converged, evals = max + 1."""
+    from paper_2401_17474_b200 import SolverConfig
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded, solve_sharded_native
+
+    s = _system()
+    plan = plan_shards(s.m, 1, 0, 8)
+    shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
+    cfg = SolverConfig(variant="rka", q=8, base_seed=1, sampling_scheme="distributed", max_iterations=150)
+    rn = solve_sharded_native(shard, cfg)
+    rh = solve_sharded(shard, cfg)
+    shard.close()
+    assert not rn.converged and rn.iterations == rh.iterations == 150
+    assert rn.error_evals == rh.error_evals == 151
+    assert np.array_equal(rn.x, rh.x)
+
+
+def test_native_sharded_nccl_world1(gpu):
+    """The NCCL communicator path (kz_comm_*, in-place all-reduce on the solve stream) with one
+    rank: bitwise the same as the collective-free loop."""
+    from paper_2401_17474_b200.multigpu import ShardComm
+
+    s = _system()
+    comm = ShardComm(0, 1, 0)
+    try:
+        rn, rh, _ = _native_vs_host(s, "rka", 8, 1, seed=5, comm=comm)
+    finally:
+        comm.close()
+    assert rn.converged and rn.iterations == rh.iterations
+    assert np.array_equal(rn.x, rh.x)
