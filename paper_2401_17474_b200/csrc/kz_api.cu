@@ -663,6 +663,8 @@ struct Plan {
     int cluster = 1;    // sync (cluster mode): CTAs per thread-block cluster
     bool tma = false;   // sync: the TMA-gather rka kernel
     int lg = 32, epl = 1, box = 0;  // rka kernel: lanes per row group, pairs per lane, TMA box width
+    bool sr = false;    // rka kernel: single round of 8 rows per warp (<= 64 workers per cluster)
+    bool wg = false;    // rka kernel: worker groups (cluster g runs q/G workers over all columns)
     size_t smem = 0;
 };
 
@@ -872,25 +874,26 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
 
 namespace {
 
-template <bool TM, bool SR>
+template <bool TM, bool SR, bool WG>
 void* rka_fn_t(int lg, int epl) {
-    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM, SR> : (void*)rka_kernel<8, 1, TM, SR>;
-    if (lg == 16) return (void*)rka_kernel<16, 1, TM, SR>;
+    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM, SR, WG> : (void*)rka_kernel<8, 1, TM, SR, WG>;
+    if (lg == 16) return (void*)rka_kernel<16, 1, TM, SR, WG>;
     switch (epl) {
-        case 1: return (void*)rka_kernel<32, 1, TM, SR>;
-        case 2: return (void*)rka_kernel<32, 2, TM, SR>;
-        case 3: return (void*)rka_kernel<32, 3, TM, SR>;
-        case 4: return (void*)rka_kernel<32, 4, TM, SR>;
+        case 1: return (void*)rka_kernel<32, 1, TM, SR, WG>;
+        case 2: return (void*)rka_kernel<32, 2, TM, SR, WG>;
+        case 3: return (void*)rka_kernel<32, 3, TM, SR, WG>;
+        case 4: return (void*)rka_kernel<32, 4, TM, SR, WG>;
         default: return nullptr;
     }
 }
 
-// the timing variant (per-phase clock stamps) only under KZ_PHASE_TIMING; SR = one
-// round of 8 rows per warp (q <= 64)
-void* rka_fn(int lg, int epl, bool sr) {
+// the timing variant (per-phase clock stamps) only under KZ_PHASE_TIMING (column-sliced plans);
+// SR = one round of 8 rows per warp (<= 64 workers per cluster); WG = worker groups
+void* rka_fn(int lg, int epl, bool sr, bool wg = false) {
+    if (wg) return sr ? rka_fn_t<false, true, true>(lg, epl) : rka_fn_t<false, false, true>(lg, epl);
     const bool tm = getenv("KZ_PHASE_TIMING") != nullptr;
-    if (tm) return sr ? rka_fn_t<true, true>(lg, epl) : rka_fn_t<true, false>(lg, epl);
-    return sr ? rka_fn_t<false, true>(lg, epl) : rka_fn_t<false, false>(lg, epl);
+    if (tm) return sr ? rka_fn_t<true, true, false>(lg, epl) : rka_fn_t<true, false, false>(lg, epl);
+    return sr ? rka_fn_t<false, true, false>(lg, epl) : rka_fn_t<false, false, false>(lg, epl);
 }
 
 size_t rka_smem(int64_t q, int box, int stages, int Pc) {
@@ -957,10 +960,88 @@ static int ensure_tmaps(kz_system* s, int box) {
 
 // rka kernel plan: G clusters of Pc CTAs; every CTA's slice <= 256 columns (one
 // TMA box) and at least two ring stages.
+// Worker-group plan (q > 64, rows narrow enough for one cluster's 16 TMA boxes):
+// G clusters of 16 CTAs, cluster g runs workers [g q/G, (g+1) q/G) over all
+// columns, so each CTA gathers ~q/G row slices per iteration instead of q
+// (the column-sliced plan needs G x 16 slices of ~n/(16 G) columns and is
+// bound by the TMA unit's per-gather cost); the clusters add their column sums
+// through tagged words once per iteration.
+static int plan_rka_wg(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
+    const int64_t ld = s->ld;
+    const int Pc = 16;
+    const int64_t cw = (((ld + Pc - 1) / Pc) + 1) & ~(int64_t)1;
+    const int box = (int)((cw + 3) & ~(int64_t)3);
+    if (box > 256) return fail(KZ_EINVAL, "rows too wide for worker groups");
+    const int npairs = box / 2;
+    const int lg = npairs <= 8 ? 8 : (npairs <= 16 ? 16 : 32);
+    const int epl = lg == 32 ? (npairs + 31) / 32 : 1;
+    int G = (int)std::min<int64_t>(RKA_MAXG, (q + 8 * RKA_NW - 1) / (8 * RKA_NW));
+    if (const char* e = getenv("KZ_RKA_WG_G")) G = std::max(2, std::min(RKA_MAXG, atoi(e)));
+    for (int guard = 0; guard < 16 && G >= 2; ++guard) {
+        const int64_t qmax = (q + G - 1) / G;
+        const size_t stage = rka_smem(qmax, box, 1, Pc) - rka_smem(qmax, box, 0, Pc);
+        const size_t fixed = rka_smem(qmax, box, 0, Pc);
+        int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);
+        if (const char* e = getenv("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+        if (stages < 2 || rka_smem(qmax, box, stages, Pc) > kSmemLimit) {
+            ++G;  // fewer workers per cluster
+            if (G > RKA_MAXG) break;
+            continue;
+        }
+        const bool sr = qmax <= 8 * RKA_NW;
+        void* fn = rka_fn(lg, epl, sr, true);
+        if (!fn) return fail(KZ_EINVAL, "no rka kernel for LG=%d EPL=%d", lg, epl);
+        const size_t smem = rka_smem(qmax, box, stages, Pc);
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(Pc * G);
+        cfg.blockDim = dim3(RKA_NT);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = Pc;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+        if (e != cudaSuccess || nclusters < 2) {
+            cudaGetLastError();
+            return fail(KZ_EINVAL, "worker groups not schedulable");
+        }
+        if (nclusters < G) {  // every cluster must be co-resident (they poll each other)
+            G = nclusters;
+            continue;
+        }
+        pl.kernel = KZ_KERNEL_SYNC_CLUSTER;
+        pl.tma = true;
+        pl.sr = sr;
+        pl.wg = true;
+        pl.threads = RKA_NT;
+        pl.ctas = Pc * G;
+        pl.cluster = Pc;
+        pl.stages = stages;
+        pl.smem = smem;
+        pl.lg = lg;
+        pl.epl = epl;
+        pl.box = box;
+        return KZ_OK;
+    }
+    return fail(KZ_EINVAL, "no feasible worker-group plan for q=%lld n=%lld", (long long)q, (long long)s->n);
+}
+
 static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     if (getenv("KZ_SYNC_V5")) return fail(KZ_EINVAL, "rka kernel disabled (KZ_SYNC_V5)");
     if (q > 512) return fail(KZ_EINVAL, "q=%lld exceeds the rka kernel's 512 workers", (long long)q);
     const int64_t ld = s->ld;
+    {
+        const char* e = getenv("KZ_RKA_WG");
+        const bool want = e ? atoi(e) != 0 : true;
+        if (want && q > 8 * RKA_NW && p->ctas == 0 && p->partial_dev == nullptr && plan_rka_wg(s, p, q, pl) == KZ_OK)
+            return KZ_OK;
+    }
     int Pc = 16, G = 1;
     if (p->ctas > 16) {
         G = p->ctas / 16;
@@ -1000,6 +1081,8 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
             continue;
         }
         void* fn = rka_fn(lg, epl, q <= 8 * RKA_NW);
+        pl.sr = q <= 8 * RKA_NW;
+        pl.wg = false;
         if (!fn) return fail(KZ_EINVAL, "no rka kernel for LG=%d EPL=%d", lg, epl);
         const size_t smem = rka_smem(q, box, stages, Pc);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1072,7 +1155,7 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
         cfg.attrs = attr2;
         cfg.numAttrs = na;
     } else if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER) {
-        fn = pl.tma ? rka_fn(pl.lg, pl.epl, args.q <= 8 * RKA_NW) : sync_fn(true, pl.lpr);
+        fn = pl.tma ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg) : sync_fn(true, pl.lpr);
         int na = 0;
         attr2[na].id = cudaLaunchAttributeClusterDimension;
         attr2[na].val.clusterDim.x = pl.cluster;
@@ -1185,7 +1268,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         // the dynamic shared-memory limit is a property of the kernel function, which another
         // system may have lowered since: restore it for this plan
         void* fn = pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair)
-                   : pl.tma                     ? rka_fn(pl.lg, pl.epl, q <= 8 * RKA_NW)
+                   : pl.tma                     ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg)
                                                 : sync_fn(pl.kernel == KZ_KERNEL_SYNC_CLUSTER, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     } else if (kern == KZ_KERNEL_CHAIN) {
@@ -1218,7 +1301,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     if (pl.tma && pl.ctas > pl.cluster) {
         // tagged words of the rka kernel's cluster exchange: a buffer of their own, zeroed once;
         // every launch draws a fresh tag range (tag_base), so stale words never match
-        const size_t words = 4 * (size_t)(pl.ctas / pl.cluster) * (q + 1);
+        const size_t words = 4 * (size_t)(pl.ctas / pl.cluster) * (pl.wg ? (size_t)s->ld : (size_t)(q + 1));
         if (s->ll.cap < words) {
             KZ_TRY(s->ll.ensure(words));
             KZ_CUDA(cudaMemsetAsync(s->ll.p, 0, s->ll.cap * sizeof(unsigned long long), st));
@@ -1254,6 +1337,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     args.use_stop = stop_mode ? 1 : 0;
     args.stages = pl.stages;
     args.box = pl.box;
+    args.wg = pl.wg ? 1 : 0;
     if (pl.tma) KZ_TRY(ensure_tmaps(s, pl.box));
     const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
     args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;
@@ -2004,8 +2088,8 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     const int world = comm ? comm->world : 1;
     cudaStream_t st = (cudaStream_t)stream;
     KZ_CUDA(cudaSetDevice(s->device));
-    KZ_TRY(s->S.ensure(s->ld));
-    KZ_CUDA(cudaMemsetAsync(s->S.p, 0, s->ld * sizeof(double), st));  // the padded tail stays zero
+    KZ_TRY(s->S.ensure(2 * s->ld));  // two worker-sum buffers: step k writes S[k % 2], reads S[(k - 1) % 2]
+    KZ_CUDA(cudaMemsetAsync(s->S.p, 0, 2 * s->ld * sizeof(double), st));  // the padded tails stay zero
     kz_params pp = *p;
     pp.partial_dev = s->S.p;
     SolveCtx cx;
@@ -2055,24 +2139,26 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
         else
             KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, (p->k_start + k) * bs, count, idx0, 1, q, st));
         for (int64_t i = 0; i < c; ++i) {
-            args.k0 = k + i;
+            const int64_t kk = k + i;
+            double* Sk = s->S.p + (kk & 1) * s->ld;
+            args.k0 = kk;
             args.idx = chain ? idx0 + i * bs : idx0 + i * q;
             args.idx_stride = chain ? count : q;
-            if (fused) args.x_sum = (k + i == 0) ? nullptr : s->S.p;  // x_0 is the resident iterate
-            KZ_TRY(launch_step(s, &pp, r, cx, k + i == 0, st));
-            if (comm)
-                KZ_NCCL(g_nccl.all_reduce(s->S.p, s->S.p, (size_t)s->ld, ncclFloat64, ncclSum, comm->nccl, st));
+            args.partial = Sk;
+            if (fused) args.x_sum = kk == 0 ? nullptr : s->S.p + ((kk - 1) & 1) * s->ld;  // x_0: resident
+            KZ_TRY(launch_step(s, &pp, r, cx, kk == 0, st));
+            if (comm) KZ_NCCL(g_nccl.all_reduce(Sk, Sk, (size_t)s->ld, ncclFloat64, ncclSum, comm->nccl, st));
             if (!fused) {
-                shard_average_kernel<<<1, 1024, 0, st>>>(s->S.p, (double)Q, s->n, s->ld, s->xref.p, s->x.p,
-                                                         p->epsilon, stop_mode ? 1 : 0, k + i + 1, s->errs.p + i,
-                                                         s->halt.p);
+                shard_average_kernel<<<1, 1024, 0, st>>>(Sk, (double)Q, s->n, s->ld, s->xref.p, s->x.p, p->epsilon,
+                                                         stop_mode ? 1 : 0, kk + 1, s->errs.p + i, s->halt.p);
                 KZ_TRY(check_launch("shard_average_kernel"));
             }
         }
         const bool last_chunk = k + c >= limit;
         if (fused && last_chunk) {  // x_K = S / Q and the check before iteration K
-            shard_average_kernel<<<1, 1024, 0, st>>>(s->S.p, (double)Q, s->n, s->ld, s->xref.p, s->x.p, p->epsilon,
-                                                     stop_mode ? 1 : 0, k + c, s->errs.p + c - 1, s->halt.p);
+            shard_average_kernel<<<1, 1024, 0, st>>>(s->S.p + ((k + c - 1) & 1) * s->ld, (double)Q, s->n, s->ld,
+                                                     s->xref.p, s->x.p, p->epsilon, stop_mode ? 1 : 0, k + c,
+                                                     s->errs.p + c - 1, s->halt.p);
             KZ_TRY(check_launch("shard_average_kernel"));
         }
         // one host synchronisation per chunk: the errors, the stop flag and the kernel status
@@ -2086,6 +2172,14 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
             const int64_t ks = hhalt - 1;
             // the stopping kernel's own error total, or the average kernel's
             err = (fused && ks < k + c) ? s->h_status->err : herr[ks - k - 1];
+            if (fused && ks < k + c && ks > 0) {
+                // the stopping step kernel left x alone: x_ks = S[(ks - 1) % 2] / Q (intact -- that
+                // kernel wrote S[ks % 2]); no stop check, no flag
+                shard_average_kernel<<<1, 1024, 0, st>>>(s->S.p + ((ks - 1) & 1) * s->ld, (double)Q, s->n, s->ld,
+                                                         s->xref.p, s->x.p, p->epsilon, 0, ks, s->errs.p + chunk_max,
+                                                         nullptr);
+                KZ_TRY(check_launch("shard_average_kernel"));
+            }
             k = ks;
             evals = k + 1;
             converged = true;

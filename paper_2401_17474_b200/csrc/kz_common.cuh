@@ -245,6 +245,40 @@ __device__ __noinline__ double ll_sum(const unsigned long long* p, int stride, i
     return s;
 }
 
+// inlined twin (no call ABI around it: the rka kernel's combine phase keeps many live registers)
+template <int GMAX>
+__device__ __forceinline__ double ll_sum_inl(const unsigned long long* p, int stride, int G, unsigned tag, int* abort) {
+    unsigned long long w0[GMAX], w1[GMAX];
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g)
+        if (g < G) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+    unsigned spins = 0;
+    for (;;) {
+        bool all = true;
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g)
+            if (g < G && !ll_ok(w0[g], w1[g], tag)) all = false;
+        if (all) break;
+        ++spins;
+        if ((spins & 1023u) == 0 && *(volatile int*)abort) break;
+        if (spins > (1u << 22)) {
+            atomicExch(abort, 1);
+            break;
+        }
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g)
+            if (g < G && !ll_ok(w0[g], w1[g], tag)) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g)
+        if (g < G) {
+            const double v = ll_value(w0[g], w1[g]);
+            s = (g == 0) ? v : __dadd_rn(s, v);
+        }
+    return s;
+}
+
 __device__ __forceinline__ unsigned cluster_rank() {
     unsigned r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));

@@ -49,7 +49,8 @@ struct SolveArgs {
                            // the rka kernel raises it (stop iteration + 1) when its stop rule fires
     unsigned tag_base;     // rka kernel: tags of this launch's tagged words are tag_base + 1 ...
     const double* x_sum;   // rka kernel, optional: x_k = x_sum / x_div (the all-reduced worker sum of the
-    double x_div;          // previous row-sharded step) instead of x; x_k is written back to x
+    double x_div;          // previous row-sharded step) instead of x
+    int wg;                // rka kernel: worker-group mode (cluster g runs workers [g q/G, (g+1) q/G))
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
@@ -67,7 +68,7 @@ __global__ void sync_kernel(SolveArgs a);
 constexpr int RKA_NW = 8;                  // compute warps
 constexpr int RKA_NT = (RKA_NW + 1) * 32;  // + the producer warp
 constexpr int RKA_MAXG = 10;               // clusters exchanging through tagged words
-template <int LG, int EPL, bool TIMING, bool SR>
+template <int LG, int EPL, bool TIMING, bool SR, bool WG>
 __global__ void rka_kernel(const __grid_constant__ SolveArgs a, const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB);
 

@@ -43,10 +43,12 @@ namespace kz {
 
 namespace {
 constexpr int NW = RKA_NW;
+
+constexpr unsigned XBAR = 2;  // named barrier: producer warp -> compute warps, x_k in place
 constexpr unsigned CBAR = 1;  // named barrier id of the compute warps
 }  // namespace
 
-template <int LG, int EPL, bool TIMING, bool SR>
+template <int LG, int EPL, bool TIMING, bool SR, bool WG>
 __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ SolveArgs a,
                                                         const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB) {
@@ -56,12 +58,21 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = a.stages;
-    const int ld = (int)a.ld, q = (int)a.q;
+    const int ld = (int)a.ld, qa = (int)a.q;
     const int P = (int)gridDim.x, c = (int)blockIdx.x;
     const int Pc = (int)cluster_size(), cr = (int)cluster_rank();
     const int G = P / Pc, gid = c / Pc;
-    const int cw = (((ld + P - 1) / P) + 1) & ~1;
-    const int c0 = c * cw < ld ? c * cw : ld;
+    // worker-group mode (a.wg): cluster g runs workers [wlo, wlo + q) over all columns (split over its
+    // Pc CTAs) and the clusters add their per-column sums through tagged words; otherwise every
+    // cluster runs all workers over its share of the columns and the clusters add dot totals
+    constexpr bool wg = WG;  // a separate instantiation: the column-sliced kernel keeps its register budget
+    const int Gx = wg ? 1 : G;                      // clusters exchanging dot totals
+    const int gx = wg ? 0 : gid;
+    const int wlo = wg ? (int)((int64_t)gid * qa / G) : 0;
+    const int q = wg ? (int)((int64_t)(gid + 1) * qa / G) - wlo : qa;  // this cluster's workers
+    const int PC = wg ? Pc : P, cc = wg ? cr : c;   // CTAs splitting the columns, this CTA's slice
+    const int cw = (((ld + PC - 1) / PC) + 1) & ~1;
+    const int c0 = cc * cw < ld ? cc * cw : ld;
     const int wdt = (c0 + cw < ld ? c0 + cw : ld) - c0;  // even
     const int cwb = a.box;                               // >= cw, multiple of 4
     const int q4 = (q + 3) & ~3;
@@ -110,12 +121,15 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         *halt = 0;
         fence_mbarrier_init_cluster();
     }
-    for (int t = tid; t < q; t += RKA_NT) alp[t] = a.alphas[t];
+    for (int t = tid; t < q; t += RKA_NT) alp[t] = a.alphas[wlo + t];
     __syncthreads();
     cluster_sync_all();  // peers' mbarriers exist before anyone pushes
 
     if (warp == NW) {
         // ================= producer warp =================
+        if (a.x_sum)  // row-sharded step: x_k = the all-reduced worker sum / Q (kz_average_from's division)
+            for (int j = lane; j < wdt; j += 32) a.x[c0 + j] = __ddiv_rn(__ldcg(a.x_sum + c0 + j), a.x_div);
+        named_sync(XBAR, RKA_NT);
         const int ng = q4 / 4, nbg = (n_own + 3) / 4;
         const unsigned bytes = rows_bytes + (unsigned)nbg * 128u;
         const unsigned ring_u = smem_u32(ring);
@@ -131,7 +145,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             }
             if (*halt) break;
             const unsigned dst = ring_u + (unsigned)(s * stage_bytes);
-            const int32_t* ix = a.idx + it * q;
+            const int32_t* ix = a.idx + it * qa + wlo;
             if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
             __syncwarp();
             const unsigned fb = smem_u32(&full[s]);
@@ -172,19 +186,14 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int gl = lane % LG, grp = lane / LG;
     double2 xv[EPL];
     for (int j = tid; j < cwb; j += NW * 32) xrs[j] = j < wdt ? a.xref[c0 + j] : 0.0;
+    named_sync(XBAR, RKA_NT);  // the producer warp formed x_k = x_sum / Q (row-sharded step)
     named_sync(CBAR, NW * 32);
     bool vld[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
         const int j = 2 * (gl + LG * e);
         vld[e] = j < wdt;
-        if (!vld[e])
-            xv[e] = make_double2(0.0, 0.0);
-        else if (a.x_sum)  // row-sharded step: x_k from the all-reduced sum (kz_average_from's division)
-            xv[e] = make_double2(__ddiv_rn(__ldcg(a.x_sum + c0 + j), a.x_div),
-                                 __ddiv_rn(__ldcg(a.x_sum + c0 + j + 1), a.x_div));
-        else
-            xv[e] = make_double2(__ldcg(a.x + c0 + j), __ldcg(a.x + c0 + j + 1));
+        xv[e] = vld[e] ? make_double2(__ldcg(a.x + c0 + j), __ldcg(a.x + c0 + j + 1)) : make_double2(0.0, 0.0);
     }
 
     // reduced-row bookkeeping: after the transposed reduction lane gl holds row ri
@@ -202,16 +211,16 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int we = wb + QB < q ? wb + QB : q;
     const int eown = Pc - 1;                                          // owner of the error total
     const bool gh = we - wb > grp * NR;  // this lane group owns at least one worker
-    const bool qpow2 = (q & (q - 1)) == 0;
-    const double invq = 1.0 / (double)q;  // RN(1/q): exact for powers of two, Markstein otherwise
-    const double qd = (double)q;
+    const bool qpow2 = (qa & (qa - 1)) == 0;  // x = (sum over all qa workers) / qa
+    const double invq = 1.0 / (double)qa;     // RN(1/qa): exact for powers of two, Markstein otherwise
+    const double qd = (double)qa;
     const bool ckpt_on = a.ckpt_every > 0;
     const int count = (int)a.count;
     const bool use_stop = opaque_i32(a.use_stop) != 0, final_check = opaque_i32(a.final_check) != 0;
     const int cnt2 = Pc >= 2 ? Pc / 2 : 1;  // partials per lane in the owner's tree (2 lanes per item)
     bool unit_alpha = true;
     for (int t = 0; t < q; ++t) unit_alpha = unit_alpha && alp[t] == 1.0;
-    const bool split = TIMING && (a.ablate & 16) ? true : (cwb >= 64 || LG == 8);  // combine layout (see below)
+    const bool split = wg || (TIMING && (a.ablate & 16)) || cwb >= 64 || LG == 8;  // combine layout (see below)
     const int ppw = ((wdt >> 1) + NW - 1) / NW;                      // column pairs per warp (split)
     const int u = lane & 1;
 
@@ -367,7 +376,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             // NOWN owner warps: warp ow takes the worker pairs ow, ow + NOWN, ... of this CTA
             const int ow = warp - (NW - NOWN);
             const unsigned tag = a.tag_base + (unsigned)kk + 1u;  // unique per launch: no reset of the words
-            unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * q1 * 2;
+            unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * Gx * q1 * 2;
             const int npair = (n_own + 1) / 2;
             const int my_pairs = npair > ow ? (npair - ow + NOWN - 1) / NOWN : 0;
             if (!last && my_pairs > 0) {
@@ -382,10 +391,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     double tot = owner_total(ib + i, RPO, live);
                     if (TIMING && rec && warp == NW - NOWN && l0 == 0)
                         a.dbg[(kk * 8 + warp) * 16 + 10] = clock64() + (long long)(tot * 0.0);
-                    if (G > 1 && u == 0 && live) {
+                    if (Gx > 1 && u == 0 && live) {
                         // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
-                        ll_store(ll + ((size_t)gid * q1 + t) * 2, tot, tag);
-                        tot = ll_sum<RKA_MAXG>(ll + 2 * t, 2 * q1, G, tag, &a.status->aborted);
+                        ll_store(ll + ((size_t)gx * q1 + t) * 2, tot, tag);
+                        tot = ll_sum<RKA_MAXG>(ll + 2 * t, 2 * q1, Gx, tag, &a.status->aborted);
                     }
                     if (live && u == 0) {
                         const double* rec4 = bsr + 4 * i;  // (b, sq, 1/sq, 0) of owned worker i
@@ -417,9 +426,9 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 mbar_wait(&ebin[par], bpar);
                 if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 10] = clock64();
                 double tot = owner_total(ein + par * Pc, 1, lane < 2);
-                if (G > 1 && lane == 0) {
-                    ll_store(ll + ((size_t)gid * q1 + q) * 2, tot, tag);
-                    tot = ll_sum<RKA_MAXG>(ll + 2 * q, 2 * q1, G, tag, &a.status->aborted);
+                if (Gx > 1 && lane == 0) {
+                    ll_store(ll + ((size_t)gx * q1 + q) * 2, tot, tag);
+                    tot = ll_sum<RKA_MAXG>(ll + 2 * q, 2 * q1, Gx, tag, &a.status->aborted);
                 }
                 tot = __shfl_sync(0xffffffffu, tot, 0);
                 if (lane < Pc)
@@ -537,6 +546,15 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             for (int pp = warp * ppw + lane; pp < (warp + 1) * ppw && pp < np; pp += 32) {
                 const int j = 2 * pp;
                 const double2 v = combine_pair(j);
+                if (wg && G > 1) {
+                    // this cluster's column sums -> tagged words [par][cluster][column] (summed below)
+                    unsigned long long* wl =
+                        reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * ld * 2;
+                    const unsigned tag = a.tag_base + (unsigned)kk + 1u;
+                    ll_store(wl + ((size_t)gid * ld + c0 + j) * 2, v.x, tag);
+                    ll_store(wl + ((size_t)gid * ld + c0 + j + 1) * 2, v.y, tag);
+                    continue;
+                }
                 if (a.partial) {  // row-sharded step: un-normalised local sum
                     __stcg(a.partial + c0 + j, v.x);
                     __stcg(a.partial + c0 + j + 1, v.y);
@@ -548,6 +566,17 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     if (c0 + j < a.n) a.ckpt[ck_slot * a.n + c0 + j] = x2.x;
                     if (c0 + j + 1 < a.n) a.ckpt[ck_slot * a.n + c0 + j + 1] = x2.y;
                 }
+            }
+            if (wg && G > 1 && tid < wdt) {
+                // worker groups: thread j adds the G clusters' sums of column c0 + j in cluster order
+                // (every cluster forms the same x bit for bit)
+                const unsigned long long* wl =
+                    reinterpret_cast<const unsigned long long*>(a.part) + (size_t)par * G * ld * 2;
+                const double tot = ll_sum_inl<RKA_MAXG>(wl + (size_t)(c0 + tid) * 2, 2 * ld, G,
+                                                        a.tag_base + (unsigned)kk + 1u, &a.status->aborted);
+                const double xj = qpow2 ? __dmul_rn(tot, invq) : div_rn_fast(tot, qd, invq);
+                xs[tid] = xj;
+                if (ck && gid == 0 && c0 + tid < a.n) a.ckpt[ck_slot * a.n + c0 + tid] = xj;
             }
             named_sync(CBAR, NW * 32);
             if (!a.partial) {
@@ -598,7 +627,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         done = kk + 1;
     }
     if (tid == 0) *halt = 1;
-    if (warp == 0 && grp == 0) {  // partial steps too: x_k (from x_sum) is the resident iterate
+    if (!a.partial && warp == 0 && grp == 0 && (!wg || gid == 0)) {
 #pragma unroll
         for (int e = 0; e < EPL; ++e)
             if (vld[e]) {
@@ -618,61 +647,89 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     }
 }
 
-template __global__ void rka_kernel<8, 1, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, true, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, true, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, true, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, true, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, true, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, true, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, true, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, true, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, false, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, true, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, true, false, false>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, true, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 2, false, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 2, false, true, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, true, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, true, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, true, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, true, false, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, true, true, false>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, false, true>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, true, true>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
 
 }  // namespace kz

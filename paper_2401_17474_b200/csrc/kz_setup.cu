@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(1024) shard_average_kernel(const double* __res
                                                              double* __restrict__ x, double eps, int use_stop,
                                                              int64_t k_next, double* __restrict__ err_out,
                                                              int* __restrict__ halt) {
-    if (*(volatile int*)halt != 0) return;  // stopped earlier: uniform over the block
+    if (halt != nullptr && *(volatile int*)halt != 0) return;  // stopped earlier: uniform over the block
     __shared__ double part[32];
     double s = 0.0;
 #pragma unroll 4
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(1024) shard_average_kernel(const double* __res
         t = warp_sum(t);
         if (threadIdx.x == 0) {
             *err_out = t;
-            if (use_stop && t < eps) *halt = (int)(k_next + 1);
+            if (use_stop && halt != nullptr && t < eps) *halt = (int)(k_next + 1);
         }
     }
 }
