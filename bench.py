@@ -172,77 +172,6 @@ def cpu_baseline(name, system, kw, budget_s=12.0):
             "sample": f"{seeds} full solves to eps (seeds 0..{seeds - 1}) of {name}, oracle/kz_oracle.c pthreads"}
 
 
-def run_b200_sharded(args, name, rank, world, local_rank):
-    """N > 1, headline: the workload's 10 seed-solves are independent objects, so the ranks
-    split them (seed-parallel weak scaling, no data-path collective): each GPU solves
-    `steps` seeds of the resident c1 system; value = all rows / max-over-ranks time.
-    Extras: the row-sharded path itself (BASELINE config 3: 160000 x 20000 counter-keyed,
-    rows split over the GPUs, q = 64 workers per GPU, one NCCL all-reduce of the worker
-    sums per outer iteration -- multigpu.solve_sharded) for RKAB bs = 1000 and RKA."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver
-    from paper_2401_17474_b200 import _native as N
-
-    torch.cuda.set_device(local_rank)
-    system, kw = build_system(name)
-    m, n = system.A.shape
-    cfg = SolverConfig(device=local_rank, **kw)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
-    ds = DeviceSystem(system, device=local_rank)
-    for w in range(args.warmup):
-        run_solver(ds, cfg.replace(base_seed=(rank + w * world) % 10))
-    torch.cuda.synchronize()
-    dist.barrier()
-    launches0 = N.launch_count()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    rows, iters = 0, []
-    with ClockSampler(local_rank) as clk:
-        for k in range(args.steps):
-            flush.fill_(k & 0xFF)
-            starts[k].record()
-            r = run_solver(ds, cfg.replace(base_seed=(rank + k * world) % 10))
-            ends[k].record()
-            assert r.converged
-            rows += r.gpu["rows_projected"]
-            iters.append(r.iterations)
-        torch.cuda.synchronize()
-    launches = N.launch_count() - launches0
-    t_ms = float(sum(s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)))
-    tt = torch.tensor([t_ms], device=f"cuda:{local_rank}")
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    tot = torch.tensor([float(rows)], device=f"cuda:{local_rank}")
-    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    t_ms = float(tt.item())
-    ds.close()
-    extras = [] if args.no_extra else sharded_extras(rank, world, local_rank)
-    if rank != 0:
-        return
-    peak, peak_src = read_peak()
-    value = float(tot.item()) / (t_ms / 1e3)
-    achieved = value / world * 8 * n / 1e9
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0; bitwise = reference)",
-        "config": {"workload": WORKLOADS[name][3], "m": m, "n": n, **kw,
-                   "parallelism": f"seed-parallel x{world}: independent solves per GPU, no collective",
-                   "seeds": "rank + k * world (mod 10)", "l2": "256 MiB write between steps"},
-        "iterations_rank0": iters,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src, "algorithmic_bytes": "8*n per row projection",
-                     "note": "per-GPU rate over the whole step"},
-        "clocks": clk.summary(),
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": n * 8,
-                "note": "multi-GPU runs keep the system resident; the host-array e2e path is measured at N=1"},
-        "gpu_launches": launches,
-        "sharded_extras": extras,
-    }
-    print(json.dumps(line), flush=True)
-
-
 def sharded_extras(rank, world, local_rank, steps=3):
     """BASELINE config 3 row-sharded across the ranks: rows/s over all GPUs (max-over-ranks
     time), RKAB bs = 1000 (1 outer iteration per step) and RKA (200 iterations per step)."""
@@ -386,13 +315,23 @@ def extra_workloads(device, peak, steps=3):
     return out
 
 
+SEEDS = 10  # BASELINE configs: every workload is solved for 10 solver seeds
+
+
+def seed_batch(cfg, base):
+    """One step: the configuration's 10 seed-solves (solver seeds base .. base + 9)."""
+    return [cfg.replace(base_seed=base + j) for j in range(SEEDS)]
+
+
 def run_b200(args, name, rank, world, local_rank):
-    if world > 1:
-        return run_b200_sharded(args, name, rank, world, local_rank)
+    """A step is one batch of the workload's 10 seed-solves to epsilon on the resident system,
+    run side by side (solve_concurrent: 10 lanes, each a system view with its own stream; one
+    16-CTA cluster per c1 solve, so up to 7 solves are co-resident).  Every rank runs its own
+    batch (solver seeds 10 * rank + 0..9): weak scaling, no collective on the data path."""
     import torch
     import torch.distributed as dist
 
-    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver, solve_concurrent
     from paper_2401_17474_b200 import _native as N
     from paper_2401_17474_b200.solvers import release_pool
 
@@ -402,8 +341,11 @@ def run_b200(args, name, rank, world, local_rank):
     cfg = SolverConfig(device=local_rank, **kw)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
     ds = DeviceSystem(system, device=local_rank)
+    base = SEEDS * rank
     for w in range(args.warmup):
-        run_solver(ds, cfg.replace(base_seed=w % 10))
+        solve_concurrent(ds, seed_batch(cfg, base), lanes=SEEDS)
+    # one seed alone: the time-to-eps of a single solve (the latency the batch hides)
+    alone = [run_solver(ds, c) for c in seed_batch(cfg, base)[:3]]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -412,47 +354,63 @@ def run_b200(args, name, rank, world, local_rank):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     rows = 0
     kernel_ms = 0.0
-    iters = []
+    iters, solve_ms = [], []
     kernel_name = None
     with ClockSampler(local_rank) as clk:
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
             starts[k].record()
-            r = run_solver(ds, cfg.replace(base_seed=k % 10))
+            rs = solve_concurrent(ds, seed_batch(cfg, base), lanes=SEEDS)
             ends[k].record()
-            assert r.converged, f"seed {k % 10} did not converge"
-            rows += r.gpu["rows_projected"]
-            kernel_ms += r.gpu["kernel_ms"]
-            kernel_name = r.gpu["kernel"]
-            iters.append(r.iterations)
+            for r in rs:
+                assert r.converged, f"seed {r.seed} did not converge"
+                rows += r.gpu["rows_projected"]
+                kernel_ms += r.gpu["kernel_ms"]
+                kernel_name = r.gpu["kernel"]
+                solve_ms.append(r.gpu["loop_ms"])
+            if k == 0:
+                iters = [r.iterations for r in rs]
         torch.cuda.synchronize()
     launches = N.launch_count() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = float(sum(step_ms))
+    tot_rows = float(rows)
     if world > 1:
         tt = torch.tensor([t_ms], device=f"cuda:{local_rank}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
+        rr = torch.tensor([tot_rows], device=f"cuda:{local_rank}")
+        dist.all_reduce(rr, op=dist.ReduceOp.SUM)
+        tot_rows = float(rr.item())
         dist.barrier()
     ds.close()
 
-    # e2e through the public API with pinned host arrays (H2D + solve + D2H per step)
+    # e2e through the public API with pinned host arrays: per step the H2D upload of A, b, x*,
+    # the 10 seed-solves and the D2H of every x
     from paper_2401_17474_b200 import LinearSystem
 
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     hsys = LinearSystem(A=pin(system.A), b=pin(system.b), x_star=pin(system.x_star), seed=0)
-    run_solver(hsys, cfg.replace(base_seed=0))  # warm the allocation pool
+    solve_concurrent(hsys, seed_batch(cfg, base), lanes=SEEDS)  # warm the allocation pool
     torch.cuda.synchronize()
     e2e_rows = 0
     t0 = time.perf_counter()
     for k in range(args.steps):
-        r = run_solver(hsys, cfg.replace(base_seed=k % 10))
-        e2e_rows += r.gpu["rows_projected"]
+        for r in solve_concurrent(hsys, seed_batch(cfg, base), lanes=SEEDS):
+            e2e_rows += r.gpu["rows_projected"]
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     release_pool()
+    e2e_val = float(e2e_rows) / e2e_s
+    if world > 1:
+        ee = torch.tensor([e2e_s], device=f"cuda:{local_rank}")
+        dist.all_reduce(ee, op=dist.ReduceOp.MAX)
+        e2e_val = world * float(e2e_rows) / float(ee.item())
     h2d = system.A.nbytes + system.b.nbytes + system.x_star.nbytes
-    d2h = n * 8
+    d2h = SEEDS * n * 8
+    extras = []
+    if world > 1 and not args.no_extra:
+        extras = sharded_extras(rank, world, local_rank)
 
     if rank != 0:
         return
@@ -466,26 +424,35 @@ def run_b200(args, name, rank, world, local_rank):
         if tr:
             traffic = tr["dram_bytes_per_launch"]
             traffic_note = {k: tr[k] for k in ("launch", "algorithmic_bytes_per_launch", "source", "note")}
-    value = world * rows / (t_ms / 1e3)
+    value = tot_rows / (t_ms / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0; bitwise = reference)",
-        "config": {"workload": WORKLOADS[name][3], "m": m, "n": n, **kw, "seeds": "0..9 cycling",
+        "config": {"workload": WORKLOADS[name][3] + f", {SEEDS} seeds per step", "m": m, "n": n, **kw,
+                   "seeds": f"solver seeds {SEEDS} * rank + 0..{SEEDS - 1}, solved side by side "
+                            f"({SEEDS} lanes, solve_concurrent)",
                    "l2": "256 MiB write between steps, outside the timed windows",
-                   "parallelism": "replicas" if world > 1 else "1 GPU", "kernel": kernel_name},
-        "time_to_eps_ms": {"mean": float(np.mean(step_ms)), "min": float(np.min(step_ms)),
-                           "max": float(np.max(step_ms))},
+                   "parallelism": f"{world} GPU(s), each its own batch of seed-solves, no collective",
+                   "kernel": kernel_name},
+        "time_to_eps_ms": {"alone_mean": float(np.mean([r.gpu["loop_ms"] for r in alone])),
+                           "in_batch_mean": float(np.mean(solve_ms)), "in_batch_max": float(np.max(solve_ms)),
+                           "batch_of_10_mean": float(np.mean(step_ms))},
         "iterations": iters,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_detail": traffic_note, "peak_source": peak_src,
                      "kernel": f"kz::rka/chain ({kernel_name})",
-                     "algorithmic_bytes": "8*n per row projection"},
+                     "algorithmic_bytes": "8*n per row projection",
+                     "aggregate_gbs": value / world * bytes_per_row / 1e9,
+                     "note": "achieved = one solve's row bytes / its own kernel time (per launch); aggregate_gbs = "
+                             "all concurrent solves' row bytes / step time on one GPU"},
         "clocks": clk.summary(),
-        "e2e": {"value": e2e_rows / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
     }
-    if not args.no_extra:
+    if world > 1:
+        line["sharded_extras"] = extras
+    elif not args.no_extra:
         line["extra_workloads"] = extra_workloads(local_rank, peak)
         line["sharded_extras"] = sharded_extras(0, 1, local_rank)  # the row-sharded path at N = 1
     if not args.no_cpu_baseline:

@@ -98,6 +98,16 @@ KZ_API int32_t kz_system_download(kz_system* sys, int64_t m2, int64_t n2, double
                                   double* xref_host, void* stream);
 /* Invalidate cached row norms / samplers after A was written in place. */
 KZ_API int32_t kz_system_touch(kz_system* sys);
+/* A view of a resident system for concurrent solves (e.g. the seeds of harness.bench's
+ * measure_iterations, harness.py:127-149, run side by side instead of one after another):
+ * it aliases the base system's A, b, x_ref, row norms and packed records and owns its
+ * iterate, samplers, scratch and a CUDA stream (used when a call passes stream = NULL).
+ * Destroy views with kz_system_destroy before the base; upload / generate / touch are
+ * refused on a view. */
+KZ_API int32_t kz_system_view(kz_system* base, kz_system** out);
+/* Re-attach a view after its base system was re-uploaded / regenerated (no allocation):
+ * the base's norms and packed records are rebuilt, the view's samplers dropped. */
+KZ_API int32_t kz_system_view_refresh(kz_system* view);
 
 /* ---- row norms: row_norm_cache (linalg.py:80-88) ------------------------
  * Bit-exact with np.einsum("ij,ij->i") (SSE2 two-lane order).  Cached on

@@ -134,9 +134,11 @@ PcgPod seed_stream(uint64_t seed, uint64_t stream) {
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
-    size_t cap = 0;  // elements
+    size_t cap = 0;         // elements
+    bool borrowed = false;  // a system view's alias of its base system's buffer: never freed or grown here
     int ensure(size_t n) {
         if (n <= cap) return KZ_OK;
+        if (borrowed) return fail(KZ_EINVAL, "a system view cannot grow its base system's buffers");
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -148,9 +150,15 @@ struct DevBuf {
         return KZ_OK;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p && !borrowed) cudaFree(p);
         p = nullptr;
         cap = 0;
+        borrowed = false;
+    }
+    void borrow(const DevBuf& o) {
+        p = o.p;
+        cap = o.cap;
+        borrowed = true;
     }
 };
 
@@ -174,7 +182,7 @@ struct kz_system {
     DevBuf<double> cg;     // CGLS work vectors (kz_cgls)
     DevBuf<double> stage;  // dense host-upload staging (one 1-D copy, then a device repack)
     DevBuf<unsigned long long> ll;  // rka kernel: tagged words of the cross-cluster exchange
-    unsigned tag_seq = 0;           // next free tag range of `ll`
+    size_t ll_words = 0;            // words the current plan uses
     DevBuf<double> S;               // kz_solve_sharded: the rank's worker sum (all-reduced in place)
     DevBuf<double> errs;            // kz_solve_sharded: ||x_k - x_ref||^2 per iteration of a chunk
     DevBuf<int> halt;               // kz_solve_sharded: device stop flag (k + 1 of the stop, 0 = running)
@@ -200,7 +208,20 @@ struct kz_system {
     int tm_box = 0;
     const void* tm_a = nullptr;
     const void* tm_b = nullptr;
+    // system views (kz_system_view): A, b, x_ref, row norms and packed records alias the base
+    // system's; the iterate, sampler, scratch, status and a stream of its own let several
+    // solves of one resident system run concurrently
+    bool is_view = false;
+    kz_system* base = nullptr;          // views: the system whose buffers they alias
+    cudaStream_t own_stream = nullptr;  // used when a call passes stream = NULL (views only)
 };
+
+// the stream of a call: the caller's, else the system's own (views), else the legacy default stream
+static inline cudaStream_t pick_stream(const kz_system* s, void* stream) {
+    return stream ? (cudaStream_t)stream : s->own_stream;
+}
+#define KZ_NOT_VIEW(s) \
+    if ((s)->is_view) return fail(KZ_EINVAL, "not allowed on a system view (it shares its base system's matrix)")
 
 extern "C" const char* kz_last_error(void) { return g_err.c_str(); }
 extern "C" int32_t kz_version(void) { return 1; }
@@ -275,6 +296,7 @@ extern "C" int32_t kz_system_destroy(kz_system* s) {
     if (s->h_status) cudaFreeHost(s->h_status);
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
+    if (s->own_stream) cudaStreamDestroy(s->own_stream);
     delete s;
     return KZ_OK;
 }
@@ -283,6 +305,7 @@ extern "C" int64_t kz_system_pitch(const kz_system* s) { return s ? s->ld : 0; }
 
 static int upload_common(kz_system* s, const double* A, int64_t lda, const double* b, const double* xref,
                          cudaStream_t st, cudaMemcpyKind kind) {
+    KZ_NOT_VIEW(s);
     if (lda < s->n) return fail(KZ_EINVAL, "lda=%lld < n=%lld", (long long)lda, (long long)s->n);
     KZ_CUDA(cudaSetDevice(s->device));
     if (kind == cudaMemcpyHostToDevice && lda == s->n && s->ld > s->n) {
@@ -339,7 +362,8 @@ extern "C" int32_t kz_system_device_ptrs(kz_system* s, double** A, double** b, d
 
 extern "C" int32_t kz_system_set_xref(kz_system* s, const double* xref, void* stream) {
     if (!s || !xref) return fail(KZ_EINVAL, "null argument");
-    cudaStream_t st = (cudaStream_t)stream;
+    KZ_NOT_VIEW(s);
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_CUDA(cudaMemcpyAsync(s->xref.p, xref, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
     KZ_CUDA(cudaStreamSynchronize(st));
@@ -356,8 +380,9 @@ extern "C" int32_t kz_generate_counter_rows(kz_system* s, uint64_t seed, int64_t
                                             double sg_lo, double sg_hi, void* stream) {
     if (row0 < 0) return fail(KZ_EINVAL, "row0 must be >= 0");
     if (!s) return fail(KZ_EINVAL, "null system");
+    KZ_NOT_VIEW(s);
     if (!(sg_lo > 0) || sg_hi < sg_lo || mu_hi < mu_lo) return fail(KZ_EINVAL, "bad generator ranges");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     const int64_t pairs = s->m * (s->ld / 2);
     const unsigned blocks = (unsigned)std::min<int64_t>((pairs + 255) / 256, (int64_t)s->sms * 64);
@@ -379,7 +404,7 @@ extern "C" int32_t kz_generate_counter_rows(kz_system* s, uint64_t seed, int64_t
 extern "C" int32_t kz_system_download(kz_system* s, int64_t m2, int64_t n2, double* A_host, double* b_host,
                                       double* xref_host, void* stream) {
     if (!s || m2 < 0 || n2 < 0 || m2 > s->m || n2 > s->n) return fail(KZ_EINVAL, "bad crop");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     if (A_host && m2 > 0 && n2 > 0)
         KZ_CUDA(cudaMemcpy2DAsync(A_host, n2 * sizeof(double), s->A.p, s->ld * sizeof(double), n2 * sizeof(double), m2,
@@ -393,6 +418,7 @@ extern "C" int32_t kz_system_download(kz_system* s, int64_t m2, int64_t n2, doub
 
 extern "C" int32_t kz_system_touch(kz_system* s) {
     if (!s) return fail(KZ_EINVAL, "null system");
+    KZ_NOT_VIEW(s);
     s->norms_valid = false;
     s->bs2_valid = false;
     s->sampler_scheme = -1;
@@ -426,7 +452,7 @@ static int ensure_norms(kz_system* s, cudaStream_t st) {
 
 extern "C" int32_t kz_row_norms(kz_system* s, double* sq_host, int64_t* bad_row, void* stream) {
     if (!s) return fail(KZ_EINVAL, "null system");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     int rc = ensure_norms(s, st);
     if (bad_row) *bad_row = s->bad_row;
@@ -434,6 +460,83 @@ extern "C" int32_t kz_row_norms(kz_system* s, double* sq_host, int64_t* bad_row,
         KZ_CUDA(cudaMemcpyAsync(sq_host, s->sq.p, s->m * sizeof(double), cudaMemcpyDeviceToHost, st));
         KZ_CUDA(cudaStreamSynchronize(st));
     }
+    return rc;
+}
+
+// packed (b_i, ||a_i||^2, RN(1/||a_i||^2), 0) records of every row (after the norms)
+static int ensure_bs2(kz_system* s, cudaStream_t st) {
+    if (s->bs2_valid) return KZ_OK;
+    KZ_TRY(s->bs2.ensure(4 * (size_t)s->m));
+    pack_bs2_kernel<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->b.p, s->sq.p, s->m, s->bs2.p);
+    KZ_TRY(check_launch("pack_bs2_kernel"));
+    s->bs2_valid = true;
+    return KZ_OK;
+}
+
+// A view of a resident system for concurrent solves: it aliases the base's matrix, right-hand
+// side, reference solution, row norms and packed records (built here first if needed), and owns
+// its iterate, samplers, scratch, status words and a CUDA stream.  The base must outlive its
+// views and must not be re-uploaded or regenerated while they exist.
+extern "C" int32_t kz_system_view(kz_system* base, kz_system** out) {
+    if (!base || !out) return fail(KZ_EINVAL, "null argument");
+    *out = nullptr;
+    if (base->is_view) return fail(KZ_EINVAL, "a view of a view: make views of the base system");
+    KZ_CUDA(cudaSetDevice(base->device));
+    KZ_TRY(ensure_norms(base, nullptr));
+    KZ_TRY(ensure_bs2(base, nullptr));
+    KZ_CUDA(cudaStreamSynchronize(nullptr));
+    kz_system* v = new kz_system();
+    v->device = base->device;
+    v->m = base->m;
+    v->n = base->n;
+    v->ld = base->ld;
+    v->sms = base->sms;
+    v->A.borrow(base->A);
+    v->b.borrow(base->b);
+    v->xref.borrow(base->xref);
+    v->sq.borrow(base->sq);
+    v->bs2.borrow(base->bs2);
+    v->norms_valid = true;
+    v->bad_row = base->bad_row;
+    v->bs2_valid = true;
+    v->has_xref = base->has_xref;
+    v->no_pairs = base->no_pairs;
+    v->is_view = true;
+    v->base = base;
+    int rc = KZ_OK;
+    if ((rc = v->x.ensure(v->ld)) || (rc = v->cdf.ensure(v->m)) || (rc = v->tmp.ensure(std::max<int64_t>(v->m, v->ld))) ||
+        (rc = v->status.ensure(1)) || (rc = v->barrier.ensure(1)) || (rc = v->zero_row.ensure(1))) {
+        kz_system_destroy(v);
+        return rc;
+    }
+    if (cudaMallocHost(&v->h_status, sizeof(SolveStatus)) != cudaSuccess ||
+        cudaStreamCreate(&v->own_stream) != cudaSuccess) {
+        cudaGetLastError();
+        kz_system_destroy(v);
+        return fail(KZ_ENOMEM, "view allocation failed");
+    }
+    for (auto& e : v->ev) cudaEventCreate(&e);
+    cudaMemset(v->x.p, 0, v->ld * sizeof(double));
+    *out = v;
+    return KZ_OK;
+}
+
+// After the base was re-uploaded or regenerated: rebuild its norms and packed records, and
+// drop the view's samplers built from the old norms (no allocation: the buffers stay aliased).
+extern "C" int32_t kz_system_view_refresh(kz_system* v) {
+    if (!v || !v->is_view || !v->base) return fail(KZ_EINVAL, "not a system view");
+    kz_system* base = v->base;
+    KZ_CUDA(cudaSetDevice(base->device));
+    const int rc = ensure_norms(base, nullptr);
+    if (rc != KZ_OK && rc != KZ_EDEGENERATE) return rc;
+    if (rc == KZ_OK) KZ_TRY(ensure_bs2(base, nullptr));
+    KZ_CUDA(cudaStreamSynchronize(nullptr));
+    v->norms_valid = true;
+    v->bad_row = base->bad_row;
+    v->bs2_valid = base->bs2_valid;
+    v->has_xref = base->has_xref;
+    v->sampler_scheme = -1;
+    v->sampler_q = 0;
     return rc;
 }
 
@@ -514,7 +617,7 @@ extern "C" int32_t kz_sampler_set_ranges(kz_system* s, int64_t q, const int64_t*
 
 extern "C" int32_t kz_sampler_build(kz_system* s, int32_t scheme, int64_t q, double* cdf_host, void* stream) {
     if (!s) return fail(KZ_EINVAL, "null system");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_TRY(ensure_sampler(s, scheme, q, st));
     if (cdf_host) {
@@ -540,7 +643,7 @@ extern "C" int32_t kz_dump_rows(kz_system* s, int32_t scheme, int64_t q, uint64_
     if (worker < 0 || worker >= q) return fail(KZ_EINVAL, "worker %lld out of range for q=%lld", (long long)worker, (long long)q);
     if (start < 0 || count < 0) return fail(KZ_EINVAL, "negative range");
     if (count == 0) return KZ_OK;
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_TRY(ensure_sampler(s, scheme, q, st));
     KZ_TRY(s->states.ensure(std::max<int64_t>(q, 1)));
@@ -584,7 +687,7 @@ static int device_norms(kz_system* s, const double* xdev, double* residual, doub
 
 extern "C" int32_t kz_norms(kz_system* s, const double* x_host, double* residual, double* error, void* stream) {
     if (!s || !x_host) return fail(KZ_EINVAL, "null argument");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_TRY(s->part.ensure(16));
     KZ_TRY(s->V.ensure(s->ld));
@@ -607,12 +710,12 @@ static int error_sq_dev(kz_system* s, double* out, cudaStream_t st) {
 extern "C" int32_t kz_error_sq(kz_system* s, double* err_host, void* stream) {
     if (!s || !err_host) return fail(KZ_EINVAL, "null argument");
     KZ_CUDA(cudaSetDevice(s->device));
-    return error_sq_dev(s, err_host, (cudaStream_t)stream);
+    return error_sq_dev(s, err_host, pick_stream(s, stream));
 }
 
 extern "C" int32_t kz_average_from(kz_system* s, const double* S_dev, int64_t Q, double* err_host, void* stream) {
     if (!s || !S_dev || Q < 1) return fail(KZ_EINVAL, "bad arguments");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     scale_copy_kernel<<<(unsigned)((s->ld + 255) / 256), 256, 0, st>>>(S_dev, (double)Q, s->ld, s->x.p);
     KZ_TRY(check_launch("scale_copy_kernel"));
@@ -623,7 +726,7 @@ extern "C" int32_t kz_average_from(kz_system* s, const double* S_dev, int64_t Q,
 
 extern "C" int32_t kz_solution_host(kz_system* s, double* x_host, void* stream) {
     if (!s || !x_host) return fail(KZ_EINVAL, "null argument");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
     KZ_CUDA(cudaStreamSynchronize(st));
@@ -632,7 +735,7 @@ extern "C" int32_t kz_solution_host(kz_system* s, double* x_host, void* stream) 
 
 extern "C" int32_t kz_set_x(kz_system* s, const double* x_host, void* stream) {
     if (!s) return fail(KZ_EINVAL, "null system");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_CUDA(cudaMemsetAsync(s->x.p, 0, s->ld * sizeof(double), st));
     if (x_host) KZ_CUDA(cudaMemcpyAsync(s->x.p, x_host, s->n * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -1224,12 +1327,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         KZ_TRY(ensure_norms(s, st));
     else
         KZ_TRY(ensure_sampler(s, p->scheme, q, st));
-    if (!s->bs2_valid) {
-        KZ_TRY(s->bs2.ensure(4 * (size_t)s->m));
-        pack_bs2_kernel<<<(unsigned)((s->m + 255) / 256), 256, 0, st>>>(s->b.p, s->sq.p, s->m, s->bs2.p);
-        KZ_TRY(check_launch("pack_bs2_kernel"));
-        s->bs2_valid = true;
-    }
+    KZ_TRY(ensure_bs2(s, st));
     if (!(s->pods_q == q && s->pods_seed == p->base_seed && s->pods_off == p->worker_offset)) {
         std::vector<PcgPod> pods(q);
         for (int64_t t = 0; t < q; ++t) pods[t] = seed_stream(p->base_seed, (uint64_t)(p->worker_offset + t));
@@ -1299,14 +1397,10 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     if (pl.kernel == KZ_KERNEL_CHAIN && q > 1) KZ_TRY(s->V.ensure((size_t)q * s->ld));
     KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
     if (pl.tma && pl.ctas > pl.cluster) {
-        // tagged words of the rka kernel's cluster exchange: a buffer of their own, zeroed once;
-        // every launch draws a fresh tag range (tag_base), so stale words never match
-        const size_t words = 4 * (size_t)(pl.ctas / pl.cluster) * (pl.wg ? (size_t)s->ld : (size_t)(q + 1));
-        if (s->ll.cap < words) {
-            KZ_TRY(s->ll.ensure(words));
-            KZ_CUDA(cudaMemsetAsync(s->ll.p, 0, s->ll.cap * sizeof(unsigned long long), st));
-            s->tag_seq = 0;
-        }
+        // tagged words of the rka kernel's cluster exchange (a buffer of their own; tags restart
+        // at 1 every launch, so launch_step zeroes the words before each launch)
+        s->ll_words = 4 * (size_t)(pl.ctas / pl.cluster) * (pl.wg ? (size_t)s->ld : (size_t)(q + 1));
+        KZ_TRY(s->ll.ensure(s->ll_words));
         KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
     }
     const int64_t n_ck_cap = p->ckpt_every > 0 ? std::max<int64_t>(0, p->ckpt_capacity) : 0;
@@ -1374,10 +1468,8 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
         KZ_CUDA(cudaMemsetAsync(s->part.p, 0, 4 * (size_t)(pl.ctas / pl.cluster) * (q + 1) * sizeof(double), st));
         KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
     }
-    if (pl.tma) {
-        args.tag_base = s->tag_seq;
-        s->tag_seq += (unsigned)args.count + 2u;
-    }
+    if (pl.tma && pl.ctas > pl.cluster)
+        KZ_CUDA(cudaMemsetAsync(s->ll.p, 0, s->ll_words * sizeof(unsigned long long), st));
     int lrc = launch_solve(s, pl, args, st);
     if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && first) {
         // CTA-pair clusters not launchable cooperatively here: one CTA per worker
@@ -1411,7 +1503,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     memset(r, 0, sizeof(*r));
     r->final_error_sq = NAN;
     r->final_residual = NAN;
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     SolveCtx cx;
     KZ_TRY(solve_setup(s, p, r, st, cx));
     const int64_t q = cx.q, bs = cx.bs;
@@ -1602,7 +1694,7 @@ extern "C" int32_t kz_cgls(kz_system* s, const double* b_host, double tol, int64
                            int64_t* iterations, void* stream) {
     if (!s || !x_out) return fail(KZ_EINVAL, "null argument");
     if (!(tol > 0)) return fail(KZ_EINVAL, "tol must be > 0, got %g", tol);
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     const int64_t m = s->m, n = s->n, ld = s->ld;
     if (max_it <= 0) max_it = 10 * n + 100;
@@ -1712,7 +1804,7 @@ extern "C" int32_t kz_spectral(kz_system* s, int64_t row_lo, int64_t row_hi, con
                                const double* v1_host, double tol, int64_t max_it, double* out, void* stream) {
     if (!s || !v0_host || !v1_host || !out) return fail(KZ_EINVAL, "null argument");
     if (row_lo < 0 || row_hi >= s->m || row_hi < row_lo) return fail(KZ_EINVAL, "bad row range");
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     const int64_t m = row_hi - row_lo + 1, n = s->n, ld = s->ld;
     const double* A = s->A.p + row_lo * ld;
@@ -2086,7 +2178,7 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     if (comm && comm->device != s->device)
         return fail(KZ_EINVAL, "communicator on device %d, shard on device %d", comm->device, s->device);
     const int world = comm ? comm->world : 1;
-    cudaStream_t st = (cudaStream_t)stream;
+    cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_TRY(s->S.ensure(2 * s->ld));  // two worker-sum buffers: step k writes S[k % 2], reads S[(k - 1) % 2]
     KZ_CUDA(cudaMemsetAsync(s->S.p, 0, 2 * s->ld * sizeof(double), st));  // the padded tails stay zero

@@ -47,7 +47,6 @@ struct SolveArgs {
     int* halt;             // optional: nonzero = the solve already stopped, the launch is a no-op
                            // (device-side stop flag of the row-sharded driver, kz_solve_sharded);
                            // the rka kernel raises it (stop iteration + 1) when its stop rule fires
-    unsigned tag_base;     // rka kernel: tags of this launch's tagged words are tag_base + 1 ...
     const double* x_sum;   // rka kernel, optional: x_k = x_sum / x_div (the all-reduced worker sum of the
     double x_div;          // previous row-sharded step) instead of x
     int wg;                // rka kernel: worker-group mode (cluster g runs workers [g q/G, (g+1) q/G))

@@ -127,9 +127,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
 
     if (warp == NW) {
         // ================= producer warp =================
-        if (a.x_sum)  // row-sharded step: x_k = the all-reduced worker sum / Q (kz_average_from's division)
+        if (a.x_sum) {  // row-sharded step: x_k = the all-reduced worker sum / Q (kz_average_from's division)
             for (int j = lane; j < wdt; j += 32) a.x[c0 + j] = __ddiv_rn(__ldcg(a.x_sum + c0 + j), a.x_div);
-        named_sync(XBAR, RKA_NT);
+            named_sync(XBAR, RKA_NT);
+        }
         const int ng = q4 / 4, nbg = (n_own + 3) / 4;
         const unsigned bytes = rows_bytes + (unsigned)nbg * 128u;
         const unsigned ring_u = smem_u32(ring);
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int gl = lane % LG, grp = lane / LG;
     double2 xv[EPL];
     for (int j = tid; j < cwb; j += NW * 32) xrs[j] = j < wdt ? a.xref[c0 + j] : 0.0;
-    named_sync(XBAR, RKA_NT);  // the producer warp formed x_k = x_sum / Q (row-sharded step)
+    if (a.x_sum) named_sync(XBAR, RKA_NT);  // the producer warp formed x_k = x_sum / Q (row-sharded step)
     named_sync(CBAR, NW * 32);
     bool vld[EPL];
 #pragma unroll
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         if (warp >= NW - NOWN) {
             // NOWN owner warps: warp ow takes the worker pairs ow, ow + NOWN, ... of this CTA
             const int ow = warp - (NW - NOWN);
-            const unsigned tag = a.tag_base + (unsigned)kk + 1u;  // unique per launch: no reset of the words
+            const unsigned tag = (unsigned)kk + 1u;  // the words are zeroed before every launch
             unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * Gx * q1 * 2;
             const int npair = (n_own + 1) / 2;
             const int my_pairs = npair > ow ? (npair - ow + NOWN - 1) / NOWN : 0;
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     // this cluster's column sums -> tagged words [par][cluster][column] (summed below)
                     unsigned long long* wl =
                         reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * G * ld * 2;
-                    const unsigned tag = a.tag_base + (unsigned)kk + 1u;
+                    const unsigned tag = (unsigned)kk + 1u;
                     ll_store(wl + ((size_t)gid * ld + c0 + j) * 2, v.x, tag);
                     ll_store(wl + ((size_t)gid * ld + c0 + j + 1) * 2, v.y, tag);
                     continue;
@@ -572,8 +573,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 // (every cluster forms the same x bit for bit)
                 const unsigned long long* wl =
                     reinterpret_cast<const unsigned long long*>(a.part) + (size_t)par * G * ld * 2;
-                const double tot = ll_sum_inl<RKA_MAXG>(wl + (size_t)(c0 + tid) * 2, 2 * ld, G,
-                                                        a.tag_base + (unsigned)kk + 1u, &a.status->aborted);
+                const double tot = ll_sum_inl<RKA_MAXG>(wl + (size_t)(c0 + tid) * 2, 2 * ld, G, (unsigned)kk + 1u,
+                                                        &a.status->aborted);
                 const double xj = qpow2 ? __dmul_rn(tot, invq) : div_rn_fast(tot, qd, invq);
                 xs[tid] = xj;
                 if (ck && gid == 0 && c0 + tid < a.n) a.ckpt[ck_slot * a.n + c0 + tid] = xj;

@@ -13,7 +13,7 @@ import numpy as np
 
 from .errors import ConvergenceError
 from .reports import RunReport, TraceRecord
-from .solvers import DeviceSystem, SolverConfig, run_solver
+from .solvers import DeviceSystem, SolverConfig, run_solver, solve_concurrent
 
 
 @dataclass
@@ -53,12 +53,18 @@ def _resident(system, cfg):
     return DeviceSystem(system, device=cfg.device), True
 
 
-def measure_iterations(system, cfg: SolverConfig, protocol: Protocol) -> MeasureResult:
+def measure_iterations(system, cfg: SolverConfig, protocol: Protocol, *, lanes: int | None = None) -> MeasureResult:
+    """Per-seed solves to epsilon (harness.py:127-149).  The seeds are independent solves of one
+    resident system, so they run side by side (solve_concurrent, `lanes` at a time; lanes=1:
+    one after another) -- bit-identical reports either way."""
     protocol.validate()
     ds, own = _resident(system, cfg)
     try:
-        reports = [run_solver(ds, cfg.replace(base_seed=cfg.base_seed + j, epsilon=protocol.epsilon))
-                   for j in range(protocol.n_seeds)]
+        cfgs = [cfg.replace(base_seed=cfg.base_seed + j, epsilon=protocol.epsilon) for j in range(protocol.n_seeds)]
+        if lanes == 1:
+            reports = [run_solver(ds, c) for c in cfgs]
+        else:
+            reports = solve_concurrent(ds, cfgs, lanes=lanes)
     finally:
         if own:
             ds.close()

@@ -145,12 +145,14 @@ class DeviceSystem:
         N.check(self._lib.kz_system_upload(self.handle, N.ptr(A), self.n, N.ptr(b),
                                            N.ptr(xr) if xr is not None else None, stream))
         self._xref_set = xr is not None
+        self._refresh_views()
 
     def upload_device(self, A_ptr: int, lda: int, b_ptr: int, xref_ptr: int | None = None, stream=None) -> None:
         """Copy from caller-owned device arrays (e.g. torch tensors' data_ptr())."""
         N.check(self._lib.kz_system_upload_device(self.handle, C.c_void_p(A_ptr), lda, C.c_void_p(b_ptr),
                                                   C.c_void_p(xref_ptr) if xref_ptr else None, stream))
         self._xref_set = bool(xref_ptr)
+        self._refresh_views()
 
     def device_ptrs(self) -> tuple[int, int, int, int]:
         """(A, b, x_ref, pitch) device pointers, for in-place generation."""
@@ -166,6 +168,7 @@ class DeviceSystem:
                                                    C.c_double(mu_range[0]), C.c_double(mu_range[1]),
                                                    C.c_double(sigma_range[0]), C.c_double(sigma_range[1]), None))
         self._xref_set = True
+        self._refresh_views()
 
     def download(self, m2: int | None = None, n2: int | None = None):
         """(A[:m2, :n2], b[:m2], x_ref[:n2]) copied to the host."""
@@ -179,6 +182,7 @@ class DeviceSystem:
 
     def touch(self) -> None:
         N.check(self._lib.kz_system_touch(self.handle))
+        self._refresh_views()
 
     def set_x_ref(self, x_ref) -> None:
         xr = N.f64(x_ref)
@@ -186,6 +190,7 @@ class DeviceSystem:
             raise DimensionMismatchError(f"expected length {self.n}, got {xr.shape}")
         N.check(self._lib.kz_system_set_xref(self.handle, N.ptr(xr), None))
         self._xref_set = True
+        self._refresh_views()
 
     @property
     def pitch(self) -> int:
@@ -358,7 +363,30 @@ class DeviceSystem:
         N.check(rc)
         return float(out[0]), float(out[1])
 
+    def _drop_views(self) -> None:
+        for v in self.__dict__.pop("_lane_views", []):
+            v.close()
+
+    def _refresh_views(self) -> None:
+        """Re-attach the cached lane views after this system's contents changed (no allocation)."""
+        for v in self.__dict__.get("_lane_views", []):
+            rc = self._lib.kz_system_view_refresh(v.handle)
+            if rc not in (N.KZ_OK, N.KZ_EDEGENERATE):  # a zero row surfaces at solve time, as in the reference
+                N.check(rc)
+
+    def view(self) -> "DeviceSystem":
+        """A view for concurrent solves (kz_system_view): it shares this system's matrix, b,
+        x_ref, row norms and packed records, and owns its iterate, samplers and CUDA stream.
+        Close views before this system; do not re-upload this system while views exist."""
+        h = C.c_void_p()
+        N.check(self._lib.kz_system_view(self.handle, C.byref(h)))
+        v = DeviceSystem.__new__(DeviceSystem)
+        v._lib, v.m, v.n, v.device = self._lib, self.m, self.n, self.device
+        v.host, v.handle, v._xref_set, v._base = self.host, h, self._xref_set, self
+        return v
+
     def close(self) -> None:
+        self._drop_views()  # views first: they alias this system's buffers
         if getattr(self, "handle", None):
             self._lib.kz_system_destroy(self.handle)
             self.handle = None
@@ -615,6 +643,48 @@ def _run_cgls(system, cfg, x_ref):
     return RunReport(variant="cgls", q=1, block_size=1, alpha_policy=cfg.alpha_policy, alpha=float("nan"),
                      seed=cfg.base_seed, iterations=-1, converged=True, wall_time_s=wall,
                      final_error_sq=err * err if x_ref is not None else float("nan"), final_residual=res, x=x)
+
+
+DEFAULT_LANES = 7  # 16-CTA thread-block clusters co-resident on one B200 (the rka kernel's unit)
+
+
+def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None) -> list[RunReport]:
+    """Independent solves of one resident system side by side (e.g. the per-seed solves of
+    harness.measure_iterations, harness.py:127-149): each of `lanes` host threads drives its
+    own system view (kz_system_view: shared matrix, own iterate / samplers / stream), so the
+    latency-bound solves of a small system share the GPU's SMs instead of queueing.  Reports
+    come back in the order of `cfgs` and are bit-identical to solving them one by one."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cfgs = list(cfgs)
+    if not cfgs:
+        return []
+    device = cfgs[0].device
+    if isinstance(system, DeviceSystem):
+        ds, own = system, False
+    else:  # host arrays: uploaded once for all the solves (recycled allocation)
+        ds, own = _pool_acquire(system, device), True
+    n_lanes = max(1, min(lanes or DEFAULT_LANES, len(cfgs)))
+    try:
+        # views persist on the system (allocations and streams are made once, not per call:
+        # a cudaFree inside a batch would synchronise the device under the other lanes)
+        cache = ds.__dict__.setdefault("_lane_views", [])
+        while len(cache) < n_lanes:
+            cache.append(ds.view())
+        views = cache[:n_lanes]
+        out: list[RunReport | None] = [None] * len(cfgs)
+
+        def lane(i):
+            for j in range(i, len(cfgs), n_lanes):
+                out[j] = run_solver(views[i], cfgs[j], budget=budget)
+
+        with ThreadPoolExecutor(n_lanes) as pool:
+            for f in [pool.submit(lane, i) for i in range(n_lanes)]:
+                f.result()
+        return out  # type: ignore[return-value]
+    finally:
+        if own:
+            _pool_release(ds)
 
 
 def run_solver(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
