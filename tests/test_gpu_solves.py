@@ -377,3 +377,24 @@ def test_chain_cta_pairs_match_oracle(gpu, oracle):
                          ckpt_every=2)
         for j, ck in enumerate(o["checkpoints"]):
             assert rel_err(cap[2 * (j + 1) - 1], ck) <= PARITY_TOL, ("rkab", j)
+
+
+def test_c3_crop_rkab_matches_oracle(gpu, oracle):
+    """BASELINE config 3's counter-keyed system (entries depend only on (seed, i, j), so a
+    16000 x 2000 system is the exact leading crop of the 160000 x 20000 one), RKAB q=64
+    bs=1000 with the distributed scheme -- the c3 solve-to-eps configuration -- for 25 outer
+    iterations: every iterate within 1e-10 of the oracle's."""
+    from paper_2401_17474_b200 import DeviceSystem, solve_rkab_seq
+
+    with DeviceSystem(m=16000, n=2000) as ds:
+        ds.generate_counter(0)
+        A, b, xr = ds.download()
+        cfg = _cfg(variant="rkab", q=64, block_size=1000, sampling_scheme="distributed")
+        cap = []
+        r = solve_rkab_seq(ds, cfg, budget=25, capture=cap)
+    o = oracle.solve(A, b, xr, variant="rkab", q=64, block_size=1000, scheme="distributed", budget=25,
+                     ckpt_every=5, nthreads=oracle.max_threads())
+    assert r.iterations == 25
+    assert rel_err(r.x, o["x"]) <= PARITY_TOL
+    for j, ck in enumerate(o["checkpoints"]):
+        assert rel_err(cap[5 * (j + 1) - 1], ck) <= PARITY_TOL, j
