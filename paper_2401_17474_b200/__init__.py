@@ -4,6 +4,7 @@ include/kz_b200.h for the C-ABI boundary."""
 
 from .errors import (ConvergenceError, DegenerateRowError, DimensionMismatchError, EmptyRangeError,
                      SpectralConvergenceError, SystemFormatError, TransportProtocolError, UnsupportedVersionError)
+from .distributed import run_distributed_solve
 from .harness import (MeasureResult, Protocol, ReplayResult, bench, measure_iterations, plateau_error,
                       timed_replay, trace_run)
 from .reports import REPORT_HEADER, TRACE_HEADER, RunReport, TraceRecord

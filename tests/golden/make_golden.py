@@ -21,6 +21,9 @@ fixtures pin:
                   final_error_sq, final x and x checkpoints (capture lists)
                   for the BASELINE configs c0, c1, c2 and desk-scale cases
 * traces.npz   -- trace_run records on an inconsistent system (harness.py:180-196)
+* dist.npz     -- run_distributed_solve (distributed.py:339-363): the simulated-MPI
+                  engine's RKA / RKAB (Algorithm 4: block_size + 1 rows, x / np
+                  before the all-reduce) per-rank iterates
 """
 
 from __future__ import annotations
@@ -200,6 +203,39 @@ def gen_ck():
     save("ck.npz", **out)
 
 
+def gen_dist():
+    """The reference's simulated-MPI engine (distributed.py:282-363, the paper's Algorithms 2 and 4):
+    run_distributed_solve over `size` ranks, one worker per rank, x/np before the all-reduce."""
+    t0 = time.time()
+    c0 = system(2000, 50, 0)
+    s2000 = system(2000, 50, 7)
+    out = {}
+
+    def record(tag, sys_, cfg, size, every, **kw):
+        caps = [[] for _ in range(size)]
+        reps = kb.run_distributed_solve(sys_, cfg, size, captures=caps, **kw)
+        r = reps[0]
+        assert all(np.array_equal(q.x, r.x) for q in reps)
+        out[f"{tag}_size"] = np.array(size)
+        out[f"{tag}_iterations"] = np.array(r.iterations)
+        out[f"{tag}_error_evals"] = np.array(r.error_evals)
+        out[f"{tag}_converged"] = np.array(r.converged)
+        out[f"{tag}_final_error_sq"] = np.array(r.final_error_sq)
+        out[f"{tag}_x"] = r.x.copy()
+        out[f"{tag}_every"] = np.array(every)
+        cap = caps[0]
+        out[f"{tag}_ckpt"] = np.array(cap[every - 1::every]) if len(cap) >= every else np.zeros((0, sys_.n))
+        print(tag, r.iterations, r.converged, f"{time.time() - t0:.1f}s", flush=True)
+
+    record("c0_rka_np4", c0, kb.SolverConfig(variant="rka", base_seed=0), 4, 50)
+    record("c0_rka_np8_s3", c0, kb.SolverConfig(variant="rka", base_seed=3), 8, 50)
+    record("s2000_rkab_np4_bs20", s2000, kb.SolverConfig(variant="rkab", block_size=20, base_seed=1), 4, 5)
+    record("s2000_rkab_np2_bs7_budget", s2000, kb.SolverConfig(variant="rkab", block_size=7, base_seed=2), 2, 10,
+           budget=60)
+    record("c0_rka_np4_fixed", c0, kb.SolverConfig(variant="rka", alpha_policy="fixed", alpha=1.3), 4, 50)
+    save("dist.npz", **out)
+
+
 def gen_kzsys():
     """A KZSYS v1 file written by the reference's own save_system (sysgen.py:190-214)."""
     kb.save_system(system(500, 20, 1), os.path.join(OUT, "kzsys_s500.bin"))
@@ -211,7 +247,10 @@ if __name__ == "__main__":
         gen_ck()
     elif len(sys.argv) > 1 and sys.argv[1] == "kzsys":
         gen_kzsys()
+    elif len(sys.argv) > 1 and sys.argv[1] == "dist":
+        gen_dist()
     else:
         main()
         gen_ck()
         gen_kzsys()
+        gen_dist()

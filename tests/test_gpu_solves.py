@@ -398,3 +398,31 @@ def test_c3_crop_rkab_matches_oracle(gpu, oracle):
     assert rel_err(r.x, o["x"]) <= PARITY_TOL
     for j, ck in enumerate(o["checkpoints"]):
         assert rel_err(cap[5 * (j + 1) - 1], ck) <= PARITY_TOL, j
+
+
+@pytest.mark.parametrize("tag", ["c0_rka_np4", "c0_rka_np8_s3", "s2000_rkab_np4_bs20", "s2000_rkab_np2_bs7_budget",
+                                 "c0_rka_np4_fixed"])
+def test_run_distributed_solve_matches_reference(gpu, systems, tag):
+    """run_distributed_solve (the reference's simulated-MPI engine, Algorithms 2 and 4) on the
+    B200 against the reference's own runs (tests/golden/dist.npz)."""
+    from test_oracle_golden import DIST_CASES
+
+    from paper_2401_17474_b200 import run_distributed_solve
+
+    g = golden("dist.npz")
+    sysname, variant, bs, seed, alpha, budget = DIST_CASES[tag]
+    s = systems[sysname]
+    size = int(g[f"{tag}_size"])
+    kw = dict(alpha_policy="fixed", alpha=alpha) if alpha is not None else {}
+    caps = [[] for _ in range(size)]
+    reps = run_distributed_solve(s, _cfg(variant=variant, block_size=bs, base_seed=seed, **kw), size,
+                                 budget=budget, captures=caps)
+    assert len(reps) == size and all(np.array_equal(r.x, reps[0].x) for r in reps)
+    r = reps[0]
+    assert r.iterations == int(g[f"{tag}_iterations"]) and r.converged == bool(g[f"{tag}_converged"])
+    if budget is None:
+        assert r.error_evals == int(g[f"{tag}_error_evals"])
+    assert rel_err(r.x, g[f"{tag}_x"]) <= PARITY_TOL
+    every = int(g[f"{tag}_every"])
+    for j, ck in enumerate(g[f"{tag}_ckpt"]):
+        assert rel_err(caps[0][every * (j + 1) - 1], ck) <= PARITY_TOL, j

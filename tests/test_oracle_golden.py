@@ -123,3 +123,32 @@ def test_oracle_cyclic_kaczmarz_matches_reference(oracle, systems):
         assert rel_err(o["x"], g[f"{tag}_x"]) <= PARITY_TOL, tag
         for j, ck in enumerate(g[f"{tag}_ckpt"]):
             assert rel_err(o["checkpoints"][j], ck) <= PARITY_TOL, (tag, j)
+
+
+DIST_CASES = {  # tag: (system, variant, block_size, seed, alpha, budget)
+    "c0_rka_np4": ("c0", "rka", 1, 0, None, None),
+    "c0_rka_np8_s3": ("c0", "rka", 1, 3, None, None),
+    "s2000_rkab_np4_bs20": ("s2000", "rkab", 20, 1, None, None),
+    "s2000_rkab_np2_bs7_budget": ("s2000", "rkab", 7, 2, None, 60),
+    "c0_rka_np4_fixed": ("c0", "rka", 1, 0, 1.3, None),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(DIST_CASES))
+def test_distributed_engine_is_distributed_scheme(oracle, systems, tag):
+    """The reference's simulated-MPI engine (run_distributed_solve, distributed.py:339-363) equals
+    the sequential solve with q = ranks, the distributed scheme and block_size + 1 rows for RKAB
+    (Algorithm 4) -- the mapping paper_2401_17474_b200.run_distributed_solve uses."""
+    g = golden("dist.npz")
+    sysname, variant, bs, seed, alpha, budget = DIST_CASES[tag]
+    s = systems[sysname]
+    size = int(g[f"{tag}_size"])
+    o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=size, block_size=bs + (1 if variant == "rkab" else 0),
+                     base_seed=seed, scheme="distributed", budget=budget,
+                     alphas=None if alpha is None else [alpha] * size, ckpt_every=int(g[f"{tag}_every"]))
+    assert o["iterations"] == int(g[f"{tag}_iterations"]) and o["converged"] == bool(g[f"{tag}_converged"])
+    if budget is None:
+        assert o["error_evals"] == int(g[f"{tag}_error_evals"])
+    assert rel_err(o["x"], g[f"{tag}_x"]) <= PARITY_TOL
+    for j, ck in enumerate(g[f"{tag}_ckpt"]):
+        assert rel_err(o["checkpoints"][j], ck) <= PARITY_TOL, j
