@@ -315,6 +315,14 @@ def extra_workloads(device, peak, steps=3):
         measure("c2", ds, 1000, SolverConfig(variant="rkab", q=64, block_size=500, device=device), None,
                 "c2: RKAB q=64 bs=500 80000x1000, solve to eps")
         ds.close()
+        # c1's row width and q with the rows streamed from HBM (c1's 80 MB stays in the
+        # 126 MB L2; this 400000 x 500 system (1.6 GB) does not)
+        s1c = generate_mother(GeneratorConfig(m_max=400000, n_max=500, seed=0))
+        ds = DeviceSystem(s1c, device=device)
+        del s1c
+        measure("c1shape_hbm_rka_q64", ds, 500, SolverConfig(variant="rka", q=64, device=device), 4000,
+                "c1 row width and q=64 on a 400000x500 system (1.6 GB > L2): RKA, 4000 iterations per step")
+        ds.close()
         s0 = generate_mother(GeneratorConfig(m_max=2000, n_max=50, seed=0))
         ds = DeviceSystem(s0, device=device)
         measure("c0", ds, 50, SolverConfig(variant="rk", device=device), None, "c0: RK 2000x50, solve to eps")
