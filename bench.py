@@ -186,17 +186,22 @@ def sharded_extras(rank, world, local_rank, steps=3):
     try:
         plan = plan_shards(m_total, world, rank, q)
         shard = CudaShard.counter(m_total, n, plan, 0, local_rank)
-        comm = ShardComm(local_rank, world, rank) if world > 1 else None
-        cases = (("c3_sharded_rkab_bs1000", dict(variant="rkab", q=q, block_size=1000), 1, True),
-                 ("c3_sharded_rka", dict(variant="rka", q=q), 200, True),
-                 ("c3_sharded_rka_host_loop", dict(variant="rka", q=q), 200, False))
-        for tag, kw, budget, native in cases:
+        comm = ShardComm(local_rank, world, rank)  # NCCL communicator (+ the fused exchange for RKA)
+        cases = (("c3_sharded_rkab_bs1000", dict(variant="rkab", q=q, block_size=1000), 1, "native",
+                  "native loop: local step + ncclAllReduce per outer iteration"),
+                 ("c3_sharded_rka", dict(variant="rka", q=q), 200, "fused",
+                  "fused: one launch per chunk, column sums exchanged in-kernel over NVLink peer memory"),
+                 ("c3_sharded_rka_nccl_loop", dict(variant="rka", q=q), 200, "native",
+                  "native loop: step kernel + ncclAllReduce per outer iteration, device stop flag"),
+                 ("c3_sharded_rka_host_loop", dict(variant="rka", q=q), 200, "host",
+                  "host-driven loop (multigpu.solve_sharded, torch.distributed all_reduce)"))
+        for tag, kw, budget, mode, how in cases:
             cfg = SolverConfig(device=local_rank, sampling_scheme="distributed", **kw)
 
             def run(c):
-                if native:
-                    return solve_sharded_native(shard, c, budget=budget, comm=comm)
-                return solve_sharded(shard, c, budget=budget)
+                if mode == "host":
+                    return solve_sharded(shard, c, budget=budget)
+                return solve_sharded_native(shard, c, budget=budget, comm=comm, fused=(mode == "fused"))
 
             run(cfg)  # warm-up
             torch.cuda.synchronize()
@@ -217,13 +222,10 @@ def sharded_extras(rank, world, local_rank, steps=3):
             rows_s = float(rr.item()) / (float(tt.item()) / 1e3)
             out.append({"workload": tag, "n_gpus": world, "rows_per_s": rows_s, "ms_per_step": float(tt.item()) / steps,
                         "desc": f"160000x20000 counter-keyed, rows sharded x{world}, q={q} per GPU, "
-                                f"{budget} outer iteration(s) per step, NCCL all-reduce per outer iteration, "
-                                + ("native loop (kz_solve_sharded: no host sync per iteration)" if native
-                                   else "host-driven loop (multigpu.solve_sharded)"),
+                                f"{budget} outer iteration(s) per step; {how}",
                         "hbm_frac_per_gpu": rows_s / world * 8 * n / 1e9 / read_peak()[0]})
         shard.close()
-        if comm is not None:
-            comm.close()
+        comm.close()
     except Exception as exc:  # extras must never sink the headline line
         out.append({"error": repr(exc)})
     return out

@@ -159,10 +159,13 @@ typedef struct {
     int64_t worker_offset;  /* stream id of local worker 0: worker t draws from Prng(seed, offset+t) */
     int64_t k_start;        /* index of the first iteration (row-draw offset k_start * block_size)   */
     int32_t keep_x;         /* start from the resident iterate instead of x0 = 0                     */
-    int32_t pad0;
+    int32_t flags;          /* KZ_FLAG_* bits (0 = none)                                             */
     double* partial_dev;    /* non-NULL: run ONE iteration and write the un-normalised worker sum   */
                             /* S = sum_t v_t (n values, device) instead of updating x                */
 } kz_params;
+/* kz_params.flags: kz_solve_sharded keeps the per-iteration NCCL all-reduce even when the
+ * communicator's fused cross-rank exchange is connected. */
+#define KZ_FLAG_NO_FUSED_EXCHANGE 1
 
 typedef struct {
     int64_t iterations;     /* RunReport.iterations                                           */
@@ -235,6 +238,15 @@ typedef struct kz_comm kz_comm;
 KZ_API int32_t kz_comm_unique_id(uint8_t* id_out);
 KZ_API int32_t kz_comm_create(int32_t device, const uint8_t* id, int32_t world, int32_t rank, kz_comm** out);
 KZ_API int32_t kz_comm_destroy(kz_comm* comm);
+/* The fused cross-rank exchange (optional; kz_solve_sharded uses it for RKA when connected):
+ * every rank sizes its exchange buffer for the shard pitch (kz_system_pitch) and exports its
+ * CUDA IPC handle (KZ_COMM_HANDLE_BYTES bytes); the caller all-gathers the handles in rank
+ * order and every rank connects.  The step kernel then writes its column sums straight into
+ * every rank's buffer over NVLink and reads the world's sums from its own (no NCCL call, one
+ * launch per chunk of iterations). */
+#define KZ_COMM_HANDLE_BYTES 64
+KZ_API int32_t kz_comm_exchange_handle(kz_comm* comm, int64_t ld, uint8_t* handle_out);
+KZ_API int32_t kz_comm_exchange_connect(kz_comm* comm, const uint8_t* handles);
 /* The whole _drive loop (solvers.py:182-263) of one rank's row shard, natively:
  * per outer iteration the local step writes the rank's worker sum S_g, S is
  * all-reduced in place over `comm` (NULL: a single rank), and x = S / (q *

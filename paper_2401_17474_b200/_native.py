@@ -35,8 +35,9 @@ EXPORTS = (
     "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
     "kz_cgls", "kz_spectral", "kz_system_load_file", "kz_generate_counter_rows",
     "kz_comm_unique_id", "kz_comm_create", "kz_comm_destroy", "kz_solve_sharded", "kz_system_view",
-    "kz_system_view_refresh",
+    "kz_system_view_refresh", "kz_comm_exchange_handle", "kz_comm_exchange_connect",
 )
+COMM_HANDLE_BYTES = 64
 COMM_ID_BYTES = 128
 
 
@@ -71,7 +72,7 @@ class Params(C.Structure):
         ("worker_offset", C.c_int64),
         ("k_start", C.c_int64),
         ("keep_x", C.c_int32),
-        ("pad0", C.c_int32),
+        ("flags", C.c_int32),
         ("partial_dev", C.c_void_p),
     ]
 
@@ -143,6 +144,8 @@ def load_library():
         L.kz_comm_unique_id.argtypes = [C.c_char_p]
         L.kz_comm_create.argtypes = [C.c_int32, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(vp)]
         L.kz_comm_destroy.argtypes = [vp]
+        L.kz_comm_exchange_handle.argtypes = [vp, C.c_int64, C.c_char_p]
+        L.kz_comm_exchange_connect.argtypes = [vp, C.c_char_p]
         L.kz_solve_sharded.argtypes = [vp, vp, C.POINTER(Params), C.POINTER(Result), _dp, vp]
         for name in EXPORTS:
             fn = getattr(L, name)

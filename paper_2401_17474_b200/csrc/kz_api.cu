@@ -768,6 +768,7 @@ struct Plan {
     int lg = 32, epl = 1, box = 0;  // rka kernel: lanes per row group, pairs per lane, TMA box width
     bool sr = false;    // rka kernel: single round of 8 rows per warp (<= 64 workers per cluster)
     bool wg = false;    // rka kernel: worker groups (cluster g runs q/G workers over all columns)
+    bool xr = false;    // rka kernel: cross-rank column sums (set per launch by kz_solve_sharded, not planned)
     size_t smem = 0;
 };
 
@@ -977,26 +978,28 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
 
 namespace {
 
-template <bool TM, bool SR, bool WG>
+template <bool TM, bool SR, int MODE>
 void* rka_fn_t(int lg, int epl) {
-    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM, SR, WG> : (void*)rka_kernel<8, 1, TM, SR, WG>;
-    if (lg == 16) return (void*)rka_kernel<16, 1, TM, SR, WG>;
+    if (lg == 8) return epl == 2 ? (void*)rka_kernel<8, 2, TM, SR, MODE> : (void*)rka_kernel<8, 1, TM, SR, MODE>;
+    if (lg == 16) return (void*)rka_kernel<16, 1, TM, SR, MODE>;
     switch (epl) {
-        case 1: return (void*)rka_kernel<32, 1, TM, SR, WG>;
-        case 2: return (void*)rka_kernel<32, 2, TM, SR, WG>;
-        case 3: return (void*)rka_kernel<32, 3, TM, SR, WG>;
-        case 4: return (void*)rka_kernel<32, 4, TM, SR, WG>;
+        case 1: return (void*)rka_kernel<32, 1, TM, SR, MODE>;
+        case 2: return (void*)rka_kernel<32, 2, TM, SR, MODE>;
+        case 3: return (void*)rka_kernel<32, 3, TM, SR, MODE>;
+        case 4: return (void*)rka_kernel<32, 4, TM, SR, MODE>;
         default: return nullptr;
     }
 }
 
 // the timing variant (per-phase clock stamps) only under KZ_PHASE_TIMING (column-sliced plans);
-// SR = one round of 8 rows per warp (<= 64 workers per cluster); WG = worker groups
-void* rka_fn(int lg, int epl, bool sr, bool wg = false) {
-    if (wg) return sr ? rka_fn_t<false, true, true>(lg, epl) : rka_fn_t<false, false, true>(lg, epl);
+// SR = one round of 8 rows per warp (<= 64 workers per cluster); mode 1 = worker groups,
+// mode 2 = cross-rank column sums (kz_solve_sharded)
+void* rka_fn(int lg, int epl, bool sr, int mode = 0) {
+    if (mode == 1) return sr ? rka_fn_t<false, true, 1>(lg, epl) : rka_fn_t<false, false, 1>(lg, epl);
+    if (mode == 2) return sr ? rka_fn_t<false, true, 2>(lg, epl) : rka_fn_t<false, false, 2>(lg, epl);
     const bool tm = getenv("KZ_PHASE_TIMING") != nullptr;
-    if (tm) return sr ? rka_fn_t<true, true, false>(lg, epl) : rka_fn_t<true, false, false>(lg, epl);
-    return sr ? rka_fn_t<false, true, false>(lg, epl) : rka_fn_t<false, false, false>(lg, epl);
+    if (tm) return sr ? rka_fn_t<true, true, 0>(lg, epl) : rka_fn_t<true, false, 0>(lg, epl);
+    return sr ? rka_fn_t<false, true, 0>(lg, epl) : rka_fn_t<false, false, 0>(lg, epl);
 }
 
 size_t rka_smem(int64_t q, int box, int stages, int Pc) {
@@ -1092,7 +1095,7 @@ static int plan_rka_wg(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
             continue;
         }
         const bool sr = qmax <= 8 * RKA_NW;
-        void* fn = rka_fn(lg, epl, sr, true);
+        void* fn = rka_fn(lg, epl, sr, 1);
         if (!fn) return fail(KZ_EINVAL, "no rka kernel for LG=%d EPL=%d", lg, epl);
         const size_t smem = rka_smem(qmax, box, stages, Pc);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1258,7 +1261,7 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
         cfg.attrs = attr2;
         cfg.numAttrs = na;
     } else if (pl.kernel == KZ_KERNEL_SYNC_CLUSTER) {
-        fn = pl.tma ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg) : sync_fn(true, pl.lpr);
+        fn = pl.tma ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg ? 1 : (pl.xr ? 2 : 0)) : sync_fn(true, pl.lpr);
         int na = 0;
         attr2[na].id = cudaLaunchAttributeClusterDimension;
         attr2[na].val.clusterDim.x = pl.cluster;
@@ -1366,7 +1369,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         // the dynamic shared-memory limit is a property of the kernel function, which another
         // system may have lowered since: restore it for this plan
         void* fn = pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair)
-                   : pl.tma                     ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg)
+                   : pl.tma                     ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg ? 1 : (pl.xr ? 2 : 0))
                                                 : sync_fn(pl.kernel == KZ_KERNEL_SYNC_CLUSTER, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     } else if (kern == KZ_KERNEL_CHAIN) {
@@ -2122,6 +2125,14 @@ int nccl_load() {
 struct kz_comm {
     int device = 0, world = 1, rank = 0;
     ncclComm_t nccl = nullptr;
+    // cross-rank exchange of the fused row-sharded kernel (rka kernel mode 2): every rank's buffer
+    // of tagged column sums [parity][rank][column], reachable from every GPU over NVLink
+    unsigned long long* xbuf = nullptr;  // this rank's buffer (cudaMalloc, exported by IPC)
+    int64_t xld = 0;                     // row pitch the buffers are sized for
+    std::vector<void*> opened;           // peers' buffers mapped with cudaIpcOpenMemHandle
+    unsigned long long** peers_dev = nullptr;  // device array of the world's buffers
+    bool xr_ready = false;
+    unsigned tag_next = 1;  // next tag: advanced identically on every rank, never reused
 };
 
 extern "C" int32_t kz_comm_unique_id(uint8_t* id_out) {
@@ -2155,8 +2166,54 @@ extern "C" int32_t kz_comm_create(int32_t device, const uint8_t* id, int32_t wor
     return KZ_OK;
 }
 
+extern "C" int32_t kz_comm_exchange_handle(kz_comm* c, int64_t ld, uint8_t* handle_out) {
+    if (!c || !handle_out) return fail(KZ_EINVAL, "null argument");
+    if (ld < 1) return fail(KZ_EINVAL, "ld must be >= 1");
+    if (c->world > RKA_MAXR) return fail(KZ_EINVAL, "the fused exchange covers up to %d ranks", RKA_MAXR);
+    static_assert(sizeof(cudaIpcMemHandle_t) == KZ_COMM_HANDLE_BYTES, "IPC handle size");
+    KZ_CUDA(cudaSetDevice(c->device));
+    if (c->xbuf && c->xld != ld) return fail(KZ_EINVAL, "exchange buffer already sized for pitch %lld", (long long)c->xld);
+    if (!c->xbuf) {
+        const size_t words = 4 * (size_t)c->world * (size_t)ld;  // [2 parities][world][ld] x 2 words
+        KZ_CUDA(cudaMalloc(&c->xbuf, words * sizeof(unsigned long long)));
+        KZ_CUDA(cudaMemset(c->xbuf, 0, words * sizeof(unsigned long long)));  // tag 0 is never used
+        c->xld = ld;
+    }
+    cudaIpcMemHandle_t h;
+    KZ_CUDA(cudaIpcGetMemHandle(&h, c->xbuf));
+    memcpy(handle_out, &h, sizeof(h));
+    return KZ_OK;
+}
+
+extern "C" int32_t kz_comm_exchange_connect(kz_comm* c, const uint8_t* handles) {
+    if (!c || !handles) return fail(KZ_EINVAL, "null argument");
+    if (!c->xbuf) return fail(KZ_EINVAL, "kz_comm_exchange_handle first");
+    KZ_CUDA(cudaSetDevice(c->device));
+    std::vector<unsigned long long*> ptrs(c->world);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) {
+            ptrs[r] = c->xbuf;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + (size_t)r * KZ_COMM_HANDLE_BYTES, sizeof(h));
+        void* p = nullptr;
+        KZ_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->opened.push_back(p);
+        ptrs[r] = reinterpret_cast<unsigned long long*>(p);
+    }
+    if (!c->peers_dev) KZ_CUDA(cudaMalloc(&c->peers_dev, RKA_MAXR * sizeof(unsigned long long*)));
+    KZ_CUDA(cudaMemcpy(c->peers_dev, ptrs.data(), c->world * sizeof(unsigned long long*), cudaMemcpyHostToDevice));
+    c->xr_ready = true;
+    return KZ_OK;
+}
+
 extern "C" int32_t kz_comm_destroy(kz_comm* c) {
     if (!c) return KZ_OK;
+    cudaSetDevice(c->device);
+    for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+    if (c->peers_dev) cudaFree(c->peers_dev);
+    if (c->xbuf) cudaFree(c->xbuf);
     if (c->nccl && g_nccl.ok) {
         cudaSetDevice(c->device);
         g_nccl.comm_destroy(c->nccl);
@@ -2207,12 +2264,64 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     int64_t k = 0, evals = 0;
     bool converged = false;
     double err = NAN;
-    if (stop_mode) {  // _drive's check before iteration 0 (x_0 = 0 or the kept iterate)
+    // fused cross-rank path (RKA on the rka kernel, communicator connected): the step kernel runs a
+    // whole chunk of outer iterations, exchanging column sums with the other ranks over NVLink peer
+    // memory every iteration and applying the stop rule itself -- like kz_solve's chunked loop
+    const bool xr = cx.pl.tma && comm && comm->xr_ready && bs == 1 && comm->xld == s->ld &&
+                    !(p->flags & KZ_FLAG_NO_FUSED_EXCHANGE);
+    if (xr) {
+        Plan& pl = cx.pl;
+        pl.xr = true;
+        void* fn = rka_fn(pl.lg, pl.epl, pl.sr, 2);
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+        KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
+        args.partial = nullptr;
+        args.x_sum = nullptr;
+        args.halt = nullptr;
+        args.use_stop = stop_mode ? 1 : 0;
+        args.x_div = (double)Q;
+        args.xr_peers = comm->peers_dev;
+        args.xr_ranks = world;
+        args.xr_rank = comm->rank;
+        args.idx = idx0;
+        args.idx_stride = q;
+        KZ_CUDA(cudaEventRecord(s->ev[0], st));
+        int64_t chunkf = stop_mode ? std::min<int64_t>(cx.chunk_cap, 4096) : cx.chunk_cap;
+        for (;;) {
+            const int64_t remaining = limit - k;
+            if (remaining <= 0 && !stop_mode) break;
+            const int64_t c = std::min<int64_t>(chunkf, remaining);
+            if (c > 0) KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, q, p->k_start + k, c, idx0, 1, q, st));
+            args.k0 = k;
+            args.count = c;
+            args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
+            args.xr_tag0 = comm->tag_next;  // every rank launches the same counts: tags agree
+            comm->tag_next += (unsigned)c + 1u;
+            KZ_TRY(launch_step(s, &pp, r, cx, k == 0, st));
+            KZ_CUDA(cudaMemcpyAsync(s->h_status, s->status.p, sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
+            KZ_CUDA(cudaStreamSynchronize(st));
+            const SolveStatus hs = *s->h_status;
+            if (hs.aborted) return fail(KZ_ECUDA, "cross-rank exchange timed out (a rank stopped launching)");
+            k += hs.iters_done;
+            evals += hs.checks;
+            if (hs.checks > 0) err = hs.err;
+            if (hs.converged) {
+                converged = true;
+                break;
+            }
+            if (hs.iters_done != c)
+                return fail(KZ_ECUDA, "solve kernel stopped early (%lld of %lld iterations)", (long long)hs.iters_done,
+                            (long long)c);
+            if (stop_mode && k >= p->max_iterations) break;
+            if (stop_mode) chunkf = std::min<int64_t>(cx.chunk_cap, chunkf * 2);
+        }
+    } else if (stop_mode) {  // _drive's check before iteration 0 (x_0 = 0 or the kept iterate)
         KZ_TRY(error_sq_dev(s, &err, st));
         evals = 1;
         converged = err < p->epsilon;
     }
-    KZ_CUDA(cudaEventRecord(s->ev[0], st));
+    if (!xr) KZ_CUDA(cudaEventRecord(s->ev[0], st));
     // rka kernel: x_k = S / Q, the stop rule and the halt flag live in the step kernel itself (one
     // kernel + one collective per outer iteration); chain kernel (RKAB): separate average kernel
     const bool fused = cx.pl.tma;
@@ -2221,7 +2330,7 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
         args.x_div = (double)Q;
     }
     int64_t chunk = stop_mode ? 64 : chunk_max;
-    while (!converged && k < limit) {
+    while (!xr && !converged && k < limit) {
         const int64_t c = std::min<int64_t>(chunk, limit - k);
         // row draws of the whole chunk: one sampler launch (x-independent)
         const int64_t count = c * bs;

@@ -201,6 +201,17 @@ __device__ __forceinline__ void ll_load_raw(const unsigned long long* p, unsigne
                                             unsigned long long& w1) {
     asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
 }
+// System scope twins: words written by kernels on other GPUs over NVLink (peer memory).
+__device__ __forceinline__ void ll_store_sys(unsigned long long* p, double v, unsigned tag) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long w0 = (bits & 0xffffffffull) | ((unsigned long long)tag << 32);
+    const unsigned long long w1 = (bits >> 32) | ((unsigned long long)tag << 32);
+    asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+__device__ __forceinline__ void ll_load_raw_sys(const unsigned long long* p, unsigned long long& w0,
+                                                unsigned long long& w1) {
+    asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+}
 __device__ __forceinline__ bool ll_ok(unsigned long long w0, unsigned long long w1, unsigned tag) {
     return (unsigned)(w0 >> 32) == tag && (unsigned)(w1 >> 32) == tag;
 }
@@ -246,12 +257,18 @@ __device__ __noinline__ double ll_sum(const unsigned long long* p, int stride, i
 }
 
 // inlined twin (no call ABI around it: the rka kernel's combine phase keeps many live registers)
-template <int GMAX>
+template <int GMAX, bool SYS = false>
 __device__ __forceinline__ double ll_sum_inl(const unsigned long long* p, int stride, int G, unsigned tag, int* abort) {
+    auto ld2 = [](const unsigned long long* a, unsigned long long& w0, unsigned long long& w1) {
+        if constexpr (SYS)
+            ll_load_raw_sys(a, w0, w1);
+        else
+            ll_load_raw(a, w0, w1);
+    };
     unsigned long long w0[GMAX], w1[GMAX];
 #pragma unroll
     for (int g = 0; g < GMAX; ++g)
-        if (g < G) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+        if (g < G) ld2(p + (size_t)g * stride, w0[g], w1[g]);
     unsigned spins = 0;
     for (;;) {
         bool all = true;
@@ -267,7 +284,7 @@ __device__ __forceinline__ double ll_sum_inl(const unsigned long long* p, int st
         }
 #pragma unroll
         for (int g = 0; g < GMAX; ++g)
-            if (g < G && !ll_ok(w0[g], w1[g], tag)) ll_load_raw(p + (size_t)g * stride, w0[g], w1[g]);
+            if (g < G && !ll_ok(w0[g], w1[g], tag)) ld2(p + (size_t)g * stride, w0[g], w1[g]);
     }
     double s = 0.0;
 #pragma unroll

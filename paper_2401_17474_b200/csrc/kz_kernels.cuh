@@ -50,6 +50,11 @@ struct SolveArgs {
     const double* x_sum;   // rka kernel, optional: x_k = x_sum / x_div (the all-reduced worker sum of the
     double x_div;          // previous row-sharded step) instead of x
     int wg;                // rka kernel: worker-group mode (cluster g runs workers [g q/G, (g+1) q/G))
+    // rka kernel, cross-rank mode (row-sharded multi-GPU in one launch): every rank's column sums
+    // go as tagged words into every rank's exchange buffer over NVLink peer memory
+    unsigned long long* const* xr_peers;  // device array: each rank's exchange buffer (own rank's is local)
+    int xr_ranks, xr_rank;
+    unsigned xr_tag0;      // tag of iteration k0 (unique across launches and solves of the communicator)
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
@@ -67,7 +72,9 @@ __global__ void sync_kernel(SolveArgs a);
 constexpr int RKA_NW = 8;                  // compute warps
 constexpr int RKA_NT = (RKA_NW + 1) * 32;  // + the producer warp
 constexpr int RKA_MAXG = 10;               // clusters exchanging through tagged words
-template <int LG, int EPL, bool TIMING, bool SR, bool WG>
+constexpr int RKA_MAXR = 8;                // ranks (GPUs of one node) exchanging column sums
+// MODE 0: column-sliced; 1: worker groups; 2: column-sliced + cross-rank column sums (kz_solve_sharded)
+template <int LG, int EPL, bool TIMING, bool SR, int MODE>
 __global__ void rka_kernel(const __grid_constant__ SolveArgs a, const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB);
 

@@ -48,7 +48,7 @@ constexpr unsigned XBAR = 2;  // named barrier: producer warp -> compute warps, 
 constexpr unsigned CBAR = 1;  // named barrier id of the compute warps
 }  // namespace
 
-template <int LG, int EPL, bool TIMING, bool SR, bool WG>
+template <int LG, int EPL, bool TIMING, bool SR, int MODE>
 __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ SolveArgs a,
                                                         const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB) {
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     // worker-group mode (a.wg): cluster g runs workers [wlo, wlo + q) over all columns (split over its
     // Pc CTAs) and the clusters add their per-column sums through tagged words; otherwise every
     // cluster runs all workers over its share of the columns and the clusters add dot totals
-    constexpr bool wg = WG;  // a separate instantiation: the column-sliced kernel keeps its register budget
+    constexpr bool wg = MODE == 1;  // separate instantiations: the column-sliced kernel keeps its register budget
+    constexpr bool xr = MODE == 2;  // cross-rank: local column slices, column sums exchanged between GPUs
     const int Gx = wg ? 1 : G;                      // clusters exchanging dot totals
     const int gx = wg ? 0 : gid;
     const int wlo = wg ? (int)((int64_t)gid * qa / G) : 0;
@@ -212,16 +213,18 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     const int we = wb + QB < q ? wb + QB : q;
     const int eown = Pc - 1;                                          // owner of the error total
     const bool gh = we - wb > grp * NR;  // this lane group owns at least one worker
-    const bool qpow2 = (qa & (qa - 1)) == 0;  // x = (sum over all qa workers) / qa
-    const double invq = 1.0 / (double)qa;     // RN(1/qa): exact for powers of two, Markstein otherwise
-    const double qd = (double)qa;
+    // x = (sum over all workers) / their count: qa here, q x ranks across GPUs
+    const double qd = xr ? a.x_div : (double)qa;
+    const int64_t qall = (int64_t)qd;
+    const bool qpow2 = (qall & (qall - 1)) == 0;
+    const double invq = 1.0 / qd;  // RN(1/Q): exact for powers of two, Markstein otherwise
     const bool ckpt_on = a.ckpt_every > 0;
     const int count = (int)a.count;
     const bool use_stop = opaque_i32(a.use_stop) != 0, final_check = opaque_i32(a.final_check) != 0;
     const int cnt2 = Pc >= 2 ? Pc / 2 : 1;  // partials per lane in the owner's tree (2 lanes per item)
     bool unit_alpha = true;
     for (int t = 0; t < q; ++t) unit_alpha = unit_alpha && alp[t] == 1.0;
-    const bool split = wg || (TIMING && (a.ablate & 16)) || cwb >= 64 || LG == 8;  // combine layout (see below)
+    const bool split = wg || xr || (TIMING && (a.ablate & 16)) || cwb >= 64 || LG == 8;  // combine layout
     const int ppw = ((wdt >> 1) + NW - 1) / NW;                      // column pairs per warp (split)
     const int u = lane & 1;
 
@@ -537,8 +540,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                          : make_double2(div_rn_fast(v.x, qd, invq), div_rn_fast(v.y, qd, invq));
         };
         double2 xn[EPL];
+        if constexpr (!xr) {  // cross-rank mode forms xn after the exchange (fewer live registers there)
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) xn[e] = xv[e];
+            for (int e = 0; e < EPL; ++e) xn[e] = xv[e];
+        }
         const bool ck = ckpt_on && (((a.k0 + kk + 1) % a.ckpt_every) == 0) &&
                         (((a.k0 + kk + 1) / a.ckpt_every) <= a.ckpt_cap);
         const int64_t ck_slot = ck ? (a.k0 + kk + 1) / a.ckpt_every - 1 : 0;
@@ -554,6 +559,21 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     const unsigned tag = (unsigned)kk + 1u;
                     ll_store(wl + ((size_t)gid * ld + c0 + j) * 2, v.x, tag);
                     ll_store(wl + ((size_t)gid * ld + c0 + j + 1) * 2, v.y, tag);
+                    continue;
+                }
+                if (xr) {
+                    // this GPU's column sums -> every rank's buffer, slot [par][this rank][column]
+                    // (NVLink peer stores; summed below in rank order, identical on every rank)
+                    // slot parity by the global iteration: consecutive launches keep alternating, so a
+                    // rank one iteration ahead never overwrites a slot another rank still polls
+                    const unsigned tag = a.xr_tag0 + (unsigned)kk;
+                    const int xpar = (int)((a.k0 + kk) & 1);
+                    const size_t off = ((size_t)(xpar * a.xr_ranks + a.xr_rank) * ld + c0 + j) * 2;
+                    for (int r = 0; r < a.xr_ranks; ++r) {
+                        unsigned long long* pb = a.xr_peers[r];
+                        ll_store_sys(pb + off, v.x, tag);
+                        ll_store_sys(pb + off + 2, v.y, tag);
+                    }
                     continue;
                 }
                 if (a.partial) {  // row-sharded step: un-normalised local sum
@@ -579,8 +599,25 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 xs[tid] = xj;
                 if (ck && gid == 0 && c0 + tid < a.n) a.ckpt[ck_slot * a.n + c0 + tid] = xj;
             }
+            if (xr && tid < wdt) {
+                // thread j adds the ranks' sums of column c0 + j in rank order
+                const unsigned long long* own =
+                    a.xr_peers[a.xr_rank] + (size_t)((a.k0 + kk) & 1) * a.xr_ranks * ld * 2;
+                // ranks polled four at a time (register budget), summed in rank order
+                const unsigned xtag = a.xr_tag0 + (unsigned)kk;
+                const unsigned long long* pw = own + (size_t)(c0 + tid) * 2;
+                double tot = ll_sum_inl<4, true>(pw, 2 * ld, a.xr_ranks < 4 ? a.xr_ranks : 4, xtag, &a.status->aborted);
+                if (a.xr_ranks > 4)
+                    tot = __dadd_rn(tot, ll_sum_inl<4, true>(pw + (size_t)8 * ld, 2 * ld, a.xr_ranks - 4, xtag,
+                                                              &a.status->aborted));
+                xs[tid] = qpow2 ? __dmul_rn(tot, invq) : div_rn_fast(tot, qd, invq);
+            }
             named_sync(CBAR, NW * 32);
-            if (!a.partial) {
+            if constexpr (xr) {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e)
+                    xn[e] = vld[e] ? *reinterpret_cast<const double2*>(xs + 2 * (gl + LG * e)) : xv[e];
+            } else if (!a.partial) {
 #pragma unroll
                 for (int e = 0; e < EPL; ++e)
                     if (vld[e]) xn[e] = *reinterpret_cast<const double2*>(xs + 2 * (gl + LG * e));
@@ -648,89 +685,117 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
     }
 }
 
-template __global__ void rka_kernel<8, 1, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, true, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, true, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, false, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 1, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, true, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, false, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 1, false, true, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, true, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<8, 2, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, true, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, false, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, true, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, false, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<8, 2, false, true, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<16, 1, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, true, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, true, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, false, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, true, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, false, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 1, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<16, 1, false, true, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, true, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, true, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, false, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 2, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, true, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, false, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 1, false, true, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, true, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 3, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, true, true, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, false, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, true, 1>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, true, false, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, false, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, true, true, false>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 2, false, true, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false, false, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 3, false, false, 0>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
-template __global__ void rka_kernel<32, 4, false, true, true>(const __grid_constant__ SolveArgs,
+template __global__ void rka_kernel<32, 3, false, true, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, true, false, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, true, true, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, false, 1>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, true, 1>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, false, 2>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 3, false, true, 2>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, false, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, true, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, true, false, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, true, true, 0>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, false, 1>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, true, 1>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, false, 2>(const __grid_constant__ SolveArgs,
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
+template __global__ void rka_kernel<32, 4, false, true, 2>(const __grid_constant__ SolveArgs,
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap);
 
 }  // namespace kz

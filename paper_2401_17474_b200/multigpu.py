@@ -149,7 +149,29 @@ class ShardComm:
             dist.broadcast_object_list(obj, src=0, group=group)
         h = C.c_void_p()
         N.check(self._lib.kz_comm_create(int(device), obj[0], int(world), int(rank), C.byref(h)))
-        self.handle, self.world, self.rank = h, world, rank
+        self.handle, self.world, self.rank, self.group = h, world, rank, group
+        self.exchange_ld = None
+
+    def connect_exchange(self, ld: int) -> None:
+        """The fused cross-rank exchange (kz_comm_exchange_*): every rank exports the IPC handle of
+        its column-sum buffer, the handles are all-gathered in rank order, every rank maps the
+        others' buffers.  Collective: all ranks call it with the same shard pitch."""
+        import ctypes as C
+
+        from . import _native as N
+
+        if self.exchange_ld == ld:
+            return
+        buf = C.create_string_buffer(N.COMM_HANDLE_BYTES)
+        N.check(self._lib.kz_comm_exchange_handle(self.handle, int(ld), buf))
+        handles = [bytes(buf.raw)]
+        if self.world > 1:
+            import torch.distributed as dist
+
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(buf.raw), group=self.group)
+        N.check(self._lib.kz_comm_exchange_connect(self.handle, b"".join(handles)))
+        self.exchange_ld = ld
 
     def close(self):
         if getattr(self, "handle", None):
@@ -163,17 +185,22 @@ class ShardComm:
             pass
 
 
-def solve_sharded_native(shard: "CudaShard", cfg, *, budget: int | None = None, comm: ShardComm | None = None
-                         ) -> RunReport:
-    """The same protocol as :func:`solve_sharded`, run by the library (kz_solve_sharded): the
-    local steps, NCCL all-reduces and averages of a chunk of outer iterations are enqueued on
-    one stream without a host round trip; a device stop flag freezes x at the stopping
-    iteration.  Bitwise the same x, errors and iteration counts as the host-driven loop."""
+def solve_sharded_native(shard: "CudaShard", cfg, *, budget: int | None = None, comm: ShardComm | None = None,
+                         fused: bool = True) -> RunReport:
+    """The same protocol as :func:`solve_sharded`, run by the library (kz_solve_sharded).
+    RKA with ``fused`` (default): one step-kernel launch per chunk of outer iterations, the
+    ranks' column sums exchanged inside the kernel over NVLink peer memory (the communicator's
+    exchange buffers) and the stop rule applied in-kernel.  Otherwise (RKAB, or fused=False):
+    per outer iteration a local step, an in-place NCCL all-reduce and x = S / Q, enqueued on one
+    stream without a host round trip; a device stop flag freezes x at the stopping iteration.
+    Same iteration counts as the host-driven loop; the same x bit for bit at one rank."""
     plan = shard.plan
     if comm is None and plan.world > 1:
         raise ValueError("a multi-rank sharded solve needs a ShardComm")
+    if comm is not None and fused and cfg.variant == "rka":
+        comm.connect_exchange(shard.ds.pitch)
     t0 = time.perf_counter()
-    r = shard.ds.solve_sharded(cfg, worker_offset=plan.worker_offset, comm=comm, budget=budget)
+    r = shard.ds.solve_sharded(cfg, worker_offset=plan.worker_offset, comm=comm, budget=budget, fused=fused)
     wall = time.perf_counter() - t0
     shard.rows += r["rows"]
     shard.kernel_ms += r["loop_ms"]
@@ -183,7 +210,8 @@ def solve_sharded_native(shard: "CudaShard", cfg, *, budget: int | None = None, 
                      converged=r["converged"], wall_time_s=wall, final_error_sq=r["final_error_sq"],
                      final_residual=float("nan"), error_evals=r["error_evals"], x=r["x"],
                      gpu={"world": plan.world, "q_local": plan.q_local, "shard": (plan.lo, plan.hi),
-                          "native": True, "loop_ms": r["loop_ms"], "launches": r["launches"]})
+                          "native": True, "fused": bool(fused and comm is not None and cfg.variant == "rka"),
+                          "loop_ms": r["loop_ms"], "launches": r["launches"]})
 
 
 def solve_sharded(shard, cfg, *, budget: int | None = None, group=None) -> RunReport:

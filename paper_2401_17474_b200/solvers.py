@@ -275,7 +275,7 @@ class DeviceSystem:
                 "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches)}
 
     def solve_sharded(self, cfg: "SolverConfig", *, worker_offset: int, comm=None, budget: int | None = None,
-                      alphas=None) -> dict:
+                      alphas=None, fused: bool = True) -> dict:
         """The whole row-sharded _drive loop of this shard natively (kz_solve_sharded): per outer
         iteration the local step, an in-place all-reduce of the worker sum over ``comm`` (a
         :class:`ShardComm`; None = one rank) and x = S / (q * world) with the stop rule on the
@@ -297,6 +297,7 @@ class DeviceSystem:
         p.kernel = N.KERNELS[cfg.kernel]
         p.threads, p.ctas = int(cfg.threads), int(cfg.ctas)
         p.worker_offset = int(worker_offset)
+        p.flags = 0 if fused else 1  # KZ_FLAG_NO_FUSED_EXCHANGE
         r = N.Result()
         x = np.empty(self.n, dtype=np.float64)
         N.check(self._lib.kz_solve_sharded(self.handle, None if comm is None else comm.handle, C.byref(p),

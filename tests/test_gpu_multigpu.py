@@ -155,3 +155,33 @@ def test_native_sharded_nccl_world1(gpu):
         comm.close()
     assert rn.converged and rn.iterations == rh.iterations
     assert np.array_equal(rn.x, rh.x)
+
+
+@pytest.mark.parametrize("n,budget", [(64, None), (4500, 40)])
+def test_fused_cross_rank_exchange_world1(gpu, oracle, n, budget):
+    """kz_solve_sharded's fused path (one launch per chunk, column sums through the communicator's
+    NVLink exchange buffers, stop rule in the kernel) at one rank: bit-identical to the
+    per-iteration loop, same iteration counts as the oracle; one and several local clusters."""
+    from paper_2401_17474_b200 import GeneratorConfig, SolverConfig, generate_mother
+    from paper_2401_17474_b200.multigpu import CudaShard, ShardComm, plan_shards, solve_sharded_native
+
+    s = _system() if n == 64 else generate_mother(GeneratorConfig(m_max=5000, n_max=n, seed=3))
+    q = 8
+    plan = plan_shards(s.m, 1, 0, q)
+    shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
+    comm = ShardComm(0, 1, 0)
+    try:
+        cfg = SolverConfig(variant="rka", q=q, base_seed=6, sampling_scheme="distributed")
+        rf = solve_sharded_native(shard, cfg, budget=budget, comm=comm)
+        rf2 = solve_sharded_native(shard, cfg.replace(base_seed=7), budget=budget, comm=comm)
+        rl = solve_sharded_native(shard, cfg, budget=budget, comm=comm, fused=False)
+    finally:
+        shard.close()
+        comm.close()
+    assert rf.gpu["fused"] and not rl.gpu["fused"]
+    assert rf.iterations == rl.iterations and rf.error_evals == rl.error_evals
+    assert np.array_equal(rf.x, rl.x)
+    o = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=q, base_seed=6, scheme="distributed", budget=budget)
+    assert rf.iterations == o["iterations"] and rel_err(rf.x, o["x"]) <= PARITY_TOL
+    o2 = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=q, base_seed=7, scheme="distributed", budget=budget)
+    assert rf2.iterations == o2["iterations"] and rel_err(rf2.x, o2["x"]) <= PARITY_TOL
