@@ -139,9 +139,11 @@ def run_reference(args, name, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
-        "config": {"workload": WORKLOADS[name][3], "m": m, "n": n, **kw, "seeds": "0..9 cycling"},
+        "config": {"workload": WORKLOADS[name][3] + f", {SEEDS} seeds per step", "m": m, "n": n, **kw,
+                   "seeds": "0..9 cycling"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full solves to eps (oracle/kz_oracle.c, pthreads x{cores})"},
+                         "sample": f"{args.steps} full solves to eps, one seed of the {SEEDS}-seed batch per step "
+                                   f"(a bounded sample; oracle/kz_oracle.c, pthreads x{cores} over the workers)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "iterations": iters,
     }
