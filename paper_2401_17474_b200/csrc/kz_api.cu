@@ -777,8 +777,8 @@ int chain_max_threads(int ep) { return ep <= 4 ? 256 : (ep <= 8 ? 384 : 320); }
 
 int chain_nv(int R) { return R + R * (R - 1) / 2 + R + 1; }
 
-int chain_smem(int64_t ldc, int stages, int R, int T) {
-    return (int)(144 + (2 * chain_nv(R) + 2) * sizeof(double) + stages * ldc * sizeof(double) +
+int chain_smem(int64_t ldc, int stages, int R, int T, int C = 2) {
+    return (int)(144 + (2 * std::max(C, 1) * chain_nv(R) + 2) * sizeof(double) + stages * ldc * sizeof(double) +
                  stages * 2 * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
                  ((size_t)chain_nv(R) * T + chain_nv(R) + 1) * sizeof(double));
 }
@@ -813,6 +813,11 @@ void* chain_fn(int ep, int R, int C) {
         case 20801: return (void*)chain_kernel<8, 1, 2>;
         case 20802: return (void*)chain_kernel<8, 2, 2>;
         case 21601: return (void*)chain_kernel<16, 1, 2>;
+                case 40104: return (void*)chain_kernel<1, 4, 4>;
+        case 40204: return (void*)chain_kernel<2, 4, 4>;
+        case 40404: return (void*)chain_kernel<4, 4, 4>;
+        case 80104: return (void*)chain_kernel<1, 4, 8>;
+        case 80204: return (void*)chain_kernel<2, 4, 8>;
         default: return nullptr;
     }
 }
@@ -833,7 +838,14 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     // a worker is one CTA, or a CTA pair (thread-block cluster of 2, each CTA
     // half the columns) when the rows are long and the pairs fit the SMs
     int C = (s->ld >= 1024 && 2 * q <= s->sms && !s->no_pairs) ? 2 : 1;  // measured: pairs win from n ~ 1000
-    if (const char* e = getenv("KZ_CHAIN_PAIR")) C = atoi(e) == 2 && 2 * q <= s->sms ? 2 : 1;
+    // one chain (RK, CK) over long rows: a cluster of 8 (measured on 80000 x 2000: 0.50 us per row
+    // against 0.54 for a pair and 0.58 for one CTA; at n = 512 the pair is best)
+    if (q == 1 && s->ld >= 1536 && s->ld % 16 == 0 && !s->no_pairs) C = 8;
+    if (const char* e = getenv("KZ_CHAIN_PAIR")) {  // experiment: 1, 2, or (one chain, q = 1) 4 / 8
+        const int want = atoi(e);
+        C = want == 2 && 2 * q <= s->sms ? 2 : ((want == 4 || want == 8) && q == 1 ? want : 1);
+    }
+    if (C > 2 && (s->ld % (2 * C) != 0 || s->no_pairs)) C = 2;  // column slices of whole 16-byte pairs
     const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
     int ep = 0, T = 0;
@@ -856,19 +868,20 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     // rows per reduction: as many as registers allow (EP small) and the ring holds (> R rows)
     int R = ep <= 4 ? 4 : (ep == 8 ? 2 : 1);  // R = 8 measured slower since the reduction got cheap
     if (C == 2) R = std::min(R, 4);
+    if (C > 2) R = std::min(R, 4);
     if (const char* e = getenv("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
     const int64_t ldc = s->ld / C;
     const int64_t stage_bytes = ldc * (int64_t)sizeof(double);
     int stages = 0;
     for (;;) {
         while (R > 1 && !chain_fn(ep, R, C)) R /= 2;
-        const int64_t fixed = chain_smem(ldc, 0, R, T);
+        const int64_t fixed = chain_smem(ldc, 0, R, T, C);
         stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
         if (const char* e = getenv("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
         if (stages >= R + 1 || R == 1) break;
         R = R > 4 ? 4 : (R > 2 ? 2 : 1);
     }
-    if (stages < 1 || (size_t)chain_smem(ldc, stages, R, T) > kSmemLimit)
+    if (stages < 1 || (size_t)chain_smem(ldc, stages, R, T, C) > kSmemLimit)
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
     void* fn = chain_fn(ep, R, C);
     if (!fn) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d C=%d", ep, R, C);
@@ -878,7 +891,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     pl.rows = R;
     pl.pair = C;
     pl.stages = stages;
-    pl.smem = chain_smem(ldc, stages, R, T);
+    pl.smem = chain_smem(ldc, stages, R, T, C);
     pl.ctas = (int)(q * C);
     KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (pl.ctas > 1) {
@@ -1251,9 +1264,9 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
             attr2[na].val.cooperative = 1;
             ++na;
         }
-        if (pl.pair == 2) {
+        if (pl.pair >= 2) {
             attr2[na].id = cudaLaunchAttributeClusterDimension;
-            attr2[na].val.clusterDim.x = 2;
+            attr2[na].val.clusterDim.x = pl.pair;
             attr2[na].val.clusterDim.y = 1;
             attr2[na].val.clusterDim.z = 1;
             ++na;
@@ -1474,7 +1487,7 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
     if (pl.tma && pl.ctas > pl.cluster)
         KZ_CUDA(cudaMemsetAsync(s->ll.p, 0, s->ll_words * sizeof(unsigned long long), st));
     int lrc = launch_solve(s, pl, args, st);
-    if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair == 2 && first) {
+    if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair >= 2 && first) {
         // CTA-pair clusters not launchable cooperatively here: one CTA per worker
         s->no_pairs = true;  // remembered for this system (no process-wide side effects)
         KZ_TRY(plan_chain(s, p, q, pl));

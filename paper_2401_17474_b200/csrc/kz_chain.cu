@@ -135,16 +135,16 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     const int D = a.stages;
     const int64_t ld = a.ld, q = a.q, bs = a.bs;
-    // C == 2: a worker is a CTA pair (thread-block cluster); CTA h owns columns
-    // [h*ld/2, (h+1)*ld/2) and the two halves of every reduction are joined
-    // through distributed shared memory (st.async + mbarrier).
-    const int h = (C == 2) ? (int)cluster_rank() : 0;
+    // C >= 2: a worker is a thread-block cluster of C CTAs (a pair for RKAB's long rows, up to
+    // 8 for one long RK chain); CTA h owns columns [h*ld/C, (h+1)*ld/C) and the C slices of
+    // every reduction are joined through distributed shared memory (st.async + mbarrier).
+    const int h = (C >= 2) ? (int)cluster_rank() : 0;
     const int64_t ldc = ld / C, cb = h * ldc;  // this CTA's columns
     ChainSmem sm;
     unsigned long long* xbar = reinterpret_cast<unsigned long long*>(smem_raw);  // 2 exchange mbarriers
     unsigned long long* full = xbar + 2;                                         // 16 row-stage mbarriers
-    double* xbuf = reinterpret_cast<double*>(smem_raw + 144);                     // 2 x NVC partner totals
-    sm.ring = xbuf + 2 * Blk<R>::NVC + 2;
+    double* xbuf = reinterpret_cast<double*>(smem_raw + 144);                     // 2 x C x NVC peer totals
+    sm.ring = xbuf + 2 * C * Blk<R>::NVC + 2;
     sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ldc);
     sm.win = reinterpret_cast<int32_t*>(sm.bsq + D);
     sm.scr = reinterpret_cast<double*>(sm.win + IDX_WINDOW);
@@ -156,9 +156,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         fence_mbarrier_init_cluster();
     }
     __syncthreads();
-    if (C == 2) cluster_sync_all();
-    int nex = 0;  // pair exchanges done
-    const unsigned partner = (unsigned)(h ^ 1);
+    if (C >= 2) cluster_sync_all();
+    int nex = 0;  // cluster exchanges done
 
     const int64_t w = blockIdx.x / C;  // worker id
     const int32_t* idx = a.idx + w * a.idx_stride;
@@ -225,19 +224,27 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     };
 
     // direct ||v - x_ref||^2 over the CTA
-    // join the two halves of a CTA pair: totals += partner's totals (IEEE
-    // addition is commutative, so both CTAs hold the same bits)
+    // join the C slices of a reduction: every CTA sends its totals to every peer (slot
+    // [parity][sender][value]) and adds the C totals in CTA order, so all hold the same bits
+    // (for a pair the order is immaterial: IEEE addition is commutative)
     auto pair_join = [&](double* vals, int nv) {
-        if (C != 2) return;
+        if (C < 2) return;
         const int xp = nex & 1;
         const unsigned ph = (unsigned)((nex >> 1) & 1);
         ++nex;
-        if (tid == 0) mbar_arrive_expect_tx(&xbar[xp], (unsigned)(nv * sizeof(double)));
-        if (tid < nv)
-            st_async_f64(mapa_u32(smem_u32(xbuf + xp * Blk<R>::NVC + tid), partner), sm.tot[tid],
-                         mapa_u32(smem_u32(&xbar[xp]), partner));
+        if (tid == 0) mbar_arrive_expect_tx(&xbar[xp], (unsigned)((C - 1) * nv * sizeof(double)));
+        for (int i = tid; i < (C - 1) * nv; i += T) {
+            const int vi = i % nv, pk = i / nv;
+            const unsigned peer = (unsigned)(pk < h ? pk : pk + 1);
+            st_async_f64(mapa_u32(smem_u32(xbuf + (xp * C + h) * Blk<R>::NVC + vi), peer), sm.tot[vi],
+                         mapa_u32(smem_u32(&xbar[xp]), peer));
+        }
         mbar_wait_cluster(&xbar[xp], ph);
-        for (int i = 0; i < nv; ++i) vals[i] = __dadd_rn(vals[i], xbuf[xp * Blk<R>::NVC + i]);
+        for (int i = 0; i < nv; ++i) {
+            double acc = h == 0 ? vals[i] : xbuf[(xp * C) * Blk<R>::NVC + i];
+            for (int c = 1; c < C; ++c) acc = __dadd_rn(acc, c == h ? vals[i] : xbuf[(xp * C + c) * Blk<R>::NVC + i]);
+            vals[i] = acc;
+        }
     };
 
     auto err_direct = [&]() {
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             if (lc < ldc) __stcg(reinterpret_cast<double2*>(dst + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
         }
     }
-    if (C == 2) cluster_sync_all();  // no DSMEM traffic may target an exited CTA
+    if (C >= 2) cluster_sync_all();  // no DSMEM traffic may target an exited CTA
     if (blockIdx.x == 0 && tid == 0) {
         a.status->iters_done = done;
         a.status->converged = conv;
@@ -552,6 +559,12 @@ KZ_CHAIN(4, 4, 2)
 KZ_CHAIN(8, 1, 2)
 KZ_CHAIN(8, 2, 2)
 KZ_CHAIN(16, 1, 2)
+// one long RK / CK chain over a cluster of 4 or 8 CTAs (q = 1)
+KZ_CHAIN(1, 4, 4)
+KZ_CHAIN(2, 4, 4)
+KZ_CHAIN(4, 4, 4)
+KZ_CHAIN(1, 4, 8)
+KZ_CHAIN(2, 4, 8)
 #undef KZ_CHAIN
 
 }  // namespace kz

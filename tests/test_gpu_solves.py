@@ -426,3 +426,26 @@ def test_run_distributed_solve_matches_reference(gpu, systems, tag):
     every = int(g[f"{tag}_every"])
     for j, ck in enumerate(g[f"{tag}_ckpt"]):
         assert rel_err(caps[0][every * (j + 1) - 1], ck) <= PARITY_TOL, j
+
+
+@pytest.mark.parametrize("variant", ["rk", "ck"])
+def test_chain_cluster_of_8_matches_oracle(gpu, oracle, variant):
+    """One long chain (RK / CK, n >= 1536) runs on a cluster of 8 CTAs, each a column slice, the
+    Gram-block reductions joined all-to-all over DSMEM in CTA order: iterates vs the oracle."""
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, generate_mother, run_solver
+
+    s = generate_mother(GeneratorConfig(m_max=6000, n_max=2000, seed=9))
+    budget = 3000
+    o = oracle.solve(s.A, s.b, s.x_star, variant=variant, base_seed=4, budget=budget, ckpt_every=500)
+    with DeviceSystem(s) as ds:
+        cap = []
+        r = run_solver(ds, _cfg(variant=variant, base_seed=4), budget=budget, capture=cap)
+        assert r.gpu["ctas"] == 8, r.gpu
+        r2 = run_solver(ds, _cfg(variant=variant, base_seed=4, max_iterations=200000))
+    assert rel_err(r.x, o["x"]) <= PARITY_TOL
+    for j, ck in enumerate(o["checkpoints"]):
+        assert rel_err(cap[500 * (j + 1) - 1], ck) <= PARITY_TOL, j
+    o2 = oracle.solve(s.A, s.b, s.x_star, variant=variant, base_seed=4, max_iterations=200000)
+    assert r2.iterations == o2["iterations"] and r2.converged == o2["converged"]
+    assert r2.error_evals == o2["error_evals"]
+    assert rel_err(r2.x, o2["x"]) <= PARITY_TOL
