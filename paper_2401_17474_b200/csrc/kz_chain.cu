@@ -330,6 +330,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             if (sl >= D) sl -= D;
             bq = sm.bsq[sl];
         }
+        // (b_r, sq_r) sit in lane r; 1/sq_r formed there now (off the critical path: the division
+        // overlaps the partial dots and the reduction)
+        const double inv_l = 1.0 / bq.y;
         double vals[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) vals[i] = 0.0;
@@ -362,17 +365,21 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw);
         pair_join(vals, NV);
         if (rec) a.dbg[nblk * 8 + 4] = clock64();
-        // (b_r, sq_r) sit in lane r; 1/sq_r formed there and shuffled to all
-        const double inv_l = 1.0 / bq.y;
+        // every row's (b, sq, 1/sq) to all lanes up front: the shuffles leave the sequential chain
+        double brs[R], sqrs[R], invrs[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            brs[r] = __shfl_sync(0xffffffffu, bq.x, r);
+            sqrs[r] = __shfl_sync(0xffffffffu, bq.y, r);
+            invrs[r] = __shfl_sync(0xffffffffu, inv_l, r);
+        }
         double s[R];
         int Reff = Rp;
         double e = CHECK ? vals[NV - 1] : 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (r < Reff) {
-                const double br = __shfl_sync(0xffffffffu, bq.x, r);
-                const double sqr = __shfl_sync(0xffffffffu, bq.y, r);
-                const double invr = __shfl_sync(0xffffffffu, inv_l, r);
+                const double br = brs[r], sqr = sqrs[r], invr = invrs[r];
                 double dr = vals[r];
 #pragma unroll
                 for (int l = 0; l < r; ++l) dr = fma(s[l], vals[R + gidx(r, l)], dr);
