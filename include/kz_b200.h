@@ -114,6 +114,10 @@ KZ_API int32_t kz_system_view_refresh(kz_system* view);
  * the system.  Returns KZ_EDEGENERATE with *bad_row = first zero row.
  * sq_host (m values) may be NULL. */
 KZ_API int32_t kz_row_norms(kz_system* sys, double* sq_host, int64_t* bad_row, void* stream);
+/* Host-computed squared row norms (m values) replace the device computation -- the fallback of
+ * SURVEY Appendix A when the host numpy's einsum summation order differs from the one the device
+ * kernel restates (sysgen.einsum_order_matches); sampler and packed records are rebuilt from them. */
+KZ_API int32_t kz_row_norms_upload(kz_system* sys, const double* sq_host, void* stream);
 
 /* ---- sampler: make_sampler / worker_streams (sampling.py:189-199,
  * solvers.py:162-171) ------------------------------------------------------

@@ -35,7 +35,7 @@ EXPORTS = (
     "kz_average_from", "kz_error_sq", "kz_solution_host", "kz_set_x", "kz_solution_device", "kz_norms",
     "kz_cgls", "kz_spectral", "kz_system_load_file", "kz_generate_counter_rows",
     "kz_comm_unique_id", "kz_comm_create", "kz_comm_destroy", "kz_solve_sharded", "kz_system_view",
-    "kz_system_view_refresh", "kz_comm_exchange_handle", "kz_comm_exchange_connect",
+    "kz_system_view_refresh", "kz_comm_exchange_handle", "kz_comm_exchange_connect", "kz_row_norms_upload",
 )
 COMM_HANDLE_BYTES = 64
 COMM_ID_BYTES = 128
@@ -140,6 +140,7 @@ def load_library():
         L.kz_set_x.argtypes = [vp, _dp, vp]
         L.kz_norms.argtypes = [vp, _dp, _dp, _dp, vp]
         L.kz_system_view.argtypes = [vp, C.POINTER(vp)]
+        L.kz_row_norms_upload.argtypes = [vp, _dp, vp]
         L.kz_system_view_refresh.argtypes = [vp]
         L.kz_comm_unique_id.argtypes = [C.c_char_p]
         L.kz_comm_create.argtypes = [C.c_int32, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(vp)]

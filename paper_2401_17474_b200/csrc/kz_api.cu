@@ -450,6 +450,28 @@ static int ensure_norms(kz_system* s, cudaStream_t st) {
     return KZ_OK;
 }
 
+extern "C" int32_t kz_row_norms_upload(kz_system* s, const double* sq_host, void* stream) {
+    if (!s || !sq_host) return fail(KZ_EINVAL, "null argument");
+    KZ_NOT_VIEW(s);
+    cudaStream_t st = pick_stream(s, stream);
+    KZ_CUDA(cudaSetDevice(s->device));
+    KZ_CUDA(cudaMemcpyAsync(s->sq.p, sq_host, s->m * sizeof(double), cudaMemcpyHostToDevice, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    s->bad_row = -1;
+    for (int64_t i = 0; i < s->m; ++i)
+        if (sq_host[i] == 0.0) {
+            s->bad_row = i;
+            break;
+        }
+    s->norms_valid = true;
+    s->bs2_valid = false;
+    s->sampler_scheme = -1;
+    if (s->bad_row >= 0)
+        return fail(KZ_EDEGENERATE, "row %lld has zero norm; sampling probabilities and projection denominators "
+                    "are undefined for zero rows", (long long)s->bad_row);
+    return KZ_OK;
+}
+
 extern "C" int32_t kz_row_norms(kz_system* s, double* sq_host, int64_t* bad_row, void* stream) {
     if (!s) return fail(KZ_EINVAL, "null system");
     cudaStream_t st = pick_stream(s, stream);

@@ -23,7 +23,7 @@ import numpy as np
 from . import _native as N
 from .errors import DimensionMismatchError
 from .reports import RunReport, TraceRecord
-from .sysgen import LinearSystem, cgls_solve, partition_bounds
+from .sysgen import LinearSystem, cgls_solve, einsum_order_matches, partition_bounds
 
 VARIANTS = ("ck", "rk", "rka", "rkab", "cgls")
 ALPHA_POLICIES = ("unit", "fixed", "optimal_full", "optimal_partial")
@@ -145,6 +145,19 @@ class DeviceSystem:
         N.check(self._lib.kz_system_upload(self.handle, N.ptr(A), self.n, N.ptr(b),
                                            N.ptr(xr) if xr is not None else None, stream))
         self._xref_set = xr is not None
+        if not einsum_order_matches():  # another numpy build: the reference's own norms (Appendix A)
+            self.set_row_norms(np.einsum("ij,ij->i", A, A))
+        self._refresh_views()
+
+    def set_row_norms(self, sq) -> None:
+        """Host-computed squared row norms replace the device's (kz_row_norms_upload); a zero norm
+        surfaces as DegenerateRowError at solve time, as in the reference."""
+        sq = N.f64(sq)
+        if sq.shape != (self.m,):
+            raise DimensionMismatchError(f"expected length {self.m}, got {sq.shape}")
+        rc = self._lib.kz_row_norms_upload(self.handle, N.ptr(sq), None)
+        if rc != N.KZ_EDEGENERATE:
+            N.check(rc)
         self._refresh_views()
 
     def upload_device(self, A_ptr: int, lda: int, b_ptr: int, xref_ptr: int | None = None, stream=None) -> None:

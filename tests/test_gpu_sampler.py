@@ -98,3 +98,24 @@ def test_degenerate_and_empty_ranges(gpu):
     with DeviceSystem(LinearSystem(A=a, b=np.ones(3), x_star=np.ones(3))) as ds:
         with pytest.raises(EmptyRangeError):
             ds.cdf("distributed", 4)
+
+
+def test_uploaded_row_norms(gpu, systems):
+    """kz_row_norms_upload: host norms (the Appendix-A fallback for another numpy build) drive the
+    sampler exactly like the device norms when they agree; a zero norm is DegenerateRowError."""
+    import numpy as np
+
+    from paper_2401_17474_b200 import DegenerateRowError, DeviceSystem, SolverConfig, run_solver
+
+    s = systems["c0"]
+    cfg = SolverConfig(variant="rka", q=4, base_seed=3)
+    with DeviceSystem(s) as ds:
+        a = run_solver(ds, cfg)
+        ds.set_row_norms(np.einsum("ij,ij->i", s.A, s.A))
+        b = run_solver(ds, cfg)
+        assert a.iterations == b.iterations and np.array_equal(a.x, b.x)
+        sq = np.einsum("ij,ij->i", s.A, s.A)
+        sq[17] = 0.0
+        ds.set_row_norms(sq)
+        with pytest.raises(DegenerateRowError):
+            run_solver(ds, cfg)

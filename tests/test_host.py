@@ -143,3 +143,17 @@ def test_kzsys_round_trip_and_reference_files(tmp_path):
     bad.write_bytes(open(p, "rb").read()[:-8])
     with pytest.raises(SystemFormatError):
         G.load_system(bad)
+
+
+def test_einsum_order_restatement_matches_reference_norms():
+    """sysgen.einsum_row_norms (the order row_sqnorm_kernel restates) equals the reference's
+    row_norm_cache bitwise on the golden matrices, and this numpy's einsum agrees with it."""
+    from conftest import golden
+    from golden.common import NORM_WIDTHS, norm_matrix
+
+    from paper_2401_17474_b200.sysgen import einsum_order_matches, einsum_row_norms
+
+    g = golden("norms.npz")
+    for n in NORM_WIDTHS:
+        assert np.array_equal(einsum_row_norms(norm_matrix(n)), g[f"sq_{n}"]), n
+    assert einsum_order_matches()
