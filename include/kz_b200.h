@@ -53,7 +53,8 @@ enum kz_kernel {                                                  /* engine sele
     KZ_KERNEL_AUTO = 0,
     KZ_KERNEL_CHAIN = 1,        /* worker-per-CTA persistent kernel (RK, RKAB)                   */
     KZ_KERNEL_SYNC_CLUSTER = 2, /* column-sliced kernel, one thread-block cluster, DSMEM reduce  */
-    KZ_KERNEL_SYNC_GRID = 3     /* column-sliced kernel, whole grid, global-memory reduce        */
+    KZ_KERNEL_SYNC_GRID = 3,    /* column-sliced kernel, whole grid, global-memory reduce        */
+    KZ_KERNEL_WARP = 4          /* one warp, register-resident x: RK / CK on rows of <= 256 columns */
 };
 
 typedef struct kz_system kz_system;

@@ -814,6 +814,10 @@ size_t sync_smem(int64_t q, int64_t cw, int stages, int P, bool cluster) {
            nwarp * sizeof(double) + q * sizeof(double) + 8 * q * sizeof(int32_t);
 }
 
+void* rkw_fn(int epl) {
+    return epl == 1 ? (void*)rkw_kernel<1, 8> : epl == 2 ? (void*)rkw_kernel<2, 8> : (void*)rkw_kernel<4, 8>;
+}
+
 void* chain_fn(int ep, int R, int C) {
     switch (C * 10000 + ep * 100 + R) {
         case 10101: return (void*)chain_kernel<1, 1, 1>;
@@ -1316,6 +1320,10 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
         attr[0].val.cooperative = 1;
         cfg.numAttrs = 1;
     }
+    if (pl.kernel == KZ_KERNEL_WARP) {
+        fn = rkw_fn(pl.ep);
+        cfg.numAttrs = 0;
+    }
     void* kargs[] = {&args, &s->tmA, &s->tmB};
     cudaError_t e = cudaLaunchKernelExC(&cfg, fn, kargs);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1391,7 +1399,11 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     Plan pl;
     int kern = p->kernel;
     if (kern == KZ_KERNEL_AUTO) {
-        if (q == 1 || bs > 1) {
+        if (q == 1 && bs == 1 && s->ld <= 128 && p->partial_dev == nullptr && p->threads == 0) {
+            // short rows: one warp beats the chain kernel's block machinery (measured, budget mode:
+            // n = 50 0.32 vs 0.38 us per row, n = 120 0.35 vs 0.36; the chain wins from n ~ 250)
+            kern = KZ_KERNEL_WARP;
+        } else if (q == 1 || bs > 1) {
             kern = KZ_KERNEL_CHAIN;
         } else {
             kern = KZ_KERNEL_SYNC_CLUSTER;  // one or several clusters; grid barrier as the fallback
@@ -1403,10 +1415,19 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         memcpy(&pl, s->plan_blob, sizeof(Plan));  // same shape as the previous call: reuse its plan
         // the dynamic shared-memory limit is a property of the kernel function, which another
         // system may have lowered since: restore it for this plan
-        void* fn = pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair)
+        void* fn = pl.kernel == KZ_KERNEL_WARP    ? rkw_fn(pl.ep)
+                   : pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair)
                    : pl.tma                     ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg ? 1 : (pl.xr ? 2 : 0))
                                                 : sync_fn(pl.kernel == KZ_KERNEL_SYNC_CLUSTER, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    } else if (kern == KZ_KERNEL_WARP) {
+        if (q != 1 || bs != 1 || s->ld > 256)
+            return fail(KZ_EINVAL, "the warp kernel runs RK / CK on rows of at most 256 columns");
+        pl.kernel = KZ_KERNEL_WARP;
+        pl.ep = s->ld <= 64 ? 1 : (s->ld <= 128 ? 2 : 4);
+        pl.ctas = 1;
+        pl.threads = 32;
+        pl.smem = 0;
     } else if (kern == KZ_KERNEL_CHAIN) {
         KZ_TRY(plan_chain(s, p, q, pl));
     } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {

@@ -62,6 +62,10 @@ struct SolveArgs {
 template <int EP, int R, int C>
 __global__ void chain_kernel(SolveArgs a);
 
+// one-warp RK / CK kernel for short rows (n <= 64 EPL); P rows prefetched in registers
+template <int EPL, int P>
+__global__ void rkw_kernel(SolveArgs a);
+
 // sync kernel: column-sliced (RKA, RKAB bs=1).  CLUSTER: reduce via DSMEM.
 template <bool CLUSTER, int LPR>
 __global__ void sync_kernel(SolveArgs a);

@@ -449,3 +449,24 @@ def test_chain_cluster_of_8_matches_oracle(gpu, oracle, variant):
     assert r2.iterations == o2["iterations"] and r2.converged == o2["converged"]
     assert r2.error_evals == o2["error_evals"]
     assert rel_err(r2.x, o2["x"]) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("n", [50, 120, 250])
+def test_warp_kernel_matches_oracle(gpu, oracle, n):
+    """The one-warp RK kernel (short rows; register ring, per-row butterflies) vs the oracle:
+    stop mode with checkpoints, and budget mode, at each EPL width."""
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, generate_mother, run_solver
+
+    s = generate_mother(GeneratorConfig(m_max=3000, n_max=n, seed=n))
+    o = oracle.solve(s.A, s.b, s.x_star, variant="rk", base_seed=5, ckpt_every=50, max_iterations=400000)
+    ob = oracle.solve(s.A, s.b, s.x_star, variant="rk", base_seed=6, budget=777)
+    with DeviceSystem(s) as ds:
+        cap = []
+        r = run_solver(ds, _cfg(variant="rk", base_seed=5, kernel="warp", max_iterations=400000), capture=cap)
+        rb = run_solver(ds, _cfg(variant="rk", base_seed=6, kernel="warp"), budget=777)
+    assert r.gpu["kernel"] == "warp"
+    assert r.iterations == o["iterations"] and r.converged == o["converged"] and r.error_evals == o["error_evals"]
+    assert rel_err(r.x, o["x"]) <= PARITY_TOL
+    for j, ck in enumerate(o["checkpoints"][:200]):
+        assert rel_err(cap[50 * (j + 1) - 1], ck) <= PARITY_TOL, j
+    assert rb.iterations == 777 and rel_err(rb.x, ob["x"]) <= PARITY_TOL
