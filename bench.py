@@ -147,7 +147,7 @@ def run_reference(args, name, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "iterations": iters,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def _oracle_kw(kw):
@@ -483,10 +483,25 @@ def run_b200(args, name, rank, world, local_rank):
             for w in line["extra_workloads"] if w.get("workload", "").endswith("_to_eps")]
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(name, system, kw)
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None  # the process's original stdout: the one JSON line goes there, everything else to stderr
+
+
+def emit(line) -> None:
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    # libraries print to stdout at the C level (e.g. NCCL's version banner): keep stdout for the
+    # JSON line only by pointing fd 1 at stderr for the rest of the run
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
