@@ -659,7 +659,7 @@ def _run_cgls(system, cfg, x_ref):
                      final_error_sq=err * err if x_ref is not None else float("nan"), final_residual=res, x=x)
 
 
-DEFAULT_LANES = 7  # 16-CTA thread-block clusters co-resident on one B200 (the rka kernel's unit)
+DEFAULT_LANES = 10  # measured best for c1 (7 co-resident 16-CTA clusters; chunk boundaries interleave the rest)
 
 
 def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None) -> list[RunReport]:
