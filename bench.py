@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -404,6 +405,17 @@ def run_b200(args, name, rank, world, local_rank):
         dist.all_reduce(rr, op=dist.ReduceOp.SUM)
         tot_rows = float(rr.item())
         dist.barrier()
+    # the reference protocol's replay leg (harness.py:152-177): budget = ceil(mean iterations to eps),
+    # fixed-budget replays with the stop rule off, one solve at a time
+    budget = int(math.ceil(float(np.mean(iters))))
+    rep_ms = []
+    for k in range(3):
+        rr_ = run_solver(ds, cfg.replace(base_seed=base + k), budget=budget)
+        assert rr_.error_evals == 0
+        rep_ms.append(rr_.gpu["loop_ms"])
+    replay = {"budget": budget, "ms_per_run": float(np.mean(rep_ms)),
+              "rows_per_s": budget * _rows_per_iter(kw) / (float(np.mean(rep_ms)) / 1e3),
+              "note": "timed_replay protocol: one solve at a time, stop rule off"}
     ds.close()
 
     # e2e through the public API with pinned host arrays: per step the H2D upload of A, b, x*,
@@ -460,6 +472,7 @@ def run_b200(args, name, rank, world, local_rank):
                            "in_batch_mean": float(np.mean(solve_ms)), "in_batch_max": float(np.max(solve_ms)),
                            "batch_of_10_mean": float(np.mean(step_ms))},
         "iterations": iters,
+        "replay": replay,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_detail": traffic_note, "peak_source": peak_src,
                      "kernel": f"kz::rka/chain ({kernel_name})",
