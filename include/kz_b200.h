@@ -171,6 +171,9 @@ typedef struct {
 /* kz_params.flags: kz_solve_sharded keeps the per-iteration NCCL all-reduce even when the
  * communicator's fused cross-rank exchange is connected. */
 #define KZ_FLAG_NO_FUSED_EXCHANGE 1
+/* kz_params.flags: stop-mode launches of at most 2048 outer iterations (instead of growing to
+ * the index buffer's capacity) -- for solves running side by side on one GPU. */
+#define KZ_FLAG_SHORT_LAUNCHES 2
 
 typedef struct {
     int64_t iterations;     /* RunReport.iterations                                           */

@@ -56,6 +56,7 @@ class SolverConfig:
     device: int = 0
     threads: int = 0  # CTA size override (0 = auto)
     ctas: int = 0     # CTA count override for the sync kernels (0 = auto)
+    short_launches: bool = False  # stop mode: 2048-iteration launches (set by solve_concurrent)
 
     def validate(self) -> None:
         if self.variant not in VARIANTS:
@@ -553,6 +554,7 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
         p.kernel = N.KERNELS[cfg.kernel]
         p.threads = int(cfg.threads)
         p.ctas = int(cfg.ctas)
+        p.flags = 2 if cfg.short_launches else 0  # KZ_FLAG_SHORT_LAUNCHES
         p.want_residual = 1
         r = N.Result()
         x = np.empty(ds.n)
@@ -690,7 +692,8 @@ def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None) -> 
 
         def lane(i):
             for j in range(i, len(cfgs), n_lanes):
-                out[j] = run_solver(views[i], cfgs[j], budget=budget)
+                c = cfgs[j].replace(short_launches=True) if n_lanes > 1 else cfgs[j]
+                out[j] = run_solver(views[i], c, budget=budget)
 
         with ThreadPoolExecutor(n_lanes) as pool:
             for f in [pool.submit(lane, i) for i in range(n_lanes)]:
