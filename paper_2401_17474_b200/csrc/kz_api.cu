@@ -795,12 +795,12 @@ struct Plan {
 };
 
 const int kChainEP[] = {1, 2, 4, 8, 16};
-int chain_max_threads(int ep) { return ep <= 4 ? 256 : (ep <= 8 ? 384 : 320); }
+int chain_max_threads(int ep) { return ep <= 8 ? 128 : 320; }  // compute threads (kz_chain.cu ChainMaxThreads)
 
 int chain_nv(int R) { return R + R * (R - 1) / 2 + R + 1; }
 
 int chain_smem(int64_t ldc, int stages, int R, int T, int C = 2) {
-    return (int)(144 + (2 * std::max(C, 1) * chain_nv(R) + 2) * sizeof(double) + stages * ldc * sizeof(double) +
+    return (int)(288 + (2 * std::max(C, 1) * chain_nv(R) + 2) * sizeof(double) + stages * ldc * sizeof(double) +
                  stages * 2 * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
                  ((size_t)chain_nv(R) * T + chain_nv(R) + 1) * sizeof(double));
 }
@@ -912,7 +912,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     void* fn = chain_fn(ep, R, C);
     if (!fn) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d C=%d", ep, R, C);
     pl.kernel = KZ_KERNEL_CHAIN;
-    pl.threads = T;
+    pl.threads = T + 32;  // + the producer warp
     pl.ep = ep;
     pl.rows = R;
     pl.pair = C;
@@ -922,7 +922,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (pl.ctas > 1) {
         int per_sm = 0;
-        KZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, T, pl.smem));
+        KZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, T + 32, pl.smem));
         if ((int64_t)per_sm * s->sms < pl.ctas)
             return fail(KZ_EINVAL, "q=%lld workers exceed the %d co-resident CTAs of the chain kernel", (long long)q,
                         per_sm * s->sms);

@@ -98,7 +98,7 @@ __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double*
         for (int j = 0; j < PER; ++j)
             if (lane * PER + j < NV) scr[warp * NP + lane * PER + j] = w[j];
     }
-    __syncthreads();
+    named_sync(1, T);  // the compute threads (the producer warp is not in the reduction)
     for (int u = tid; u < NV; u += T) {
         double a[16];
 #pragma unroll
@@ -109,7 +109,7 @@ __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double*
             for (int k = 0; k + hh < 16; k += 2 * hh) a[k] = __dadd_rn(a[k], a[k + hh]);
         tot[u] = a[0];
     }
-    __syncthreads();
+    named_sync(1, T);
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = tot[i];
 }
@@ -124,15 +124,30 @@ struct FalseT {
 }  // namespace
 
 template <int EP>
-struct ChainMaxThreads {
-    static constexpr int value = EP <= 4 ? 256 : (EP <= 8 ? 384 : 320);
+struct ChainMaxThreads {  // compute threads; the CTA adds one producer warp
+    static constexpr int value = EP <= 8 ? 128 : 320;  // the plan keeps CTAs <= 128 threads below EP 16
 };
 
+// grid barrier over the compute threads of every CTA (the producer warps keep streaming)
+__device__ __forceinline__ void grid_barrier_c(unsigned* counter, unsigned target, int T) {
+    named_sync(1, T);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(counter) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(counter) : "memory");
+        } while (v < target);
+    }
+    named_sync(1, T);
+}
+
 template <int EP, int R, int C>
-__global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
-    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
+    // compute threads T = blockDim - 32; the last warp is the producer (row ring issue)
+    const int T = (int)blockDim.x - 32, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
     const int D = a.stages;
     const int64_t ld = a.ld, q = a.q, bs = a.bs;
     // C >= 2: a worker is a thread-block cluster of C CTAs (a pair for RKAB's long rows, up to
@@ -143,7 +158,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     ChainSmem sm;
     unsigned long long* xbar = reinterpret_cast<unsigned long long*>(smem_raw);  // 2 exchange mbarriers
     unsigned long long* full = xbar + 2;                                         // 16 row-stage mbarriers
-    double* xbuf = reinterpret_cast<double*>(smem_raw + 144);                     // 2 x C x NVC peer totals
+    unsigned long long* empty = full + 16;                                       // 16 stage releases
+    volatile int* halt = reinterpret_cast<volatile int*>(smem_raw + 272);        // compute done
+    double* xbuf = reinterpret_cast<double*>(smem_raw + 288);                     // 2 x C x NVC peer totals
     sm.ring = xbuf + 2 * C * Blk<R>::NVC + 2;
     sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ldc);
     sm.win = reinterpret_cast<int32_t*>(sm.bsq + D);
@@ -152,7 +169,11 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     if (tid == 0) {
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
-        for (int k = 0; k < D; ++k) mbar_init(&full[k], 1);
+        for (int k = 0; k < D; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], 1);
+        }
+        *halt = 0;
         fence_mbarrier_init_cluster();
     }
     __syncthreads();
@@ -164,6 +185,61 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
     const double alpha = a.alphas[w];
     const int64_t total = a.count * bs;  // draws of this worker in the launch
     const double2* bs2 = reinterpret_cast<const double2*>(a.bs2);
+    const unsigned row_bytes = (unsigned)(ldc * sizeof(double));
+
+    if (warp == nw) {
+        // ================= producer warp: the row ring =================
+        // Row j goes into stage j mod D once row j - D has been released by the compute
+        // threads; its slice by one bulk copy (TMA engine), its (b, sq) pair by a 16-byte
+        // cp.async on the same mbarrier.  Indices are read 32 at a time, one per lane.
+        // Rows go out up to four at a time on deep rings, one per lane: the per-row TMA and
+        // mbarrier issue costs overlap; the compute threads release stages in row order, so the
+        // release of a group's last predecessor covers the whole group.
+        constexpr int GI = 4;
+        int64_t j = 0;
+        for (int64_t j0 = 0; j0 < total && !*halt; j0 += 32) {
+            const int32_t my = (j0 + lane < total) ? idx[j0 + lane] : 0;
+            const int cnt = (int)(total - j0 < 32 ? total - j0 : 32);
+            bool stop = false;
+            // groups only on deep rings: a group waits for its last row's stage, which would hold
+            // back its first rows on a shallow ring (c3: two 80 KB stages)
+            const int gmax = D >= 4 * GI ? GI : 1;
+            for (int u0 = 0; u0 < cnt; u0 += gmax) {
+                const int g = cnt - u0 < gmax ? cnt - u0 : gmax;
+                const int64_t jl = j0 + u0 + g - 1;  // the group's last row
+                if (jl >= D) {
+                    const unsigned eph = (unsigned)(((jl / D) - 1) & 1);
+                    bool ok = false;
+                    while (!(ok = mbar_try_wait(&empty[jl % D], eph)))
+                        if (*halt) break;
+                    if (!ok) {
+                        stop = true;
+                        break;
+                    }
+                }
+                const int64_t i = __shfl_sync(0xffffffffu, my, (u0 + lane) & 31);
+                if (lane < g) {
+                    const int st = (int)((j0 + u0 + lane) % D);
+                    cp_async16(sm.bsq + st, bs2 + 2 * i);
+                    cp_async_mbar_arrive(&full[st]);
+                    mbar_arrive_expect_tx(&full[st], row_bytes);
+                    bulk_g2s(sm.ring + (size_t)st * ldc, a.A + i * ld + cb, row_bytes, &full[st]);
+                }
+                __syncwarp();
+                j = jl + 1;  // rows issued
+            }
+            if (stop || *halt) break;
+        }
+        // every issued copy must land before the CTA exits
+        if (lane == 0)
+            for (int k = 0; k < D && k < j; ++k) {
+                const int64_t last = k + ((j - 1 - k) / D) * D;  // the last row issued into stage k
+                mbar_wait(&full[k], (unsigned)((last / D) & 1));
+            }
+        __syncwarp();
+        if (C >= 2) cluster_sync_all();
+        return;
+    }
 
     double v[2 * EP];
 #pragma unroll
@@ -174,54 +250,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         v[2 * p] = xv.x;
         v[2 * p + 1] = xv.y;
     }
-    for (int64_t e = tid; e < IDX_WINDOW && e < total; e += T) sm.win[e] = idx[e];
-    __syncthreads();
-
-    // ---- issue side of the row ring: one bulk copy (TMA engine) per row slice
-    // and one per (b, sq) pair, both completing the stage's mbarrier --------------
-    int64_t issued = 0, win_next = IDX_WINDOW / 2;
-    int iss_stage = 0;
-    const unsigned row_bytes = (unsigned)(ldc * sizeof(double));
-    auto issue_upto = [&](int64_t lim) {
-        if (lim > total) lim = total;
-        while (issued < lim) {
-            // rows [issued, issued + cnt) without crossing a window refill point
-            int64_t stop = lim < win_next ? lim : win_next;
-            if (issued >= win_next) {
-                // refill the window half the issue pointer has left.  Only warp 0
-                // touches the window (its lanes are the only readers), so no other
-                // warp can overwrite entries that are still to be issued.
-                if (warp == 0) {
-                    for (int64_t e = win_next + IDX_WINDOW / 2 + lane; e < win_next + IDX_WINDOW && e < total; e += 32)
-                        sm.win[e & (IDX_WINDOW - 1)] = idx[e];
-                    __syncwarp();
-                }
-                win_next += IDX_WINDOW / 2;
-                stop = lim < win_next ? lim : win_next;
-            }
-            const int cnt = (int)(stop - issued);
-            // row issued + j goes out from warp j % nw, lane j / nw: the per-row mbarrier and
-            // TMA issue costs (~200 cycles) spread over the warps instead of queueing in warp 0.
-            // Every warp tracks the same `issued`; only warp 0 rewrites the window, and only
-            // slots of rows already issued (see above), so these reads are safe.
-            const int jrow = lane * nw + warp;
-            if (jrow < cnt) {
-                const int lane_j = jrow;
-                int st = iss_stage + lane_j;
-                if (st >= D) st -= D;
-                const int64_t i = sm.win[(issued + lane_j) & (IDX_WINDOW - 1)];
-                // the (b, sq) pair by a 16-byte cp.async tracked on the same mbarrier: one TMA op
-                // per row instead of two (a bulk op costs ~60-110 cycles of TMA issue)
-                cp_async16(sm.bsq + st, bs2 + 2 * i);
-                cp_async_mbar_arrive(&full[st]);
-                mbar_arrive_expect_tx(&full[st], row_bytes);
-                bulk_g2s(sm.ring + (size_t)st * ldc, a.A + i * ld + cb, row_bytes, &full[st]);
-            }
-            issued += cnt;
-            iss_stage += cnt;
-            if (iss_stage >= D) iss_stage -= D;
-        }
-    };
+    named_sync(1, T);
 
     // direct ||v - x_ref||^2 over the CTA
     // join the C slices of a reduction: every CTA sends its totals to every peer (slot
@@ -440,17 +469,23 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
         }
         if (rec) a.dbg[nblk * 8 + 6] = clock64();
         ++nblk;
+        // the applied rows' stages go back to the producer (every thread read them before the
+        // reduction's barriers: rows live in registers, (b, sq) in lanes)
+        if (tid == 0)
+            for (int r = 0; r < Reff; ++r) {
+                int st = c_stage + r;
+                if (st >= D) st -= D;
+                mbar_arrive(&empty[st]);
+            }
         d += Reff;
         c_stage += Reff;
         if (c_stage >= D) {
             c_stage -= D;
             c_par ^= 1u;
         }
-        issue_upto(d + D);  // stages of the applied rows are free (every thread holds them in registers)
         return Reff;
     };
 
-    issue_upto(D);
     if (q == 1) {
         // one chain: outer iteration k = rows [k*bs, (k+1)*bs); x = v after each
         while (d < total) {
@@ -493,7 +528,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 const int64_t lc = 2 * ((int64_t)p * T + tid);
                 if (lc < ldc) __stcg(reinterpret_cast<double2*>(vw + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
             }
-            grid_barrier(a.barrier, (++epoch) * gridDim.x);
+            grid_barrier_c(a.barrier, (++epoch) * gridDim.x, T);
             const int64_t G = gridDim.x;
             const int64_t cw = ((ld + G - 1) / G + 1) & ~(int64_t)1;
             const int64_t c0 = blockIdx.x * cw, c1 = (c0 + cw < ld) ? c0 + cw : ld;
@@ -508,7 +543,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
                 __stcg(a.x + col, xn);
                 if (ck && col < a.n) a.ckpt[slot * a.n + col] = xn;
             }
-            grid_barrier(a.barrier, (++epoch) * gridDim.x);
+            grid_barrier_c(a.barrier, (++epoch) * gridDim.x, T);
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
                 const int64_t lc = 2 * ((int64_t)p * T + tid);
@@ -521,14 +556,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value, 1) chain_kernel(So
             done = kk + 1;
         }
     }
-    // drain bulk copies still in flight (rows issued ahead of a stop) before exit
-    for (int64_t row = d; row < issued; ++row) {
-        mbar_wait(&full[c_stage], c_par);
-        if (++c_stage == D) {
-            c_stage = 0;
-            c_par ^= 1u;
-        }
-    }
+    if (tid == 0) *halt = 1;  // the producer stops issuing and drains what it issued
     if (q == 1) {
         double* dst = a.partial ? a.partial : a.x;
 #pragma unroll
