@@ -664,7 +664,8 @@ def _run_cgls(system, cfg, x_ref):
 DEFAULT_LANES = 10  # measured best for c1 (7 co-resident 16-CTA clusters; chunk boundaries interleave the rest)
 
 
-def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None) -> list[RunReport]:
+def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None, x_ref=None,
+                     trace_step=None) -> list[RunReport]:
     """Independent solves of one resident system side by side (e.g. the per-seed solves of
     harness.measure_iterations, harness.py:127-149): each of `lanes` host threads drives its
     own system view (kz_system_view: shared matrix, own iterate / samplers / stream), so the
@@ -684,6 +685,8 @@ def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None) -> 
     try:
         # views persist on the system (allocations and streams are made once, not per call:
         # a cudaFree inside a batch would synchronise the device under the other lanes)
+        if x_ref is not None:  # one reference for all the solves, set on the system the views alias
+            ds.set_x_ref(x_ref)
         cache = ds.__dict__.setdefault("_lane_views", [])
         while len(cache) < n_lanes:
             cache.append(ds.view())
@@ -693,7 +696,7 @@ def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None) -> 
         def lane(i):
             for j in range(i, len(cfgs), n_lanes):
                 c = cfgs[j].replace(short_launches=True) if n_lanes > 1 else cfgs[j]
-                out[j] = run_solver(views[i], c, budget=budget)
+                out[j] = run_solver(views[i], c, budget=budget, trace_step=trace_step)
 
         with ThreadPoolExecutor(n_lanes) as pool:
             for f in [pool.submit(lane, i) for i in range(n_lanes)]:
