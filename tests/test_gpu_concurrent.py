@@ -84,3 +84,21 @@ def test_views_follow_reupload(gpu, systems):
         alone = [run_solver(ds, c) for c in cfgs]
     for t, s_ in zip(together, alone):
         assert t.iterations == s_.iterations and np.array_equal(t.x, s_.x)
+
+
+def test_concurrent_traces_with_shared_reference(gpu, inc2000):
+    """Trace mode side by side with one x_ref for all solves (the c4 horizon protocol): the
+    trace records equal those of the solves run alone."""
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver, solve_concurrent
+
+    s = inc2000
+    x_ls = s.x_ls if s.x_ls is not None else None
+    cfgs = [SolverConfig(variant="rka", q=8, base_seed=k, max_iterations=3000) for k in range(4)]
+    with DeviceSystem(s) as ds:
+        xr = x_ls if x_ls is not None else ds.cgls(tol=1e-12)
+        alone = [run_solver(ds, c, x_ref=xr, trace_step=500) for c in cfgs]
+        together = solve_concurrent(ds, cfgs, lanes=4, x_ref=xr, trace_step=500)
+    for a, t in zip(alone, together):
+        assert [(r.iteration, r.error_norm, r.residual_norm) for r in a.trace] == \
+               [(r.iteration, r.error_norm, r.residual_norm) for r in t.trace]
+        assert np.array_equal(a.x, t.x)
