@@ -194,6 +194,13 @@ typedef struct {
 
 /* Full solve with host output x_host (n values, may be NULL). */
 KZ_API int32_t kz_solve(kz_system* sys, const kz_params* params, kz_result* result, double* x_host, void* stream);
+/* The seeds of one RK configuration (seeds[S]) solved side by side in one launch per chunk:
+ * one warp per seed on short rows (n <= 256), each with its own iterate, row draws
+ * (Prng(seed, worker_offset)), status and stop flag.  results[S]; x_host: S x n (may be NULL).
+ * Stop or budget mode (no trace / checkpoints).  The BASELINE config-0 protocol's 10 seeds
+ * (harness.py:127-149) in one go instead of ten latency-bound solves. */
+KZ_API int32_t kz_solve_seeds(kz_system* sys, const kz_params* params, const uint64_t* seeds, int64_t S,
+                              kz_result* results, double* x_host, void* stream);
 /* Resident iterate: copy out (n values) / overwrite (NULL = zeros). */
 KZ_API int32_t kz_solution_host(kz_system* sys, double* x_host, void* stream);
 KZ_API int32_t kz_set_x(kz_system* sys, const double* x_host, void* stream);

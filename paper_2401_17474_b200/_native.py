@@ -36,6 +36,7 @@ EXPORTS = (
     "kz_cgls", "kz_spectral", "kz_system_load_file", "kz_generate_counter_rows",
     "kz_comm_unique_id", "kz_comm_create", "kz_comm_destroy", "kz_solve_sharded", "kz_system_view",
     "kz_system_view_refresh", "kz_comm_exchange_handle", "kz_comm_exchange_connect", "kz_row_norms_upload",
+    "kz_solve_seeds",
 )
 COMM_HANDLE_BYTES = 64
 COMM_ID_BYTES = 128
@@ -141,6 +142,8 @@ def load_library():
         L.kz_norms.argtypes = [vp, _dp, _dp, _dp, vp]
         L.kz_system_view.argtypes = [vp, C.POINTER(vp)]
         L.kz_row_norms_upload.argtypes = [vp, _dp, vp]
+        L.kz_solve_seeds.argtypes = [vp, C.POINTER(Params), C.POINTER(C.c_uint64), C.c_int64,
+                                     C.POINTER(Result), _dp, vp]
         L.kz_system_view_refresh.argtypes = [vp]
         L.kz_comm_unique_id.argtypes = [C.c_char_p]
         L.kz_comm_create.argtypes = [C.c_int32, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(vp)]

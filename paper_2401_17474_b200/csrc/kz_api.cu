@@ -184,6 +184,7 @@ struct kz_system {
     DevBuf<unsigned long long> ll;  // rka kernel: tagged words of the cross-cluster exchange
     size_t ll_words = 0;            // words the current plan uses
     DevBuf<double> S;               // kz_solve_sharded: the rank's worker sum (all-reduced in place)
+    DevBuf<double> xs;              // kz_solve_seeds: one iterate per seed
     DevBuf<double> errs;            // kz_solve_sharded: ||x_k - x_ref||^2 per iteration of a chunk
     DevBuf<int> halt;               // kz_solve_sharded: device stop flag (k + 1 of the stop, 0 = running)
     // per-call host work reused across kz_solve calls (row-sharded loops call it every iteration):
@@ -280,7 +281,7 @@ extern "C" int32_t kz_system_destroy(kz_system* s) {
     if (!s) return KZ_OK;
     cudaSetDevice(s->device);
     for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas, &s->bs2,
-                    &s->cg, &s->stage, &s->S, &s->errs})
+                    &s->cg, &s->stage, &s->S, &s->errs, &s->xs})
         b->release();
     s->ll.release();
     s->halt.release();
@@ -2470,5 +2471,139 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
     KZ_CUDA(cudaStreamSynchronize(st));
     r->kernel_launches = g_launches.load() - launches0;
+    return KZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Many seeds of one RK configuration in one launch per chunk (the 10 seeds of BASELINE config 0:
+// harness.measure_iterations, harness.py:127-149).  Each seed is one block of the one-warp RK
+// kernel with its own iterate, row draws (stream Prng(seed, 0)), status and stop flag; a seed
+// that meets the stop rule drops out of later launches.  Short rows only (the warp kernel).
+// ---------------------------------------------------------------------------
+extern "C" int32_t kz_solve_seeds(kz_system* s, const kz_params* p, const uint64_t* seeds, int64_t S,
+                                  kz_result* results, double* x_host, void* stream) {
+    if (!s || !p || !seeds || !results) return fail(KZ_EINVAL, "null argument");
+    if (S < 1) return fail(KZ_EINVAL, "need at least one seed");
+    if (p->variant != KZ_RK) return fail(KZ_EINVAL, "kz_solve_seeds runs RK (variant %d)", p->variant);
+    if (s->ld > 256) return fail(KZ_EINVAL, "kz_solve_seeds covers rows of at most 256 columns");
+    if (p->trace_step > 0 || p->ckpt_every > 0 || p->partial_dev)
+        return fail(KZ_EINVAL, "kz_solve_seeds has no trace, checkpoint or partial mode");
+    if (!(p->epsilon > 0)) return fail(KZ_EINVAL, "epsilon must be > 0, got %g", p->epsilon);
+    if (p->max_iterations < 1) return fail(KZ_EINVAL, "max_iterations must be >= 1, got %lld", (long long)p->max_iterations);
+    const bool budget_mode = p->budget > 0, stop_mode = !budget_mode;
+    if (stop_mode && !s->has_xref) return fail(KZ_EINVAL, "system carries no reference solution");
+    cudaStream_t st = pick_stream(s, stream);
+    KZ_CUDA(cudaSetDevice(s->device));
+    for (int64_t i = 0; i < S; ++i) {
+        memset(&results[i], 0, sizeof(kz_result));
+        results[i].final_error_sq = NAN;
+        results[i].final_residual = NAN;
+    }
+    // one full-access range per seed: the RK sampler (q = 1) for every stream
+    KZ_TRY(ensure_sampler(s, KZ_FULL_ACCESS, S, st));
+    KZ_TRY(ensure_bs2(s, st));
+    {
+        std::vector<PcgPod> pods(S);
+        for (int64_t i = 0; i < S; ++i) pods[i] = seed_stream(seeds[i], (uint64_t)p->worker_offset);
+        KZ_TRY(s->states.ensure(S));
+        KZ_CUDA(cudaMemcpyAsync(s->states.p, pods.data(), S * sizeof(PcgPod), cudaMemcpyHostToDevice, st));
+        s->pods_q = -1;  // kz_solve's cached streams are overwritten
+    }
+    const double alpha = p->alphas_host ? p->alphas_host[0] : 1.0;
+    KZ_TRY(s->alphas.ensure(1));
+    KZ_CUDA(cudaMemcpyAsync(s->alphas.p, &alpha, sizeof(double), cudaMemcpyHostToDevice, st));
+    s->alphas_cache.clear();
+    const int64_t chunk_max = 4096;
+    KZ_TRY(s->xs.ensure((size_t)S * s->ld));
+    KZ_CUDA(cudaMemsetAsync(s->xs.p, 0, (size_t)S * s->ld * sizeof(double), st));
+    KZ_TRY(s->idx.ensure((size_t)S * chunk_max));
+    KZ_TRY(s->status.ensure(S));
+    KZ_TRY(s->halt.ensure(S));
+    KZ_CUDA(cudaMemsetAsync(s->halt.p, 0, S * sizeof(int), st));
+    std::vector<SolveStatus> hs(S);
+    std::vector<int> hh(S, 0);
+    std::vector<int64_t> iters(S, 0), evals(S, 0);
+    std::vector<double> errv(S, NAN);
+    std::vector<int> conv(S, 0);
+
+    const int epl = s->ld <= 64 ? 1 : (s->ld <= 128 ? 2 : 4);
+    void* fn = rkw_fn(epl);
+    SolveArgs args = {};
+    args.A = s->A.p;
+    args.b = s->b.p;
+    args.sq = s->sq.p;
+    args.bs2 = s->bs2.p;
+    args.xref = s->xref.p;
+    args.x = s->xs.p;
+    args.idx = s->idx.p;
+    args.alphas = s->alphas.p;
+    args.status = s->status.p;
+    args.halt = s->halt.p;
+    args.n = s->n;
+    args.ld = s->ld;
+    args.q = 1;
+    args.bs = 1;
+    args.eps = p->epsilon;
+    args.use_stop = stop_mode ? 1 : 0;
+    const long long launches0 = g_launches.load();
+    const int64_t limit = budget_mode ? p->budget : p->max_iterations;
+    KZ_CUDA(cudaEventRecord(s->ev[0], st));
+    int64_t k = 0, active = S;
+    for (;;) {
+        const int64_t remaining = limit - k;
+        if (remaining <= 0 && !stop_mode) break;
+        const int64_t c = std::min<int64_t>(chunk_max, remaining);
+        if (c > 0) KZ_TRY(launch_sampler(s, s->states.p, s->lo.p, s->len.p, S, k, c, s->idx.p, c, 1, st));
+        args.k0 = k;
+        args.count = c;
+        args.idx_stride = c;
+        args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
+        void* kargs[] = {&args};
+        KZ_CUDA(cudaLaunchKernel(fn, dim3((unsigned)S), dim3(32), kargs, 0, st));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        KZ_CUDA(cudaMemcpyAsync(hs.data(), s->status.p, S * sizeof(SolveStatus), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        bool newly = false;
+        for (int64_t i = 0; i < S; ++i) {
+            if (hh[i]) continue;
+            iters[i] = k + hs[i].iters_done;
+            evals[i] += hs[i].checks;
+            if (hs[i].checks > 0) errv[i] = hs[i].err;
+            if (hs[i].converged) {
+                conv[i] = 1;
+                hh[i] = 1;
+                --active;
+                newly = true;
+            } else if (hs[i].iters_done != c) {
+                return fail(KZ_ECUDA, "seed %lld stopped early (%lld of %lld iterations)", (long long)i,
+                            (long long)hs[i].iters_done, (long long)c);
+            }
+        }
+        k += c;
+        if (active == 0 || (stop_mode && k >= p->max_iterations)) break;
+        if (newly) KZ_CUDA(cudaMemcpyAsync(s->halt.p, hh.data(), S * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    KZ_CUDA(cudaEventRecord(s->ev[1], st));
+    KZ_CUDA(cudaEventSynchronize(s->ev[1]));
+    float loop_ms = 0.f;
+    cudaEventElapsedTime(&loop_ms, s->ev[0], s->ev[1]);
+    for (int64_t i = 0; i < S; ++i) {
+        kz_result& r = results[i];
+        r.iterations = iters[i];
+        r.converged = conv[i];
+        r.error_evals = stop_mode ? evals[i] : 0;
+        r.final_error_sq = stop_mode ? errv[i] : NAN;
+        r.rows_projected = iters[i];
+        r.loop_ms = loop_ms;
+        r.kernel_ms = loop_ms;
+        r.kernel_used = KZ_KERNEL_WARP;
+        r.ctas = (int32_t)S;
+        r.threads = 32;
+        r.kernel_launches = g_launches.load() - launches0;
+    }
+    if (x_host)
+        KZ_CUDA(cudaMemcpy2DAsync(x_host, s->n * sizeof(double), s->xs.p, s->ld * sizeof(double), s->n * sizeof(double),
+                                  S, cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
     return KZ_OK;
 }

@@ -26,9 +26,15 @@ namespace kz {
 template <int EPL, int P>
 __global__ void __launch_bounds__(32, 1) rkw_kernel(SolveArgs a) {
     static_assert(P <= 32, "one record per lane");
-    if (a.halt != nullptr && *a.halt != 0) return;
+    // block b = one independent solve (kz_solve_seeds: the seeds of a configuration side by
+    // side, each with its own iterate, row draws, status and stop flag); one block otherwise
+    const int64_t sb = blockIdx.x;
+    if (a.halt != nullptr && a.halt[sb] != 0) return;
     const int lane = threadIdx.x;
     const int64_t ld = a.ld, n = a.n, total = a.count;
+    double* const xg = a.x + sb * ld;
+    const int32_t* const ix = a.idx + sb * a.idx_stride;
+    SolveStatus* const stat = a.status + sb;
     const double alpha = a.alphas[0];
     const bool use_stop = a.use_stop != 0, final_check = a.final_check != 0;
     const bool ckpt_on = a.ckpt_every > 0;
@@ -39,13 +45,13 @@ __global__ void __launch_bounds__(32, 1) rkw_kernel(SolveArgs a) {
     for (int e = 0; e < EPL; ++e) {
         const int64_t col = 2 * (int64_t)(lane + 32 * e);
         vld[e] = col < ld;
-        x[e] = vld[e] ? __ldcg(reinterpret_cast<const double2*>(a.x + col)) : make_double2(0.0, 0.0);
+        x[e] = vld[e] ? __ldcg(reinterpret_cast<const double2*>(xg + col)) : make_double2(0.0, 0.0);
         xr[e] = vld[e] ? __ldg(reinterpret_cast<const double2*>(a.xref + col)) : make_double2(0.0, 0.0);
     }
     auto row_ptr = [&](int i, int e) {
         return reinterpret_cast<const double2*>(a.A + (int64_t)i * ld + 2 * (lane + 32 * e));
     };
-    auto idx_at = [&](int64_t j) -> int { return (lane < P && j < total) ? a.idx[j] : 0; };
+    auto idx_at = [&](int64_t j) -> int { return (lane < P && j < total) ? ix[j] : 0; };
     auto load_rec = [&](int64_t j, int i, double& b, double& sq, double& rc) {
         if (lane < P && j < total) {
             const double2 r01 = __ldg(reinterpret_cast<const double2*>(a.bs2 + 4 * (int64_t)i));
@@ -148,12 +154,12 @@ __global__ void __launch_bounds__(32, 1) rkw_kernel(SolveArgs a) {
     }
 #pragma unroll
     for (int e = 0; e < EPL; ++e)
-        if (vld[e]) __stcg(reinterpret_cast<double2*>(a.x + 2 * (lane + 32 * e)), x[e]);
+        if (vld[e]) __stcg(reinterpret_cast<double2*>(xg + 2 * (lane + 32 * e)), x[e]);
     if (lane == 0) {
-        a.status->iters_done = done;
-        a.status->converged = conv;
-        a.status->checks = checks;
-        a.status->err = err_last;
+        stat->iters_done = done;
+        stat->converged = conv;
+        stat->checks = checks;
+        stat->err = err_last;
     }
 }
 

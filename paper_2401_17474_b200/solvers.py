@@ -661,6 +661,62 @@ def _run_cgls(system, cfg, x_ref):
                      final_error_sq=err * err if x_ref is not None else float("nan"), final_residual=res, x=x)
 
 
+def _seed_batchable(system, cfgs, budget, trace_step) -> bool:
+    """RK solves that differ only in the seed, on rows short enough for the warp kernel."""
+    c0 = cfgs[0]
+    n = system.n if isinstance(system, DeviceSystem) else getattr(system.A, "shape", (0, 0))[1]
+    return (trace_step is None and len(cfgs) > 1 and c0.variant == "rk" and c0.kernel in ("auto", "warp")
+            and n <= 128 and all(c.replace(base_seed=c0.base_seed) == c0 for c in cfgs))
+
+
+def solve_seeds(system, cfg: SolverConfig, seeds, *, budget=None) -> list[RunReport]:
+    """The seeds of one RK configuration side by side in one launch per chunk (kz_solve_seeds):
+    one warp per seed on short rows.  Reports in seed order, bit-identical to solving each
+    seed alone on the warp kernel."""
+    cfg.validate()
+    seeds = [int(x) for x in seeds]
+    own = not isinstance(system, DeviceSystem)
+    ds = _pool_acquire(system, cfg.device) if own else system
+    try:
+        alphas = N.f64(resolve_alphas(ds, cfg, 1))
+        if budget is None and not ds._xref_set:
+            host = ds.host if not own else system
+            if host is None:
+                raise ValueError("system carries no reference solution")
+            ds.set_x_ref(host.x_ref())
+        p = N.Params()
+        p.variant = N.VARIANT_IDS["rk"]
+        p.scheme = N.SCHEME_IDS["full_access"]
+        p.q = 1
+        p.block_size = 1
+        p.alphas_host = N.ptr(alphas)
+        p.epsilon = float(cfg.epsilon)
+        p.max_iterations = int(cfg.max_iterations)
+        p.budget = 0 if budget is None else int(budget)
+        S = len(seeds)
+        res = (N.Result * S)()
+        sv = (C.c_uint64 * S)(*seeds)
+        X = np.empty((S, ds.n))
+        N.check(ds._lib.kz_solve_seeds(ds.handle, C.byref(p), sv, S, res, N.ptr(X), None))
+        out = []
+        for i, sd in enumerate(seeds):
+            r = res[i]
+            resid = ds.norms(X[i])[0] if budget is None else float("nan")  # ||A x - b||, solvers.py:246
+            out.append(RunReport(variant="rk", q=1, block_size=1, alpha_policy=cfg.alpha_policy,
+                                 alpha=float(alphas[0]), seed=sd, iterations=int(r.iterations),
+                                 converged=bool(r.converged), wall_time_s=float(r.loop_ms) / 1e3,
+                                 final_error_sq=float(r.final_error_sq), final_residual=float(resid),
+                                 error_evals=int(r.error_evals), x=X[i].copy(),
+                                 gpu={"kernel": "warp", "ctas": int(r.ctas), "threads": int(r.threads),
+                                      "loop_ms": float(r.loop_ms), "kernel_ms": float(r.kernel_ms),
+                                      "rows_projected": int(r.rows_projected),
+                                      "launches": int(r.kernel_launches), "seed_batch": S}))
+        return out
+    finally:
+        if own:
+            _pool_release(ds)
+
+
 DEFAULT_LANES = 10  # measured best for c1 (7 co-resident 16-CTA clusters; chunk boundaries interleave the rest)
 
 
@@ -676,6 +732,8 @@ def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None, x_r
     cfgs = list(cfgs)
     if not cfgs:
         return []
+    if _seed_batchable(system, cfgs, budget, trace_step):  # short-row RK: all seeds in one launch
+        return solve_seeds(system, cfgs[0], [c.base_seed for c in cfgs], budget=budget)
     device = cfgs[0].device
     if isinstance(system, DeviceSystem):
         ds, own = system, False

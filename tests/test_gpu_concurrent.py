@@ -102,3 +102,32 @@ def test_concurrent_traces_with_shared_reference(gpu, inc2000):
         assert [(r.iteration, r.error_norm, r.residual_norm) for r in a.trace] == \
                [(r.iteration, r.error_norm, r.residual_norm) for r in t.trace]
         assert np.array_equal(a.x, t.x)
+
+
+@pytest.mark.parametrize("budget", [None, 2500])
+def test_seed_batch_equals_solves_alone(gpu, systems, budget):
+    """kz_solve_seeds (one warp per seed, one launch per chunk for all seeds) vs each seed solved
+    alone on the warp kernel: bit-identical iterates, same counts, errors and residuals; and
+    against the reference's own c0 runs (tests/golden/solves.npz)."""
+    from conftest import PARITY_TOL, golden, rel_err
+
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver, solve_concurrent, solve_seeds
+
+    s = systems["c0"]
+    cfg = SolverConfig(variant="rk")
+    with DeviceSystem(s) as ds:
+        batch = solve_seeds(ds, cfg, list(range(10)), budget=budget)
+        alone = [run_solver(ds, cfg.replace(base_seed=k), budget=budget) for k in range(10)]
+        via = solve_concurrent(ds, [cfg.replace(base_seed=k) for k in range(10)], budget=budget)
+    for b, a, v in zip(batch, alone, via):
+        assert b.gpu["seed_batch"] == 10 and v.gpu.get("seed_batch") == 10
+        assert b.iterations == a.iterations and b.converged == a.converged and b.error_evals == a.error_evals
+        assert np.array_equal(b.x, a.x) and np.array_equal(v.x, b.x)
+        if budget is None:
+            assert b.final_error_sq == a.final_error_sq
+            assert abs(b.final_residual - a.final_residual) <= 1e-12 * (1 + a.final_residual)
+    if budget is None:
+        g = golden("solves.npz")
+        for k, b in enumerate(batch):
+            assert b.iterations == int(g[f"c0_rk_s{k}_iterations"])
+            assert rel_err(b.x, g[f"c0_rk_s{k}_x"]) <= PARITY_TOL
