@@ -865,9 +865,10 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     // a worker is one CTA, or a CTA pair (thread-block cluster of 2, each CTA
     // half the columns) when the rows are long and the pairs fit the SMs
     int C = (s->ld >= 1024 && 2 * q <= s->sms && !s->no_pairs) ? 2 : 1;  // measured: pairs win from n ~ 1000
-    // one chain (RK, CK) over long rows: a cluster of 8 (measured on 80000 x 2000: 0.50 us per row
-    // against 0.54 for a pair and 0.58 for one CTA; at n = 512 the pair is best)
-    if (q == 1 && s->ld >= 1536 && s->ld % 16 == 0 && !s->no_pairs) C = 8;
+    // one chain (RK, CK) over long rows: a cluster of 4 (measured on 80000 x 2000 with the
+    // producer warp: 0.40 us per row against 0.42 for 8 CTAs and 0.45 for a pair; at n = 512
+    // the pair is best)
+    if (q == 1 && s->ld >= 1536 && s->ld % 8 == 0 && !s->no_pairs) C = 4;
     if (const char* e = getenv("KZ_CHAIN_PAIR")) {  // experiment: 1, 2, or (one chain, q = 1) 4 / 8
         const int want = atoi(e);
         C = want == 2 && 2 * q <= s->sms ? 2 : ((want == 4 || want == 8) && q == 1 ? want : 1);
