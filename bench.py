@@ -316,6 +316,7 @@ def extra_workloads(device, peak, steps=3):
             hs = [float(np.mean([t.error_norm for t in r.trace[-10:]])) for r in rs]
             h = float(np.mean(hs))
             rows = sum(r.gpu["rows_projected"] for r in rs)
+            gemv_bytes = sum(len(r.trace) + 1 for r in rs) * 8 * (inc.m * 2000 + inc.m)
             kms = sum(r.gpu["kernel_ms"] for r in rs)
             gbs = rows * 8 * 2000 / (kms / 1e3) / 1e9
             g = rs[0].gpu
@@ -327,7 +328,12 @@ def extra_workloads(device, peak, steps=3):
                         "horizon_norm": h, "horizon_sq": h * h, "horizon_norm_per_seed": hs,
                         "trace_records": len(rs[0].trace), "cgls_ms": cg_ms, "cgls_iterations": ds.cgls_iterations,
                         "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
-                                     "note": "per-solve kernel time"}})
+                                     "note": "per-solve kernel time"},
+                        # every trace record carries ||Ax - b|| (harness trace semantics): one pass
+                        # over A per record and one for the final residual, on top of the row bytes
+                        "step_traffic": {"row_bytes": rows * 8 * 2000, "residual_bytes": gemv_bytes,
+                                         "gbs": (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9,
+                                         "frac": (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9 / peak}})
         ds.close()
         s2 = generate_mother(GeneratorConfig(m_max=80000, n_max=1000, seed=0))
         ds = DeviceSystem(s2, device=device)

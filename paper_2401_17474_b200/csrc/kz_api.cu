@@ -684,6 +684,8 @@ extern "C" int32_t kz_dump_rows(kz_system* s, int32_t scheme, int64_t q, uint64_
 // norms for traces / reports
 // ---------------------------------------------------------------------------
 static int device_norms(kz_system* s, const double* xdev, double* residual, double* error, cudaStream_t st) {
+    // both sums land in part[0..1] and come back with one copy and one host sync (a trace
+    // record costs one round trip, not two)
     double h[2] = {NAN, NAN};
     if (residual) {
         const int rows_per_cta = 8;
@@ -692,19 +694,20 @@ static int device_norms(kz_system* s, const double* xdev, double* residual, doub
         KZ_TRY(check_launch("residual_rows_kernel"));
         sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->m, s->part.p);
         KZ_TRY(check_launch("sum_kernel"));
-        KZ_CUDA(cudaMemcpyAsync(&h[0], s->part.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-        KZ_CUDA(cudaStreamSynchronize(st));
-        *residual = std::sqrt(h[0]);
     }
     if (error) {
+        // tmp is reused: stream order puts this after the residual sum has consumed it
         diff_sq_kernel<<<(unsigned)((s->n + 255) / 256), 256, 0, st>>>(xdev, s->xref.p, s->n, s->tmp.p);
         KZ_TRY(check_launch("diff_sq_kernel"));
-        sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->n, s->part.p);
+        sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->n, s->part.p + 1);
         KZ_TRY(check_launch("sum_kernel"));
-        KZ_CUDA(cudaMemcpyAsync(&h[1], s->part.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-        KZ_CUDA(cudaStreamSynchronize(st));
-        *error = std::sqrt(h[1]);
     }
+    if (residual || error) {
+        KZ_CUDA(cudaMemcpyAsync(h, s->part.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+    }
+    if (residual) *residual = std::sqrt(h[0]);
+    if (error) *error = std::sqrt(h[1]);
     return KZ_OK;
 }
 
