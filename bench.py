@@ -316,7 +316,8 @@ def extra_workloads(device, peak, steps=3):
             hs = [float(np.mean([t.error_norm for t in r.trace[-10:]])) for r in rs]
             h = float(np.mean(hs))
             rows = sum(r.gpu["rows_projected"] for r in rs)
-            gemv_bytes = sum(len(r.trace) + 1 for r in rs) * 8 * (inc.m * 2000 + inc.m)
+            # passes over A for ||Ax - b||: the trace records go 32 to a pass, + the final residual
+            gemv_bytes = sum(-(-len(r.trace) // 32) + 1 for r in rs) * 8 * (inc.m * 2000 + inc.m)
             kms = sum(r.gpu["kernel_ms"] for r in rs)
             gbs = rows * 8 * 2000 / (kms / 1e3) / 1e9
             g = rs[0].gpu
@@ -330,7 +331,7 @@ def extra_workloads(device, peak, steps=3):
                         "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
                                      "note": "per-solve kernel time"},
                         # every trace record carries ||Ax - b|| (harness trace semantics): one pass
-                        # over A per record and one for the final residual, on top of the row bytes
+                        # over A per 32 records and one for the final residual, on top of the row bytes
                         "step_traffic": {"row_bytes": rows * 8 * 2000, "residual_bytes": gemv_bytes,
                                          "gbs": (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9,
                                          "frac": (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9 / peak}})

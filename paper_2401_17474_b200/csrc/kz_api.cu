@@ -187,6 +187,7 @@ struct kz_system {
     DevBuf<double> xs;              // kz_solve_seeds: one iterate per seed
     DevBuf<double> errs;            // kz_solve_sharded: ||x_k - x_ref||^2 per iteration of a chunk
     DevBuf<int> halt;               // kz_solve_sharded: device stop flag (k + 1 of the stop, 0 = running)
+    DevBuf<double> tsnap, tr2, tsum;  // trace mode: pending iterate snapshots, their squared residuals, sums
     // per-call host work reused across kz_solve calls (row-sharded loops call it every iteration):
     // worker streams, weights and the kernel plan
     uint64_t pods_seed = 0;
@@ -281,7 +282,7 @@ extern "C" int32_t kz_system_destroy(kz_system* s) {
     if (!s) return KZ_OK;
     cudaSetDevice(s->device);
     for (auto* b : {&s->A, &s->b, &s->xref, &s->x, &s->sq, &s->cdf, &s->tmp, &s->V, &s->part, &s->ckpt, &s->alphas, &s->bs2,
-                    &s->cg, &s->stage, &s->S, &s->errs, &s->xs})
+                    &s->cg, &s->stage, &s->S, &s->errs, &s->xs, &s->tsnap, &s->tr2, &s->tsum})
         b->release();
     s->ll.release();
     s->halt.release();
@@ -1585,13 +1586,49 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     const long long launches0 = g_launches.load();
     float kernel_ms = 0.f;
 
+    // trace records are taken as device snapshots of x and evaluated in batches of up to 32:
+    // one pass over A gives all their residuals (residual_batch_kernel), one host round trip
+    // returns residuals and errors; the loop itself never waits for a record
+    constexpr int TRACE_BATCH = 32;
+    int64_t pending = 0;
+    if (trace_mode) {
+        KZ_TRY(s->tsnap.ensure((size_t)TRACE_BATCH * s->ld));
+        KZ_TRY(s->tr2.ensure((size_t)TRACE_BATCH * s->m));
+        KZ_TRY(s->tsum.ensure(2 * TRACE_BATCH));
+        KZ_TRY(s->tmp.ensure((size_t)std::max(s->m, s->n)));
+    }
+    auto flush_trace = [&]() -> int {
+        if (pending == 0) return KZ_OK;
+        const int K = (int)pending;
+        residual_batch_kernel<<<(unsigned)((s->m + 31) / 32), 256, 0, st>>>(s->A.p, s->b.p, s->tsnap.p, s->m, s->n,
+                                                                              s->ld, K, s->tr2.p);
+        KZ_TRY(check_launch("residual_batch_kernel"));
+        for (int j = 0; j < K; ++j) {
+            sum_kernel<<<1, 1024, 0, st>>>(s->tr2.p + (int64_t)j * s->m, s->m, s->tsum.p + 2 * j);
+            KZ_TRY(check_launch("sum_kernel"));
+            diff_sq_kernel<<<(unsigned)((s->n + 255) / 256), 256, 0, st>>>(s->tsnap.p + (int64_t)j * s->ld,
+                                                                            s->xref.p, s->n, s->tmp.p);
+            KZ_TRY(check_launch("diff_sq_kernel"));
+            sum_kernel<<<1, 1024, 0, st>>>(s->tmp.p, s->n, s->tsum.p + 2 * j + 1);
+            KZ_TRY(check_launch("sum_kernel"));
+        }
+        double h[2 * TRACE_BATCH];
+        KZ_CUDA(cudaMemcpyAsync(h, s->tsum.p, 2 * (size_t)K * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        for (int j = 0; j < K; ++j) {
+            const int64_t t = n_trace - K + j;
+            p->trace_host[3 * t + 1] = std::sqrt(h[2 * j + 1]);
+            p->trace_host[3 * t + 2] = std::sqrt(h[2 * j]);
+        }
+        pending = 0;
+        return KZ_OK;
+    };
     auto record_trace = [&]() -> int {
-        double res = 0, e = 0;
-        KZ_TRY(device_norms(s, s->x.p, &res, &e, st));
+        KZ_CUDA(cudaMemcpyAsync(s->tsnap.p + pending * s->ld, s->x.p, s->ld * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
         p->trace_host[3 * n_trace + 0] = (double)k;
-        p->trace_host[3 * n_trace + 1] = e;
-        p->trace_host[3 * n_trace + 2] = res;
         ++n_trace;
+        if (++pending == TRACE_BATCH) KZ_TRY(flush_trace());
         return KZ_OK;
     };
 
@@ -1658,6 +1695,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         if (stop_mode && k >= p->max_iterations) break;
         if (stop_mode) chunk = std::min<int64_t>(chunk_max, chunk * 2);
     }
+    KZ_TRY(flush_trace());
     KZ_CUDA(cudaEventRecord(s->ev[1], st));
     KZ_CUDA(cudaEventSynchronize(s->ev[1]));
     float loop_ms = 0.f;

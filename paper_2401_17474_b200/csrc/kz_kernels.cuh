@@ -118,6 +118,9 @@ __global__ void sample_rows_kernel(const double* __restrict__ cdf, const int64_t
 __global__ void residual_rows_kernel(const double* __restrict__ A, const double* __restrict__ b,
                                      const double* __restrict__ x, int64_t m, int64_t n, int64_t ld,
                                      double* __restrict__ out);
+__global__ void residual_batch_kernel(const double* __restrict__ A, const double* __restrict__ b,
+                                      const double* __restrict__ X, int64_t m, int64_t n, int64_t ld, int K,
+                                      double* __restrict__ out);
 __global__ void diff_sq_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                                double* __restrict__ out);
 __global__ void pack_bs2_kernel(const double* __restrict__ b, const double* __restrict__ sq, int64_t m,

@@ -228,6 +228,59 @@ __global__ void residual_rows_kernel(const double* __restrict__ A, const double*
     }
 }
 
+// Trace residuals of K iterate snapshots (the trace records of one solve) in one pass over A:
+// out[j * m + i] = (<a_i, X_j> - b_i)^2, X_j = X + j * ld.  harness trace semantics
+// (solvers.py:210-224: every record carries ||Ax - b||) cost one GEMV over A per record; a
+// 32-row x 32-snapshot tile per CTA reads A once for up to 32 records (fp64 FMAs on the CUDA
+// cores, A and X staged 32 columns at a time through shared memory).  The dot of row i with
+// snapshot j runs over the columns in ascending order, so a record's value does not depend on
+// which other records share its batch.
+__global__ void __launch_bounds__(256) residual_batch_kernel(const double* __restrict__ A,
+                                                             const double* __restrict__ b,
+                                                             const double* __restrict__ X, int64_t m, int64_t n,
+                                                             int64_t ld, int K, double* __restrict__ out) {
+    constexpr int TM = 32, KB = 32, TK = 32;
+    __shared__ double As[TK][TM + 1];
+    __shared__ __align__(16) double Xs[TK][KB];
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    const int64_t row0 = (int64_t)blockIdx.x * TM;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t c0 = 0; c0 < n; c0 += TK) {
+#pragma unroll
+        for (int t = 0; t < (TM * TK) / 256; ++t) {
+            const int e = tid + 256 * t, r = e / TK, c = e % TK;
+            const int64_t gr = row0 + r, gc = c0 + c;
+            As[c][r] = (gr < m && gc < n) ? __ldg(A + gr * ld + gc) : 0.0;
+            Xs[c][r] = (r < K && gc < n) ? __ldg(X + (int64_t)r * ld + gc) : 0.0;  // r = snapshot here
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < TK; ++kk) {
+            const double a0 = As[kk][2 * ty], a1 = As[kk][2 * ty + 1];
+            const double2 xv = *reinterpret_cast<const double2*>(&Xs[kk][2 * tx]);
+            acc[0][0] = fma(a0, xv.x, acc[0][0]);
+            acc[0][1] = fma(a0, xv.y, acc[0][1]);
+            acc[1][0] = fma(a1, xv.x, acc[1][0]);
+            acc[1][1] = fma(a1, xv.y, acc[1][1]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int64_t gr = row0 + 2 * ty + i;
+        if (gr >= m) continue;
+        const double bi = b[gr];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int sj = 2 * tx + j;
+            if (sj < K) {
+                const double r = acc[i][j] - bi;
+                out[(int64_t)sj * m + gr] = r * r;
+            }
+        }
+    }
+}
+
 __global__ void diff_sq_kernel(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                                double* __restrict__ out) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
