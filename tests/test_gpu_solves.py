@@ -470,3 +470,23 @@ def test_warp_kernel_matches_oracle(gpu, oracle, n):
     for j, ck in enumerate(o["checkpoints"][:200]):
         assert rel_err(cap[50 * (j + 1) - 1], ck) <= PARITY_TOL, j
     assert rb.iterations == 777 and rel_err(rb.x, ob["x"]) <= PARITY_TOL
+
+
+def test_trace_records_past_one_residual_batch(gpu, inc2000):
+    """Trace records are evaluated 32 to a pass over A (kz_api.cu flush_trace); 71 records cross
+    two batch boundaries.  Each record must equal ||A x_k - b|| and ||x_k - x_ref|| of the
+    iterate checkpointed at the same k (harness.py:188, solvers.py:210-224)."""
+    from paper_2401_17474_b200 import DeviceSystem, run_solver
+
+    a, b, xr = inc2000.A, inc2000.b, inc2000.x_ls
+    with DeviceSystem(inc2000) as ds:
+        cap = []
+        r = run_solver(ds, _cfg(variant="rka", q=4, base_seed=1, max_iterations=7000), x_ref=xr, trace_step=100,
+                       capture=cap, checkpoint_every=100)
+    assert len(r.trace) == 71 and len(cap) == 70
+    for j, rec in enumerate(r.trace):
+        x = np.zeros(a.shape[1]) if j == 0 else cap[j - 1]
+        assert rec.iteration == 100 * j
+        res, err = float(np.linalg.norm(a @ x - b)), float(np.linalg.norm(x - xr))
+        assert abs(rec.residual_norm - res) <= 1e-9 * (1 + res), j
+        assert abs(rec.error_norm - err) <= 1e-9 * (1 + err), j
