@@ -1,27 +1,43 @@
 """Benchmark: row projections/s and time-to-||x - x*||^2 < 1e-8 (fp64) of the
-B200 RK / RKA / RKAB engine on BASELINE.json's configurations.
+B200 RK / RKA / RKAB engine on BASELINE.json config 3.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-A *step* is one full solve to epsilon of one solver seed (seeds cycle 0..9,
-the reference protocol's per-seed measurement, harness.py:127-149) on the
-workload's system, which is resident in HBM before timing starts.  `value`
-is rows projected / device time of the K timed steps; L2 is flushed between
-steps (the flush is outside the timed windows).  `e2e` runs the same solves
-through the public API with host (pinned) arrays: H2D of A, b, x*, the
-solve, and the D2H of x are inside its timed region.
+Workload (BASELINE.json configs[3], the largest single-GPU configuration):
+the 160000 x 20000 (25.6 GB) counter-keyed system, rows sharded over the N
+GPUs (partition_bounds(m, N, g), sampling.py:119-131), 64 RKAB workers per
+GPU (Q = 64 N), block size 1000, the reference's `distributed` sampling
+scheme (worker t samples partition_bounds(m, Q, t) with stream Prng(seed, t);
+its oracle is solve_rkab_seq(q=Q, sampling_scheme="distributed"),
+solvers.py:337-371), alpha = 1, x0 = 0.
 
-`--impl reference` times the reference algorithm's CPU implementation --
-the oracle port in oracle/ (the reference itself is pure Python + numpy and
-cannot be compiled) -- on all host cores, same workload, metric and units.
+A *step* is one solve to ||x - x*||^2 < 1e-8 for one solver seed (seeds
+cycle 0..9, harness.py:127-149), the shard resident in HBM before timing
+starts.  At N = 1 a solve is one kz_solve (whole chunks of outer iterations
+per chain-kernel launch); at N > 1 every rank runs kz_solve_sharded (per
+outer iteration the local step, an in-place NCCL all-reduce of the worker
+sum over NVLink, x = S / Q), and the ranks' final x must agree bitwise.
+`value` = rows projected by all ranks / max-over-ranks device time of the K
+steps.  The inputs (25.6 GB / N per GPU) are larger than L2, so no flush.
+`e2e` runs the same solves through the public API from pinned host arrays
+(the H2D of the shard and the D2H of x inside the timed region).
+
+`--impl reference` times the reference algorithm's CPU implementation -- the
+oracle port in oracle/ (the reference itself is pure Python + numpy; it
+cannot be compiled into oracle/_ref and does not travel to the GPU box) --
+on the box's host cores: same matrix (generated on the GPU, copied back),
+same configuration, fixed budgets of outer iterations per step, rows/s over
+the iteration loop's wall time (the reference times the loop only,
+solvers.py:203-208).
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
-import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -35,12 +51,11 @@ sys.path.insert(0, ROOT)
 METRIC = "row projections/s (fp64, solve to ||x-x*||^2<1e-8)"
 UNIT = "rows/s"
 
-WORKLOADS = {
-    # name: (m, n, solver kwargs, description)
-    "c0": (2000, 50, dict(variant="rk", q=1), "BASELINE c0: sequential RK, 2000x50"),
-    "c1": (20000, 500, dict(variant="rka", q=64), "BASELINE c1: RKA q=64, 20000x500"),
-    "c2": (80000, 1000, dict(variant="rkab", q=64, block_size=500), "BASELINE c2: RKAB q=64 bs=500, 80000x1000"),
-}
+# BASELINE.json configs[3]
+C3_M, C3_N, C3_Q, C3_BS, C3_SEED = 160000, 20000, 64, 1000, 0
+SEEDS = 10  # solver seeds of every BASELINE configuration
+REF_BUDGET = 4  # outer iterations per reference-arm step (256000 projections at N = 1, ~0.5 s on 16 cores)
+CPU_BASELINE_BUDGET = 24  # outer iterations of the cpu_baseline sample at N = 1 (~3-5 s of loop)
 
 
 def read_peak():
@@ -50,6 +65,18 @@ def read_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def c3_config(world: int) -> dict:
+    """The workload description shared by both arms (identical dicts at the same N)."""
+    return {"workload": "BASELINE c3: 160000x20000 counter-keyed (seed 0) fp64 system, RKAB 64 workers per GPU, "
+                        "block size 1000, distributed sampling scheme, solved to ||x-x*||^2<1e-8",
+            "m": C3_M, "n": C3_N, "variant": "rkab", "q_per_gpu": C3_Q, "q_total": C3_Q * world,
+            "block_size": C3_BS, "sampling_scheme": "distributed", "alpha": 1.0, "epsilon": 1e-8,
+            "solver_seeds": f"0..{SEEDS - 1} cycling, one solve per step",
+            "parallelism": f"rows sharded over {world} GPU(s) (partition_bounds), x averaged across GPUs "
+                           f"every outer iteration" if world > 1 else "1 GPU, whole system resident",
+            "l2": "inputs larger than L2 (25.6 GB / N per GPU vs 126 MB), no flush"}
 
 
 class ClockSampler:
@@ -105,146 +132,255 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def build_system(name):
-    from paper_2401_17474_b200 import GeneratorConfig, generate_mother
+def host_info() -> dict:
+    """The CPU side of the comparison: model, cores, the oracle's toolchain and numpy's BLAS."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name')} {b.get('version')}"
+    except Exception:
+        pass
+    cc = None
+    try:
+        cc = subprocess.run(["gcc", "--version"], capture_output=True, text=True).stdout.splitlines()[0]
+    except (OSError, IndexError):
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__, "blas": blas,
+            "oracle_cc": cc, "oracle_flags": "-O2 -ffp-contract=off (oracle/Makefile)"}
 
-    m, n, kw, _ = WORKLOADS[name]
-    return generate_mother(GeneratorConfig(m_max=m, n_max=n, seed=0)), kw
+
+def c3_host_system(device: int):
+    """The full c3 matrix on the host: generated on the GPU (the counter-keyed generator is
+    defined by its device code, kz_gen.cu), copied back once, outside any timing."""
+    from paper_2401_17474_b200 import DeviceSystem
+
+    with DeviceSystem(m=C3_M, n=C3_N, device=device) as ds:
+        ds.generate_counter(C3_SEED)
+        return ds.download()
 
 
-def run_reference(args, name, rank, world):
-    """CPU arm: the oracle port of the reference algorithm on all host cores."""
+def oracle_sample(A, b, xr, q_total: int, budget: int, seed: int, cores: int) -> dict:
+    import oracle as O
+
+    r = O.solve(A, b, xr, variant="rkab", q=q_total, block_size=C3_BS, scheme="distributed", base_seed=seed,
+                budget=budget, nthreads=cores)
+    return {"rows": budget * q_total * C3_BS, "loop_s": r["loop_seconds"]}
+
+
+def run_reference(args, rank, world, local_rank):
+    """CPU arm: the oracle port of the reference algorithm on all host cores, rank 0 only."""
     if rank != 0:
         return
     import oracle as O
 
-    system, kw = build_system(name)
     cores = O.max_threads()
-    m, n = system.A.shape
-
-    def one(seed):
-        t0 = time.perf_counter()
-        r = O.solve(system.A, system.b, system.x_star, base_seed=seed, nthreads=cores, **_oracle_kw(kw))
-        return time.perf_counter() - t0, r
-
+    A, b, xr = c3_host_system(local_rank)
+    Q = C3_Q * world
     for w in range(args.warmup):
-        one(w % 10)
-    tot_t, rows, iters = 0.0, 0, []
+        oracle_sample(A, b, xr, Q, REF_BUDGET, w % SEEDS, cores)
+    rows, loop_s = 0, 0.0
     for k in range(args.steps):
-        dt, r = one(k % 10)
-        tot_t += dt
-        rows += r["iterations"] * _rows_per_iter(kw)
-        iters.append(r["iterations"])
-    value = rows / tot_t
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator, seed 0)",
-        "config": {"workload": WORKLOADS[name][3] + f", {SEEDS} seeds per step", "m": m, "n": n, **kw,
-                   "seeds": "0..9 cycling"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full solves to eps, one seed of the {SEEDS}-seed batch per step "
-                                   f"(a bounded sample; oracle/kz_oracle.c, pthreads x{cores} over the workers)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "iterations": iters,
-    }
-    emit(line)
+        s = oracle_sample(A, b, xr, Q, REF_BUDGET, k % SEEDS, cores)
+        rows += s["rows"]
+        loop_s += s["loop_s"]
+    value = rows / loop_s
+    sample = (f"{args.steps} steps, each {REF_BUDGET} outer iterations ({REF_BUDGET * Q * C3_BS} row projections) "
+              f"of the c3 RKAB solve (q={Q}, bs={C3_BS}, distributed scheme) on the same 160000x20000 matrix, "
+              f"oracle/kz_oracle.c with {cores} pthreads over the workers; loop wall time only")
+    emit({"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+          "warmup": args.warmup, "ms_per_step": 1e3 * loop_s / args.steps, "higher_is_better": True,
+          "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic (counter-keyed c3 generator, seed 0, generated on the GPU and copied back)",
+          "config": c3_config(world),
+          "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                           "host": host_info()},
+          "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
-def _oracle_kw(kw):
-    out = dict(variant=kw["variant"], q=kw.get("q", 1), block_size=kw.get("block_size", 1))
-    return out
+def x_digest(x) -> str:
+    return hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()[:16]
 
 
-def _rows_per_iter(kw):
-    return kw.get("q", 1) * (kw.get("block_size", 1) if kw["variant"] == "rkab" else 1)
-
-
-def cpu_baseline(name, system, kw, budget_s=12.0):
-    import oracle as O
-
-    cores = O.max_threads()
-    rows, t, seeds = 0, 0.0, 0
-    while t < budget_s and seeds < 10:
-        t0 = time.perf_counter()
-        r = O.solve(system.A, system.b, system.x_star, base_seed=seeds, nthreads=cores, **_oracle_kw(kw))
-        t += time.perf_counter() - t0
-        rows += r["iterations"] * _rows_per_iter(kw)
-        seeds += 1
-    return {"value": rows / t, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{seeds} full solves to eps (seeds 0..{seeds - 1}) of {name}, oracle/kz_oracle.c pthreads"}
-
-
-def sharded_extras(rank, world, local_rank, steps=3):
-    """BASELINE config 3 row-sharded across the ranks: rows/s over all GPUs (max-over-ranks
-    time), RKAB bs = 1000 (1 outer iteration per step) and RKA (200 iterations per step)."""
+def run_b200(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2401_17474_b200 import SolverConfig
-    from paper_2401_17474_b200.multigpu import CudaShard, ShardComm, plan_shards, solve_sharded, solve_sharded_native
+    from paper_2401_17474_b200 import LinearSystem, SolverConfig, solve_rkab_seq
+    from paper_2401_17474_b200 import _native as N
+    from paper_2401_17474_b200.multigpu import CudaShard, ShardComm, plan_shards, solve_sharded_native
 
-    out = []
-    m_total, n, q = 160000, 20000, 64
-    try:
-        plan = plan_shards(m_total, world, rank, q)
-        shard = CudaShard.counter(m_total, n, plan, 0, local_rank)
-        comm = ShardComm(local_rank, world, rank)  # NCCL communicator (+ the fused exchange for RKA)
-        cases = (("c3_sharded_rkab_bs1000", dict(variant="rkab", q=q, block_size=1000), 1, "native",
-                  "native loop: local step + ncclAllReduce per outer iteration"),
-                 ("c3_sharded_rka", dict(variant="rka", q=q), 200, "fused",
-                  "fused: one launch per chunk, column sums exchanged in-kernel over NVLink peer memory"),
-                 ("c3_sharded_rka_nccl_loop", dict(variant="rka", q=q), 200, "native",
-                  "native loop: step kernel + ncclAllReduce per outer iteration, device stop flag"),
-                 ("c3_sharded_rka_host_loop", dict(variant="rka", q=q), 200, "host",
-                  "host-driven loop (multigpu.solve_sharded, torch.distributed all_reduce)"))
-        for tag, kw, budget, mode, how in cases:
-            cfg = SolverConfig(device=local_rank, sampling_scheme="distributed", **kw)
+    torch.cuda.set_device(local_rank)
+    dev = f"cuda:{local_rank}"
+    t_setup = time.perf_counter()
+    plan = plan_shards(C3_M, world, rank, C3_Q)
+    shard = CudaShard.counter(C3_M, C3_N, plan, C3_SEED, local_rank)
+    comm = ShardComm(local_rank, world, rank) if world > 1 else None
+    cfg = SolverConfig(variant="rkab", q=C3_Q, block_size=C3_BS, sampling_scheme="distributed", device=local_rank)
+    setup_s = time.perf_counter() - t_setup
 
-            def run(c):
-                if mode == "host":
-                    return solve_sharded(shard, c, budget=budget)
-                return solve_sharded_native(shard, c, budget=budget, comm=comm, fused=(mode == "fused"))
+    def step(k):
+        return solve_sharded_native(shard, cfg.replace(base_seed=k % SEEDS), comm=comm)
 
-            run(cfg)  # warm-up
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            rows0 = shard.rows
-            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ev0.record()
-            for k in range(steps):
-                run(cfg.replace(base_seed=k))
-            ev1.record()
-            torch.cuda.synchronize()
-            tt = torch.tensor([ev0.elapsed_time(ev1)], device=f"cuda:{local_rank}")
-            rr = torch.tensor([float(shard.rows - rows0)], device=f"cuda:{local_rank}")
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                dist.all_reduce(rr, op=dist.ReduceOp.SUM)
-            rows_s = float(rr.item()) / (float(tt.item()) / 1e3)
-            out.append({"workload": tag, "n_gpus": world, "rows_per_s": rows_s, "ms_per_step": float(tt.item()) / steps,
-                        "desc": f"160000x20000 counter-keyed, rows sharded x{world}, q={q} per GPU, "
-                                f"{budget} outer iteration(s) per step; {how}",
-                        "hbm_frac_per_gpu": rows_s / world * 8 * n / 1e9 / read_peak()[0]})
-        shard.close()
+    for w in range(args.warmup):
+        r = step(w)
+        assert r.converged, f"warm-up seed {w % SEEDS} did not converge"
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = N.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for k in range(args.steps):
+            reps.append(step(k))
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = N.launch_count() - launches0
+    t_ms = ev0.elapsed_time(ev1)
+    rows = sum(r.iterations * C3_Q * C3_BS for r in reps)
+    kernel_ms = sum(r.gpu["kernel_ms"] for r in reps)
+    for r in reps:
+        assert r.converged, f"seed {r.seed} did not converge"
+    digests = [x_digest(r.x) for r in reps]
+    agree = None
+    tt = torch.tensor([t_ms], device=dev)
+    rr = torch.tensor([float(rows)], device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rr, op=dist.ReduceOp.SUM)
+        every = [None] * world
+        dist.all_gather_object(every, digests)
+        agree = all(d == digests for d in every)
+        assert agree, "ranks disagree on x (the all-reduced iterate must be bit-identical on every rank)"
+    t_all_ms, rows_all = float(tt.item()), float(rr.item())
+
+    # e2e through the public API from pinned host arrays: per step the H2D of this rank's rows,
+    # the solve and the D2H of x (N = 1: the reference entry point solve_rkab_seq on a host
+    # LinearSystem; N > 1: a CudaShard uploaded from host rows + the sharded solve)
+    pinned = lambda *shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
+    A_h, b_h, xr_h = pinned(plan.m_local, C3_N), pinned(plan.m_local), pinned(C3_N)
+    shard.ds.download(out=(A_h, b_h, xr_h))
+    e2e_steps = min(args.steps, 3)
+
+    def e2e_step(k):
+        c = cfg.replace(base_seed=k % SEEDS)
+        if world == 1:
+            return solve_rkab_seq(LinearSystem(A=A_h, b=b_h, x_star=xr_h, seed=C3_SEED), c)
+        sh = CudaShard(A_h, b_h, xr_h, plan, device=local_rank)
+        try:
+            return solve_sharded_native(sh, c, comm=comm)
+        finally:
+            sh.close()
+
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e2e_rows = 0
+    for k in range(e2e_steps):
+        r = e2e_step(k)
+        e2e_rows += r.iterations * C3_Q * C3_BS
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    ee = torch.tensor([e2e_s], device=dev)
+    er = torch.tensor([float(e2e_rows)], device=dev)
+    if world > 1:
+        dist.all_reduce(ee, op=dist.ReduceOp.MAX)
+        dist.all_reduce(er, op=dist.ReduceOp.SUM)
+    e2e_val = float(er.item()) / float(ee.item())
+    h2d = A_h.nbytes + b_h.nbytes + xr_h.nbytes
+    d2h = C3_N * 8
+
+    extras = []
+    if world == 1 and not args.no_extra:
+        extras = extra_workloads(local_rank, read_peak()[0])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+
+        cores = O.max_threads()
+        s = oracle_sample(A_h, b_h, xr_h, C3_Q, CPU_BASELINE_BUDGET, 0, cores)
+        cpu = {"value": s["rows"] / s["loop_s"], "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{CPU_BASELINE_BUDGET} outer iterations ({s['rows']} row projections) of the c3 RKAB solve, "
+                         f"seed 0, same matrix and configuration, oracle/kz_oracle.c with {cores} pthreads over the "
+                         f"workers (the GPU's decomposition: all workers of one solve in parallel); loop wall time",
+               "host": host_info()}
+    del A_h, b_h, xr_h
+    shard.close()
+    if comm is not None:
         comm.close()
-    except Exception as exc:  # extras must never sink the headline line
-        out.append({"error": repr(exc)})
-    return out
+    if rank != 0:
+        return
+
+    peak, peak_src = read_peak()
+    bytes_per_row = 8 * C3_N
+    achieved = rows * bytes_per_row / (kernel_ms / 1e3) / 1e9
+    traffic, traffic_note = None, None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):  # measured once with ncu --set full (never under this timing run)
+        tr = json.load(open(tpath)).get("c3")
+        if tr:
+            traffic = tr["dram_bytes_per_launch"]
+            traffic_note = {k: tr[k] for k in ("launch", "algorithmic_bytes_per_launch", "source", "note") if k in tr}
+    value = rows_all / (t_all_ms / 1e3)
+    solve_ms = [r.gpu["loop_ms"] for r in reps]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_all_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (counter-keyed generator keyed on (seed, i, j), seed 0, generated in place on each GPU)",
+        "config": c3_config(world),
+        "time_to_eps_ms": {"mean": float(np.mean(solve_ms)), "min": float(np.min(solve_ms)),
+                           "max": float(np.max(solve_ms))},
+        "iterations": [r.iterations for r in reps],
+        "seeds": [r.seed for r in reps],
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "traffic_detail": traffic_note, "peak_source": peak_src,
+                     "kernel": reps[-1].gpu.get("kernel"),
+                     "algorithmic_bytes": "8*n = 160000 bytes per row projection; one outer iteration = "
+                                          f"{C3_Q} workers x {C3_BS} rows = 10.24 GB per GPU",
+                     "note": "achieved = rows x 8n / summed device time of the solve-kernel launches (CUDA events "
+                             "on the launching stream, rank 0)"},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "api": "solve_rkab_seq(LinearSystem(host arrays), cfg)" if world == 1
+                else "CudaShard(host rows) + solve_sharded_native"},
+        "gpu_launches": launches,
+        "setup_s": setup_s,
+    }
+    if world > 1:
+        line["rank_agreement"] = {"bitwise_x_all_steps": agree, "digests": digests}
+    if extras:
+        line["extra_workloads"] = extras
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    emit(line)
 
 
 def extra_workloads(device, peak, steps=3):
-    """The other BASELINE configurations on this GPU (same metric; fixed budgets for
-    the large ones, time-to-eps for c0 / c2).  Kernel-time roofline per workload."""
+    """The other BASELINE configurations on this GPU (same metric; fixed budgets for the RKA
+    shapes, time-to-eps where the configuration asks for it).  Kernel-time roofline each."""
     import torch
 
-    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, SolverConfig, generate_mother, run_solver
+    from paper_2401_17474_b200 import (DeviceSystem, GeneratorConfig, LinearSystem, SolverConfig, generate_mother,
+                                       run_solver, solve_concurrent, solve_seeds)
 
     out = []
 
-    def measure(tag, ds, n, cfg, budget, desc, n_steps=steps, warm_budget=None):
-        run_solver(ds, cfg, budget=warm_budget or budget)  # warm-up
+    def measure(tag, ds, n, cfg, budget, desc, n_steps=steps):
+        run_solver(ds, cfg, budget=budget)  # warm-up
         torch.cuda.synchronize()
         rows, kms, lms, its, conv = 0, 0.0, 0.0, [], []
         for k in range(n_steps):
@@ -257,282 +393,123 @@ def extra_workloads(device, peak, steps=3):
         gbs = rows * 8 * n / (kms / 1e3) / 1e9
         out.append({"workload": tag, "desc": desc, "rows_per_s": rows / (lms / 1e3),
                     "ms_per_step": lms / n_steps, "iterations": its, "kernel": r.gpu["kernel"],
-                    "ctas": r.gpu["ctas"], "threads": r.gpu["threads"],
+                    "ctas": r.gpu["ctas"], "threads": r.gpu["threads"], "plan": r.gpu.get("plan"),
                     **({"converged": conv} if budget is None else {}),
                     "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak}})
 
-    try:
-        ds = DeviceSystem(m=160000, n=20000, device=device)
-        ds.generate_counter(0)
-        measure("c3_rkab_bs1000", ds, 20000, SolverConfig(variant="rkab", q=64, block_size=1000,
-                sampling_scheme="distributed", device=device), 1,
-                "c3: 160000x20000 counter-keyed, RKAB q=64 bs=1000 distributed, 1 outer iteration per step")
-        measure("c3_rka", ds, 20000, SolverConfig(variant="rka", q=64, sampling_scheme="distributed", device=device),
-                200, "c3: 160000x20000 counter-keyed, RKA q=64 distributed, 200 iterations per step")
-        measure("c3_rkab_bs1", ds, 20000, SolverConfig(variant="rkab", q=64, block_size=1,
-                sampling_scheme="distributed", device=device), 200,
-                "c3: RKAB q=64 bs=1 (= RKA) distributed, 200 iterations per step")
-        # north_star target: a solve to ||x - x*||^2 < 1e-8 at n >= 2000 (one solve, ~2 s)
-        measure("c3_rkab_bs1000_to_eps", ds, 20000, SolverConfig(variant="rkab", q=64, block_size=1000,
-                sampling_scheme="distributed", device=device), None,
-                "c3: 160000x20000 counter-keyed, RKAB q=64 bs=1000 distributed, solved to ||x-x*||^2<1e-8",
-                n_steps=1, warm_budget=1)
-        ds.close()
+    def guarded(fn):
+        try:
+            fn()
+        except Exception as exc:  # extras must never sink the headline line
+            out.append({"error": f"{fn.__name__}: {exc!r}"})
+
+    def c3_rka():
+        with DeviceSystem(m=C3_M, n=C3_N, device=device) as ds:
+            ds.generate_counter(C3_SEED)
+            measure("c3_rka", ds, C3_N, SolverConfig(variant="rka", q=64, sampling_scheme="distributed",
+                                                       device=device), 400,
+                    "c3: 160000x20000 counter-keyed, RKA q=64 (bs=1) distributed, 400 iterations per step")
+
+    def c4():
         s4 = generate_mother(GeneratorConfig(m_max=80000, n_max=2000, seed=0))
-        ds = DeviceSystem(s4, device=device)
-        measure("c4_rka_q64", ds, 2000, SolverConfig(variant="rka", q=64, device=device), 2000,
-                "c4 shape 80000x2000: RKA q=64, 2000 iterations per step")
-        measure("c4_rka_q512", ds, 2000, SolverConfig(variant="rka", q=512, device=device), 500,
-                "c4 shape 80000x2000: RKA q=512, 500 iterations per step")
-        measure("c4_rk_q1", ds, 2000, SolverConfig(variant="rk", device=device), 20000,
-                "c4 shape 80000x2000: RK (q=1), 20000 iterations per step")
-        measure("c4shape_rkab_bs2000_to_eps", ds, 2000, SolverConfig(variant="rkab", q=64, block_size=2000,
-                device=device), None, "c4 shape 80000x2000 consistent: RKAB q=64 bs=2000, solved to ||x-x*||^2<1e-8")
-        ds.close()
+        with DeviceSystem(s4, device=device) as ds:
+            measure("c4_rka_q64", ds, 2000, SolverConfig(variant="rka", q=64, device=device), 2000,
+                    "c4 shape 80000x2000: RKA q=64, 2000 iterations per step")
+            measure("c4_rka_q512", ds, 2000, SolverConfig(variant="rka", q=512, device=device), 500,
+                    "c4 shape 80000x2000: RKA q=512, 500 iterations per step")
+            measure("c4_rk_q1", ds, 2000, SolverConfig(variant="rk", device=device), 20000,
+                    "c4 shape 80000x2000: RK (q=1), 20000 iterations per step")
+            measure("c4shape_rkab_bs2000_to_eps", ds, 2000, SolverConfig(variant="rkab", q=64, block_size=2000,
+                    device=device), None, "c4 shape 80000x2000 consistent: RKAB q=64 bs=2000, solved to 1e-8")
         # c4 proper: inconsistent b_LS = b + xi (sysgen.py:175-176), x_LS by CGLS on the device,
         # RKA horizons = mean of the last 10 trace records (harness.py:192-196), SURVEY 8(d) budgets
-        from paper_2401_17474_b200 import LinearSystem
         from paper_2401_17474_b200.sysgen import TAG_NOISE, Prng
 
         b_ls = s4.b + Prng(0, TAG_NOISE).standard_normal(size=s4.m)
         inc = LinearSystem(A=s4.A, b=b_ls, x_star=None, x_ls=None, consistent=False, seed=0)
-        ds = DeviceSystem(inc, device=device)
-        t0 = time.perf_counter()
-        x_ls = ds.cgls(tol=1e-12)
-        cg_ms = (time.perf_counter() - t0) * 1e3
-        from paper_2401_17474_b200 import solve_concurrent
+        with DeviceSystem(inc, device=device) as ds:
+            t0 = time.perf_counter()
+            x_ls = ds.cgls(tol=1e-12)
+            cg_ms = (time.perf_counter() - t0) * 1e3
+            for q, budget in ((1, 120000), (64, 60000), (512, 48000)):
+                cfg = SolverConfig(variant="rka" if q > 1 else "rk", q=q, device=device, max_iterations=budget)
+                cfgs = [cfg.replace(base_seed=k) for k in range(SEEDS)]
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                rs = solve_concurrent(ds, cfgs, lanes=1 if q > 64 else SEEDS, x_ref=x_ls, trace_step=1000)
+                e1.record()
+                torch.cuda.synchronize()
+                wall_ms = e0.elapsed_time(e1)
+                hs = [float(np.mean([t.error_norm for t in r.trace[-10:]])) for r in rs]
+                h = float(np.mean(hs))
+                rows = sum(r.gpu["rows_projected"] for r in rs)
+                # every trace record carries ||Ax - b||: records are evaluated 32 to a pass over A
+                gemv_bytes = sum(-(-len(r.trace) // 32) for r in rs) * 8 * (inc.m * 2000 + inc.m)
+                kms = sum(r.gpu["kernel_ms"] for r in rs)
+                gbs = rows * 8 * 2000 / (kms / 1e3) / 1e9
+                g = rs[0].gpu
+                tot = (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9
+                out.append({"workload": f"c4_horizon_q{q}", "desc": f"c4: 80000x2000 inconsistent (noise seed 0), "
+                            f"{'RK' if q == 1 else 'RKA'} q={q}, {budget} iterations, trace every 1000 vs CGLS "
+                            f"x_LS, solver seeds 0..9", "rows_per_s": rows / (wall_ms / 1e3), "ms_per_step": wall_ms,
+                            "iterations": [r.iterations for r in rs], "kernel": g["kernel"], "ctas": g["ctas"],
+                            "horizon_norm": h, "horizon_sq": h * h, "horizon_norm_per_seed": hs,
+                            "trace_records": len(rs[0].trace), "cgls_ms": cg_ms,
+                            "cgls_iterations": ds.cgls_iterations,
+                            "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
+                                         "note": "per-solve kernel time"},
+                            "step_traffic": {"row_bytes": rows * 8 * 2000, "residual_bytes": gemv_bytes,
+                                             "gbs": tot, "frac": tot / peak}})
 
-        for q, budget in ((1, 120000), (64, 60000), (512, 48000)):
-            # the 10 solver seeds (BASELINE c4), side by side where the plan leaves room (q=512
-            # occupies 7 clusters: one at a time)
-            cfg = SolverConfig(variant="rka" if q > 1 else "rk", q=q, device=device, max_iterations=budget)
-            cfgs = [cfg.replace(base_seed=k) for k in range(10)]
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            rs = solve_concurrent(ds, cfgs, lanes=1 if q > 64 else 10, x_ref=x_ls, trace_step=1000)
-            e1.record()
-            torch.cuda.synchronize()
-            wall_ms = e0.elapsed_time(e1)
-            hs = [float(np.mean([t.error_norm for t in r.trace[-10:]])) for r in rs]
-            h = float(np.mean(hs))
-            rows = sum(r.gpu["rows_projected"] for r in rs)
-            # passes over A for ||Ax - b||: the trace records go 32 to a pass, + the final residual
-            gemv_bytes = sum(-(-len(r.trace) // 32) + 1 for r in rs) * 8 * (inc.m * 2000 + inc.m)
-            kms = sum(r.gpu["kernel_ms"] for r in rs)
-            gbs = rows * 8 * 2000 / (kms / 1e3) / 1e9
-            g = rs[0].gpu
-            out.append({"workload": f"c4_horizon_q{q}", "desc": f"c4: 80000x2000 inconsistent (noise seed 0), "
-                        f"{'RK' if q == 1 else 'RKA'} q={q}, {budget} iterations, trace every 1000 vs CGLS x_LS, "
-                        f"solver seeds 0..9",
-                        "rows_per_s": rows / (wall_ms / 1e3), "ms_per_step": wall_ms,
-                        "iterations": [r.iterations for r in rs], "kernel": g["kernel"], "ctas": g["ctas"],
-                        "horizon_norm": h, "horizon_sq": h * h, "horizon_norm_per_seed": hs,
-                        "trace_records": len(rs[0].trace), "cgls_ms": cg_ms, "cgls_iterations": ds.cgls_iterations,
-                        "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
-                                     "note": "per-solve kernel time"},
-                        # every trace record carries ||Ax - b|| (harness trace semantics): one pass
-                        # over A per 32 records and one for the final residual, on top of the row bytes
-                        "step_traffic": {"row_bytes": rows * 8 * 2000, "residual_bytes": gemv_bytes,
-                                         "gbs": (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9,
-                                         "frac": (rows * 8 * 2000 + gemv_bytes) / (wall_ms / 1e3) / 1e9 / peak}})
-        ds.close()
+    def c2():
         s2 = generate_mother(GeneratorConfig(m_max=80000, n_max=1000, seed=0))
-        ds = DeviceSystem(s2, device=device)
-        measure("c2", ds, 1000, SolverConfig(variant="rkab", q=64, block_size=500, device=device), None,
-                "c2: RKAB q=64 bs=500 80000x1000, solve to eps")
-        ds.close()
-        # c1's row width and q with the rows streamed from HBM (c1's 80 MB stays in the
-        # 126 MB L2; this 400000 x 500 system (1.6 GB) does not)
-        s1c = generate_mother(GeneratorConfig(m_max=400000, n_max=500, seed=0))
-        ds = DeviceSystem(s1c, device=device)
-        del s1c
-        measure("c1shape_hbm_rka_q64", ds, 500, SolverConfig(variant="rka", q=64, device=device), 4000,
-                "c1 row width and q=64 on a 400000x500 system (1.6 GB > L2): RKA, 4000 iterations per step")
-        ds.close()
+        with DeviceSystem(s2, device=device) as ds:
+            measure("c2", ds, 1000, SolverConfig(variant="rkab", q=64, block_size=500, device=device), None,
+                    "c2: RKAB q=64 bs=500 80000x1000, solve to eps")
+
+    def c1():
+        # c1's 10 seed-solves side by side (solve_concurrent: 10 lanes, one 16-CTA cluster each)
+        s1 = generate_mother(GeneratorConfig(m_max=20000, n_max=500, seed=0))
+        cfg = SolverConfig(variant="rka", q=64, device=device)
+        with DeviceSystem(s1, device=device) as ds:
+            cfgs = [cfg.replace(base_seed=k) for k in range(SEEDS)]
+            solve_concurrent(ds, cfgs, lanes=SEEDS)
+            best = None
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                rs = solve_concurrent(ds, cfgs, lanes=SEEDS)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1)
+                best = (ms, rs) if best is None or ms < best[0] else best
+            ms, rs = best
+            rows = sum(r.gpu["rows_projected"] for r in rs)
+            alone = run_solver(ds, cfg)
+            out.append({"workload": "c1_ten_seeds", "desc": "c1: RKA q=64 20000x500, the 10 seed-solves to eps side "
+                        "by side (solve_concurrent)", "rows_per_s": rows / (ms / 1e3), "ms_per_step": ms,
+                        "iterations": [r.iterations for r in rs], "converged": [r.converged for r in rs],
+                        "kernel": rs[0].gpu["kernel"], "one_solve_alone_ms": alone.gpu["loop_ms"]})
+
+    def c0():
         s0 = generate_mother(GeneratorConfig(m_max=2000, n_max=50, seed=0))
-        ds = DeviceSystem(s0, device=device)
-        measure("c0", ds, 50, SolverConfig(variant="rk", device=device), None, "c0: RK 2000x50, solve to eps")
-        # the configuration's 10 seeds in one launch per chunk (kz_solve_seeds: a warp per seed)
-        from paper_2401_17474_b200 import solve_seeds
+        with DeviceSystem(s0, device=device) as ds:
+            c0cfg = SolverConfig(variant="rk", device=device)
+            solve_seeds(ds, c0cfg, list(range(SEEDS)))
+            best = None
+            for _ in range(3):
+                rb = solve_seeds(ds, c0cfg, list(range(SEEDS)))
+                if best is None or rb[0].gpu["loop_ms"] < best[0].gpu["loop_ms"]:
+                    best = rb
+            rows = sum(r.iterations for r in best)
+            out.append({"workload": "c0_ten_seeds", "desc": "c0: RK 2000x50, the 10 solver seeds to eps side by side "
+                        "(one warp each, one launch per chunk)", "rows_per_s": rows / (best[0].gpu["loop_ms"] / 1e3),
+                        "ms_per_step": best[0].gpu["loop_ms"], "iterations": [r.iterations for r in best],
+                        "converged": [r.converged for r in best], "kernel": "warp"})
 
-        c0cfg = SolverConfig(variant="rk", device=device)
-        solve_seeds(ds, c0cfg, list(range(10)))
-        best = None
-        for _ in range(3):
-            rb = solve_seeds(ds, c0cfg, list(range(10)))
-            if best is None or rb[0].gpu["loop_ms"] < best[0].gpu["loop_ms"]:
-                best = rb
-        rows = sum(r.iterations for r in best)
-        out.append({"workload": "c0_seed_batch", "desc": "c0: RK 2000x50, the 10 solver seeds to eps side by side "
-                    "(one warp each, one launch per chunk)", "rows_per_s": rows / (best[0].gpu["loop_ms"] / 1e3),
-                    "ms_per_step": best[0].gpu["loop_ms"], "iterations": [r.iterations for r in best],
-                    "converged": [r.converged for r in best], "kernel": "warp", "ctas": 10, "threads": 32})
-        ds.close()
-    except Exception as exc:  # extras must never sink the headline line
-        out.append({"error": repr(exc)})
+    for fn in (c3_rka, c4, c2, c1, c0):
+        guarded(fn)
     return out
-
-
-SEEDS = 10  # BASELINE configs: every workload is solved for 10 solver seeds
-
-
-def seed_batch(cfg, base):
-    """One step: the configuration's 10 seed-solves (solver seeds base .. base + 9)."""
-    return [cfg.replace(base_seed=base + j) for j in range(SEEDS)]
-
-
-def run_b200(args, name, rank, world, local_rank):
-    """A step is one batch of the workload's 10 seed-solves to epsilon on the resident system,
-    run side by side (solve_concurrent: 10 lanes, each a system view with its own stream; one
-    16-CTA cluster per c1 solve, so up to 7 solves are co-resident).  Every rank runs its own
-    batch (solver seeds 10 * rank + 0..9): weak scaling, no collective on the data path."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver, solve_concurrent
-    from paper_2401_17474_b200 import _native as N
-    from paper_2401_17474_b200.solvers import release_pool
-
-    torch.cuda.set_device(local_rank)
-    system, kw = build_system(name)
-    m, n = system.A.shape
-    cfg = SolverConfig(device=local_rank, **kw)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local_rank}")
-    ds = DeviceSystem(system, device=local_rank)
-    base = SEEDS * rank
-    for w in range(args.warmup):
-        solve_concurrent(ds, seed_batch(cfg, base), lanes=SEEDS)
-    # one seed alone: the time-to-eps of a single solve (the latency the batch hides)
-    alone = [run_solver(ds, c) for c in seed_batch(cfg, base)[:3]]
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches0 = N.launch_count()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    rows = 0
-    kernel_ms = 0.0
-    iters, solve_ms = [], []
-    kernel_name = None
-    with ClockSampler(local_rank) as clk:
-        for k in range(args.steps):
-            flush.fill_(k & 0xFF)
-            starts[k].record()
-            rs = solve_concurrent(ds, seed_batch(cfg, base), lanes=SEEDS)
-            ends[k].record()
-            for r in rs:
-                assert r.converged, f"seed {r.seed} did not converge"
-                rows += r.gpu["rows_projected"]
-                kernel_ms += r.gpu["kernel_ms"]
-                kernel_name = r.gpu["kernel"]
-                solve_ms.append(r.gpu["loop_ms"])
-            if k == 0:
-                iters = [r.iterations for r in rs]
-        torch.cuda.synchronize()
-    launches = N.launch_count() - launches0
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t_ms = float(sum(step_ms))
-    tot_rows = float(rows)
-    if world > 1:
-        tt = torch.tensor([t_ms], device=f"cuda:{local_rank}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        rr = torch.tensor([tot_rows], device=f"cuda:{local_rank}")
-        dist.all_reduce(rr, op=dist.ReduceOp.SUM)
-        tot_rows = float(rr.item())
-        dist.barrier()
-    # the reference protocol's replay leg (harness.py:152-177): budget = ceil(mean iterations to eps),
-    # fixed-budget replays with the stop rule off, one solve at a time
-    budget = int(math.ceil(float(np.mean(iters))))
-    rep_ms = []
-    for k in range(3):
-        rr_ = run_solver(ds, cfg.replace(base_seed=base + k), budget=budget)
-        assert rr_.error_evals == 0
-        rep_ms.append(rr_.gpu["loop_ms"])
-    replay = {"budget": budget, "ms_per_run": float(np.mean(rep_ms)),
-              "rows_per_s": budget * _rows_per_iter(kw) / (float(np.mean(rep_ms)) / 1e3),
-              "note": "timed_replay protocol: one solve at a time, stop rule off"}
-    ds.close()
-
-    # e2e through the public API with pinned host arrays: per step the H2D upload of A, b, x*,
-    # the 10 seed-solves and the D2H of every x
-    from paper_2401_17474_b200 import LinearSystem
-
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    hsys = LinearSystem(A=pin(system.A), b=pin(system.b), x_star=pin(system.x_star), seed=0)
-    solve_concurrent(hsys, seed_batch(cfg, base), lanes=SEEDS)  # warm the allocation pool
-    torch.cuda.synchronize()
-    e2e_rows = 0
-    t0 = time.perf_counter()
-    for k in range(args.steps):
-        for r in solve_concurrent(hsys, seed_batch(cfg, base), lanes=SEEDS):
-            e2e_rows += r.gpu["rows_projected"]
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    release_pool()
-    e2e_val = float(e2e_rows) / e2e_s
-    if world > 1:
-        ee = torch.tensor([e2e_s], device=f"cuda:{local_rank}")
-        dist.all_reduce(ee, op=dist.ReduceOp.MAX)
-        e2e_val = world * float(e2e_rows) / float(ee.item())
-    h2d = system.A.nbytes + system.b.nbytes + system.x_star.nbytes
-    d2h = SEEDS * n * 8
-    extras = []
-    if world > 1 and not args.no_extra:
-        extras = sharded_extras(rank, world, local_rank)
-
-    if rank != 0:
-        return
-    peak, peak_src = read_peak()
-    bytes_per_row = 8 * n
-    achieved = rows * bytes_per_row / (kernel_ms / 1e3) / 1e9
-    traffic, traffic_note = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
-    if os.path.exists(tpath):  # measured once with ncu --set full (never under this timing run)
-        tr = json.load(open(tpath)).get(name)
-        if tr:
-            traffic = tr["dram_bytes_per_launch"]
-            traffic_note = {k: tr[k] for k in ("launch", "algorithmic_bytes_per_launch", "source", "note")}
-    value = tot_rows / (t_ms / 1e3)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (reference generator restated on numpy, seed 0; bitwise = reference)",
-        "config": {"workload": WORKLOADS[name][3] + f", {SEEDS} seeds per step", "m": m, "n": n, **kw,
-                   "seeds": f"solver seeds {SEEDS} * rank + 0..{SEEDS - 1}, solved side by side "
-                            f"({SEEDS} lanes, solve_concurrent)",
-                   "l2": "256 MiB write between steps, outside the timed windows",
-                   "parallelism": f"{world} GPU(s), each its own batch of seed-solves, no collective",
-                   "kernel": kernel_name},
-        "time_to_eps_ms": {"alone_mean": float(np.mean([r.gpu["loop_ms"] for r in alone])),
-                           "in_batch_mean": float(np.mean(solve_ms)), "in_batch_max": float(np.max(solve_ms)),
-                           "batch_of_10_mean": float(np.mean(step_ms))},
-        "iterations": iters,
-        "replay": replay,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "traffic_detail": traffic_note, "peak_source": peak_src,
-                     "kernel": f"kz::rka/chain ({kernel_name})",
-                     "algorithmic_bytes": "8*n per row projection",
-                     "aggregate_gbs": value / world * bytes_per_row / 1e9,
-                     "note": "achieved = one solve's row bytes / its own kernel time (per launch); aggregate_gbs = "
-                             "all concurrent solves' row bytes / step time on one GPU"},
-        "clocks": clk.summary(),
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-    }
-    if world > 1:
-        line["sharded_extras"] = extras
-    elif not args.no_extra:
-        line["extra_workloads"] = extra_workloads(local_rank, peak)
-        line["sharded_extras"] = sharded_extras(0, 1, local_rank)  # the row-sharded path at N = 1
-        # north_star: oracle-matching solves to ||x - x*||^2 < 1e-8 at n >= 2000 vs the 60 % HBM target
-        line["north_star_n_ge_2000"] = [
-            {"workload": w["workload"], "time_to_eps_ms": w["ms_per_step"], "iterations": w["iterations"],
-             "converged": w.get("converged"), "rows_per_s": w["rows_per_s"], "hbm_frac": w["roofline"]["frac"]}
-            for w in line["extra_workloads"] if w.get("workload", "").endswith("_to_eps")]
-    if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(name, system, kw)
-    emit(line)
 
 
 _JSON_OUT = None  # the process's original stdout: the one JSON line goes there, everything else to stderr
@@ -544,37 +521,64 @@ def emit(line) -> None:
     out.flush()
 
 
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without a launcher: one process per GPU through torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE workloads")
+    return ap.parse_args(argv)
+
+
 def main():
     global _JSON_OUT
+    args = parse_args()
+    if args.warmup < 3:
+        sys.exit("bench.py: at least 3 warm-up steps (--warmup >= 3)")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    world = int(env_world or "1")
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} disagrees with WORLD_SIZE={world}")
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     # libraries print to stdout at the C level (e.g. NCCL's version banner): keep stdout for the
     # JSON line only by pointing fd 1 at stderr for the rest of the run
     sys.stdout.flush()
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c1")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE workloads")
-    args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl" if args.impl == "b200" else "gloo")
     if args.impl == "reference":
-        run_reference(args, args.workload, rank, world)
-    else:
-        run_b200(args, args.workload, rank, world, local_rank)
+        run_reference(args, rank, world, local_rank)  # rank 0 alone; no process group needed
+        return
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.destroy_process_group()
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -174,6 +174,9 @@ typedef struct {
 /* kz_params.flags: stop-mode launches of at most 2048 outer iterations (instead of growing to
  * the index buffer's capacity) -- for solves running side by side on one GPU. */
 #define KZ_FLAG_SHORT_LAUNCHES 2
+/* kz_params.flags: kz_solve_sharded without a communicator (one rank) runs its per-iteration
+ * sharded loop instead of delegating to kz_solve's chunked kernels (tests of the loop itself). */
+#define KZ_FLAG_SHARDED_LOOP 4
 
 typedef struct {
     int64_t iterations;     /* RunReport.iterations                                           */
@@ -190,6 +193,10 @@ typedef struct {
     int64_t kernel_launches;/* kernels launched by this call                                  */
     int32_t ctas;           /* CTAs of the solve kernel                                       */
     int32_t threads;        /* threads per CTA of the solve kernel                            */
+    int32_t plan_ep;        /* chain kernel: 16-byte column pairs per thread (EP); rka: pairs per lane */
+    int32_t plan_rows;      /* chain kernel: rows per CTA reduction (R)                        */
+    int32_t plan_cluster;   /* CTAs per thread-block cluster (chain: CTAs per worker)           */
+    int32_t plan_stages;    /* shared-memory ring stages                                        */
 } kz_result;
 
 /* Full solve with host output x_host (n values, may be NULL). */
@@ -272,7 +279,10 @@ KZ_API int32_t kz_comm_exchange_connect(kz_comm* comm, const uint8_t* handles);
  * together (distributed.py:233-235).  params: variant RKA or RKAB, scheme
  * KZ_SCHEME_RANGES (kz_sampler_set_ranges with the rank's worker blocks),
  * worker_offset = rank * q, stop or budget mode (no trace / checkpoints);
- * partial_dev is ignored.  result->rows_projected counts this rank's rows. */
+ * partial_dev is ignored.  result->rows_projected counts this rank's rows.
+ * With comm = NULL (one rank, nothing to exchange) the solve is kz_solve on the shard's
+ * worker ranges -- whole chunks of outer iterations per launch -- unless
+ * KZ_FLAG_SHARDED_LOOP asks for the per-iteration loop. */
 KZ_API int32_t kz_solve_sharded(kz_system* shard, kz_comm* comm, const kz_params* params, kz_result* result,
                                 double* x_host, void* stream);
 

@@ -55,6 +55,7 @@ class _Result(C.Structure):
         ("error_evals", C.c_int64),
         ("n_ckpt", C.c_int64),
         ("bad_row", C.c_int64),
+        ("loop_seconds", C.c_double),
     ]
 
 
@@ -180,4 +181,5 @@ def solve(A, b, x_ref, *, variant="rk", q=1, block_size=1, alphas=None, base_see
         "error_evals": int(r.error_evals),
         "x": x,
         "checkpoints": ck[: r.n_ckpt].copy(),
+        "loop_seconds": float(r.loop_seconds),
     }

@@ -22,6 +22,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
+#include <time.h>
 #include <unistd.h>
 
 typedef unsigned __int128 u128;
@@ -180,6 +181,44 @@ static double einsum_sqnorm(const double* r, int64_t n) {
 
 void kzo_row_sqnorms(const double* A, int64_t m, int64_t n, int64_t lda, double* out) {
     for (int64_t i = 0; i < m; ++i) out[i] = einsum_sqnorm(A + i * lda, n);
+}
+
+/* Row norms over row bands on `nt` threads: each row is still one einsum_sqnorm, so the
+ * result is bitwise the serial one (the CPU baseline's setup on 25.6 GB systems). */
+typedef struct {
+    const double* A;
+    int64_t m, n, lda;
+    double* out;
+    int tid, nt;
+} norms_arg_t;
+
+static void* norms_body(void* argp) {
+    norms_arg_t* a = (norms_arg_t*)argp;
+    const int64_t r0 = (a->m * a->tid) / a->nt, r1 = (a->m * (a->tid + 1)) / a->nt;
+    for (int64_t i = r0; i < r1; ++i) a->out[i] = einsum_sqnorm(a->A + i * a->lda, a->n);
+    return NULL;
+}
+
+static void row_sqnorms_mt(const double* A, int64_t m, int64_t n, int64_t lda, double* out, int nt) {
+    if (nt <= 1 || m < 4096) {
+        kzo_row_sqnorms(A, m, n, lda, out);
+        return;
+    }
+    if (nt > 256) nt = 256;
+    pthread_t th[256];
+    norms_arg_t args[256];
+    for (int i = 0; i < nt; ++i) {
+        args[i] = (norms_arg_t){A, m, n, lda, out, i, nt};
+        if (i > 0) pthread_create(&th[i], NULL, norms_body, &args[i]);
+    }
+    norms_body(&args[0]);
+    for (int i = 1; i < nt; ++i) pthread_join(th[i], NULL);
+}
+
+static double now_seconds(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
 
 static int64_t first_zero(const double* sq, int64_t m) {
@@ -498,7 +537,7 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
         rc = KZO_ENOMEM;
         goto done;
     }
-    kzo_row_sqnorms(A, m, n, n, sq);
+    row_sqnorms_mt(A, m, n, n, sq, p->nthreads);
     R.sq = sq;
     r->bad_row = first_zero(sq, m);
     if (r->bad_row >= 0) {
@@ -522,6 +561,7 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
     int64_t evals = 0;
 
     const int nt = (p->nthreads > 1 && p->variant != KZO_RK && p->variant != KZO_CK) ? p->nthreads : 1;
+    const double t_loop0 = now_seconds(); /* the reference times the loop only (solvers.py:203-208) */
     if (nt <= 1) {
         for (;;) {
             if (use_stop) {
@@ -569,6 +609,7 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
         evals = S.evals;
         n_ck = S.n_ck;
     }
+    r->loop_seconds = now_seconds() - t_loop0;
     r->iterations = k;
     r->converged = converged;
     r->final_error_sq = use_stop ? e : 0.0;

@@ -74,6 +74,7 @@ typedef struct {
     int64_t error_evals;
     int64_t n_ckpt;
     int64_t bad_row;          /* KZO_EDEGENERATE: first zero row            */
+    double loop_seconds;      /* wall time of the iteration loop alone      */
 } kzo_result;
 
 /* SeedSequence(entropy).generate_state(n_words, uint32) */

@@ -94,6 +94,10 @@ class Result(C.Structure):
         ("kernel_launches", C.c_int64),
         ("ctas", C.c_int32),
         ("threads", C.c_int32),
+        ("plan_ep", C.c_int32),
+        ("plan_rows", C.c_int32),
+        ("plan_cluster", C.c_int32),
+        ("plan_stages", C.c_int32),
     ]
 
 

@@ -57,6 +57,16 @@ static int fail(int code, const char* fmt, ...) {
         if (rc_ != KZ_OK) return rc_; \
     } while (0)
 
+// Experiment switches (plan overrides, phase timing, ablations) are read only when
+// KZ_EXPERIMENTS=1 is set in the environment: a production solve never consults them.
+static const char* dbg_env(const char* name) {
+    static const bool on = [] {
+        const char* e = getenv("KZ_EXPERIMENTS");
+        return e != nullptr && atoi(e) != 0;
+    }();
+    return on ? getenv(name) : nullptr;
+}
+
 static int check_launch(const char* what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
@@ -844,9 +854,12 @@ void* chain_fn(int ep, int R, int C) {
         case 20801: return (void*)chain_kernel<8, 1, 2>;
         case 20802: return (void*)chain_kernel<8, 2, 2>;
         case 21601: return (void*)chain_kernel<16, 1, 2>;
-                case 40104: return (void*)chain_kernel<1, 4, 4>;
+        case 40104: return (void*)chain_kernel<1, 4, 4>;
         case 40204: return (void*)chain_kernel<2, 4, 4>;
         case 40404: return (void*)chain_kernel<4, 4, 4>;
+        case 40801: return (void*)chain_kernel<8, 1, 4>;
+        case 40802: return (void*)chain_kernel<8, 2, 4>;
+        case 41601: return (void*)chain_kernel<16, 1, 4>;
         case 80104: return (void*)chain_kernel<1, 4, 8>;
         case 80204: return (void*)chain_kernel<2, 4, 8>;
         default: return nullptr;
@@ -865,19 +878,8 @@ constexpr int MAXG_CLUSTERS = 10;  // = MAXG in kz_sync.cu
 
 }  // namespace
 
-static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
-    // a worker is one CTA, or a CTA pair (thread-block cluster of 2, each CTA
-    // half the columns) when the rows are long and the pairs fit the SMs
-    int C = (s->ld >= 1024 && 2 * q <= s->sms && !s->no_pairs) ? 2 : 1;  // measured: pairs win from n ~ 1000
-    // one chain (RK, CK) over long rows: a cluster of 4 (measured on 80000 x 2000 with the
-    // producer warp: 0.40 us per row against 0.42 for 8 CTAs and 0.45 for a pair; at n = 512
-    // the pair is best)
-    if (q == 1 && s->ld >= 1536 && s->ld % 8 == 0 && !s->no_pairs) C = 4;
-    if (const char* e = getenv("KZ_CHAIN_PAIR")) {  // experiment: 1, 2, or (one chain, q = 1) 4 / 8
-        const int want = atoi(e);
-        C = want == 2 && 2 * q <= s->sms ? 2 : ((want == 4 || want == 8) && q == 1 ? want : 1);
-    }
-    if (C > 2 && (s->ld % (2 * C) != 0 || s->no_pairs)) C = 2;  // column slices of whole 16-byte pairs
+// Chain-kernel plan for a worker of C CTAs (a thread-block cluster of C column slices).
+static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan& pl) {
     const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
     int ep = 0, T = 0;
@@ -901,7 +903,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     int R = ep <= 4 ? 4 : (ep == 8 ? 2 : 1);  // R = 8 measured slower since the reduction got cheap
     if (C == 2) R = std::min(R, 4);
     if (C > 2) R = std::min(R, 4);
-    if (const char* e = getenv("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
+    if (const char* e = dbg_env("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
     const int64_t ldc = s->ld / C;
     const int64_t stage_bytes = ldc * (int64_t)sizeof(double);
     int stages = 0;
@@ -909,7 +911,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         while (R > 1 && !chain_fn(ep, R, C)) R /= 2;
         const int64_t fixed = chain_smem(ldc, 0, R, T, C);
         stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
-        if (const char* e = getenv("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
+        if (const char* e = dbg_env("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
         if (stages >= R + 1 || R == 1) break;
         R = R > 4 ? 4 : (R > 2 ? 2 : 1);
     }
@@ -936,6 +938,32 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     return KZ_OK;
 }
 
+// A worker is one CTA, or a cluster of C CTAs each owning ld / C columns: a pair when the rows
+// are long and the pairs fit the SMs, 4 for one long chain (RK, CK).  When the preferred width
+// has no kernel for the row length (the EP x R x C instantiations in kz_chain.cu) or does not
+// fit, narrower clusters are tried, so every n up to the chain kernel's limit is accepted:
+// 16 pairs x 320 threads x 2 columns per CTA, i.e. n <= 10240 C (C = 1, 2, or 4 for q = 1).
+static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
+    int C = (s->ld >= 1024 && 2 * q <= s->sms && !s->no_pairs) ? 2 : 1;  // measured: pairs win from n ~ 1000
+    // one chain (RK, CK) over long rows: a cluster of 4 (measured on 80000 x 2000 with the
+    // producer warp: 0.40 us per row against 0.42 for 8 CTAs and 0.45 for a pair; at n = 512
+    // the pair is best)
+    if (q == 1 && s->ld >= 1536 && !s->no_pairs) C = 4;
+    if (const char* e = dbg_env("KZ_CHAIN_PAIR")) {  // experiment: 1, 2, or (one chain, q = 1) 4 / 8
+        const int want = atoi(e);
+        C = want == 2 && 2 * q <= s->sms ? 2 : ((want == 4 || want == 8) && q == 1 ? want : 1);
+    }
+    int rc = KZ_EINVAL;
+    std::string first_err;
+    for (int c = C; c >= 1; c /= 2) {
+        if (c > 1 && (s->ld % (2 * c) != 0 || s->no_pairs || c * q > s->sms)) continue;  // whole 16-byte pairs
+        rc = plan_chain_c(s, p, q, c, pl);
+        if (rc == KZ_OK) return KZ_OK;
+        if (first_err.empty()) first_err = g_err;
+    }
+    return fail(rc, "%s", first_err.empty() ? "no chain-kernel plan" : first_err.c_str());
+}
+
 static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, Plan& pl) {
     pl.threads = 256;
     if (q > 512) return fail(KZ_EINVAL, "q=%lld exceeds the sync kernel's 512 workers", (long long)q);
@@ -951,7 +979,7 @@ static int plan_sync(kz_system* s, const kz_params* p, int64_t q, bool cluster, 
             // several clusters once every CTA of one cluster would carry > 128 columns
             G = (int)std::max<int64_t>(1, std::min<int64_t>(MAXG_CLUSTERS, s->ld / (16 * 128)));
         }
-        if (const char* e = getenv("KZ_SYNC_CLUSTERS")) G = std::max(1, std::min(MAXG_CLUSTERS, atoi(e)));
+        if (const char* e = dbg_env("KZ_SYNC_CLUSTERS")) G = std::max(1, std::min(MAXG_CLUSTERS, atoi(e)));
     } else {
         P = p->ctas > 0 ? p->ctas : s->sms;
     }
@@ -1042,7 +1070,7 @@ void* rka_fn_t(int lg, int epl) {
 void* rka_fn(int lg, int epl, bool sr, int mode = 0) {
     if (mode == 1) return sr ? rka_fn_t<false, true, 1>(lg, epl) : rka_fn_t<false, false, 1>(lg, epl);
     if (mode == 2) return sr ? rka_fn_t<false, true, 2>(lg, epl) : rka_fn_t<false, false, 2>(lg, epl);
-    const bool tm = getenv("KZ_PHASE_TIMING") != nullptr;
+    const bool tm = dbg_env("KZ_PHASE_TIMING") != nullptr;
     if (tm) return sr ? rka_fn_t<true, true, 0>(lg, epl) : rka_fn_t<true, false, 0>(lg, epl);
     return sr ? rka_fn_t<false, true, 0>(lg, epl) : rka_fn_t<false, false, 0>(lg, epl);
 }
@@ -1127,13 +1155,13 @@ static int plan_rka_wg(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     const int lg = npairs <= 8 ? 8 : (npairs <= 16 ? 16 : 32);
     const int epl = lg == 32 ? (npairs + 31) / 32 : 1;
     int G = (int)std::min<int64_t>(RKA_MAXG, (q + 8 * RKA_NW - 1) / (8 * RKA_NW));
-    if (const char* e = getenv("KZ_RKA_WG_G")) G = std::max(2, std::min(RKA_MAXG, atoi(e)));
+    if (const char* e = dbg_env("KZ_RKA_WG_G")) G = std::max(2, std::min(RKA_MAXG, atoi(e)));
     for (int guard = 0; guard < 16 && G >= 2; ++guard) {
         const int64_t qmax = (q + G - 1) / G;
         const size_t stage = rka_smem(qmax, box, 1, Pc) - rka_smem(qmax, box, 0, Pc);
         const size_t fixed = rka_smem(qmax, box, 0, Pc);
         int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);
-        if (const char* e = getenv("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+        if (const char* e = dbg_env("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
         if (stages < 2 || rka_smem(qmax, box, stages, Pc) > kSmemLimit) {
             ++G;  // fewer workers per cluster
             if (G > RKA_MAXG) break;
@@ -1184,11 +1212,11 @@ static int plan_rka_wg(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
 }
 
 static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
-    if (getenv("KZ_SYNC_V5")) return fail(KZ_EINVAL, "rka kernel disabled (KZ_SYNC_V5)");
+    if (dbg_env("KZ_SYNC_V5")) return fail(KZ_EINVAL, "rka kernel disabled (KZ_SYNC_V5)");
     if (q > 512) return fail(KZ_EINVAL, "q=%lld exceeds the rka kernel's 512 workers", (long long)q);
     const int64_t ld = s->ld;
     {
-        const char* e = getenv("KZ_RKA_WG");
+        const char* e = dbg_env("KZ_RKA_WG");
         const bool want = e ? atoi(e) != 0 : true;
         if (want && q > 8 * RKA_NW && p->ctas == 0 && p->partial_dev == nullptr && plan_rka_wg(s, p, q, pl) == KZ_OK)
             return KZ_OK;
@@ -1205,7 +1233,7 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         // 80000 x 2000, q = 64: 1 cluster 2.54 us / iteration, 3 clusters 2.89 us)
         G = 1;
     }
-    if (const char* e = getenv("KZ_SYNC_CLUSTERS")) G = atoi(e);
+    if (const char* e = dbg_env("KZ_SYNC_CLUSTERS")) G = atoi(e);
     G = std::max<int>(G, (int)((ld + Pc * 256 - 1) / (Pc * 256)));
     G = std::max(1, std::min(RKA_MAXG, G));
     int gcap = RKA_MAXG;
@@ -1221,12 +1249,12 @@ static int plan_rka(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
         const int npairs = box / 2;
         int lg = npairs <= 8 ? 8 : (npairs <= 16 ? 16 : 32);
         int epl = lg == 32 ? (npairs + 31) / 32 : 1;
-        if (const char* e = getenv("KZ_RKA_LG8"))  // experiment: 8 lanes per row, 2 pairs per lane
+        if (const char* e = dbg_env("KZ_RKA_LG8"))  // experiment: 8 lanes per row, 2 pairs per lane
             if (atoi(e) && npairs <= 16) lg = 8, epl = 2;
         const size_t stage = rka_smem(q, box, 1, Pc) - rka_smem(q, box, 0, Pc);
         const size_t fixed = rka_smem(q, box, 0, Pc);
         int stages = (int)std::min<int64_t>(8, ((int64_t)kSmemLimit - (int64_t)fixed) / (int64_t)stage);
-        if (const char* e = getenv("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+        if (const char* e = dbg_env("KZ_SYNC_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
         if (stages < 2 || rka_smem(q, box, stages, Pc) > kSmemLimit) {
             ++G;  // thinner slices
             continue;
@@ -1291,7 +1319,10 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
     if (pl.kernel == KZ_KERNEL_CHAIN) {
         fn = chain_fn(pl.ep, pl.rows, pl.pair);
         int na = 0;
-        if (pl.ctas > 1) {
+        // KZ_NO_COOP (experiments): drop the cooperative attribute so a profiler can replay the
+        // launch; safe only when every CTA fits at once (one per SM, ctas <= SMs)
+        static const bool no_coop = dbg_env("KZ_NO_COOP") != nullptr;
+        if (pl.ctas > 1 && !(no_coop && pl.ctas <= s->sms)) {
             attr2[na].id = cudaLaunchAttributeCooperative;
             attr2[na].val.cooperative = 1;
             ++na;
@@ -1439,7 +1470,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {
         if (bs != 1) return fail(KZ_EINVAL, "the sync kernels run RKA / RKAB with block_size 1 only");
         int rc = kern == KZ_KERNEL_SYNC_CLUSTER ? plan_rka(s, p, q, pl) : KZ_EINVAL;
-        if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && getenv("KZ_DEBUG_PLAN"))
+        if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && dbg_env("KZ_DEBUG_PLAN"))
             fprintf(stderr, "[kz plan] rka kernel not used: %s\n", g_err.c_str());
         if (rc != KZ_OK) rc = plan_sync(s, p, q, kern == KZ_KERNEL_SYNC_CLUSTER, pl);
         if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && p->kernel == KZ_KERNEL_AUTO)
@@ -1453,6 +1484,10 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     r->kernel_used = pl.kernel;
     r->ctas = pl.ctas;
     r->threads = pl.threads;
+    r->plan_ep = pl.kernel == KZ_KERNEL_CHAIN || pl.kernel == KZ_KERNEL_WARP ? pl.ep : pl.epl;
+    r->plan_rows = pl.kernel == KZ_KERNEL_CHAIN ? pl.rows : 1;
+    r->plan_cluster = pl.kernel == KZ_KERNEL_CHAIN ? pl.pair : pl.cluster;
+    r->plan_stages = pl.stages;
 
     // --- scratch ---
     const int64_t draws_per_iter = q * bs;
@@ -1498,8 +1533,8 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     args.box = pl.box;
     args.wg = pl.wg ? 1 : 0;
     if (pl.tma) KZ_TRY(ensure_tmaps(s, pl.box));
-    const bool phase_timing = getenv("KZ_PHASE_TIMING") != nullptr;
-    args.ablate = getenv("KZ_ABLATE") ? atoi(getenv("KZ_ABLATE")) : 0;
+    const bool phase_timing = dbg_env("KZ_PHASE_TIMING") != nullptr;
+    args.ablate = dbg_env("KZ_ABLATE") ? atoi(dbg_env("KZ_ABLATE")) : 0;
     if (phase_timing) {
         KZ_TRY(s->dbg.ensure(32 * 128));
         KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 128 * sizeof(long long), st));
@@ -1544,6 +1579,10 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
         args.stages = pl.stages;
         r->ctas = pl.ctas;
         r->threads = pl.threads;
+        r->plan_ep = pl.ep;
+        r->plan_rows = pl.rows;
+        r->plan_cluster = pl.pair;
+        r->plan_stages = pl.stages;
         if (pl.ctas > 1) KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
         lrc = launch_solve(s, pl, args, st);
     }
@@ -1767,7 +1806,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             fprintf(stderr, "[kz phase end, max over warps, cycles from start] top %.0f issued %.0f dots %.0f waited %.0f "
                             "err %.0f scales %.0f update %.0f | iteration %.0f (n=%d)\n", acc[0] / nrec, acc[1] / nrec,
                     acc[2] / nrec, acc[3] / nrec, acc[4] / nrec, acc[5] / nrec, acc[6] / nrec, span / nrec, nrec);
-        if (atoi(getenv("KZ_PHASE_TIMING")) >= 2) {  // per-warp mean stamps relative to the earliest warp start
+        if (atoi(dbg_env("KZ_PHASE_TIMING")) >= 2) {  // per-warp mean stamps relative to the earliest warp start
             double pw[8][16] = {{0}};
             int nk = 0;
             for (int k = 4; k < 31; ++k) {
@@ -2340,6 +2379,15 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     if (comm && comm->device != s->device)
         return fail(KZ_EINVAL, "communicator on device %d, shard on device %d", comm->device, s->device);
     const int world = comm ? comm->world : 1;
+    if (!comm && !(p->flags & KZ_FLAG_SHARDED_LOOP)) {
+        // one rank and no communicator: the local sum is the whole sum, x = S / q is kz_solve's
+        // in-kernel average, so the chunked single-GPU driver runs the identical iteration
+        kz_params pp = *p;
+        pp.partial_dev = nullptr;
+        pp.k_start = 0;
+        pp.keep_x = 0;
+        return kz_solve(s, &pp, r, x_host, stream);
+    }
     cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
     KZ_TRY(s->S.ensure(2 * s->ld));  // two worker-sum buffers: step k writes S[k % 2], reads S[(k - 1) % 2]

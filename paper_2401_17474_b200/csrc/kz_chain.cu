@@ -594,10 +594,13 @@ KZ_CHAIN(4, 4, 2)
 KZ_CHAIN(8, 1, 2)
 KZ_CHAIN(8, 2, 2)
 KZ_CHAIN(16, 1, 2)
-// one long RK / CK chain over a cluster of 4 or 8 CTAs (q = 1)
+// one long RK / CK chain over a cluster of 4 or 8 CTAs (q = 1); EP 8 / 16: n up to 40960
 KZ_CHAIN(1, 4, 4)
 KZ_CHAIN(2, 4, 4)
 KZ_CHAIN(4, 4, 4)
+KZ_CHAIN(8, 1, 4)
+KZ_CHAIN(8, 2, 4)
+KZ_CHAIN(16, 1, 4)
 KZ_CHAIN(1, 4, 8)
 KZ_CHAIN(2, 4, 8)
 #undef KZ_CHAIN

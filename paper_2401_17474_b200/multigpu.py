@@ -186,21 +186,24 @@ class ShardComm:
 
 
 def solve_sharded_native(shard: "CudaShard", cfg, *, budget: int | None = None, comm: ShardComm | None = None,
-                         fused: bool = True) -> RunReport:
+                         fused: bool = True, loop: bool = False) -> RunReport:
     """The same protocol as :func:`solve_sharded`, run by the library (kz_solve_sharded).
     RKA with ``fused`` (default): one step-kernel launch per chunk of outer iterations, the
     ranks' column sums exchanged inside the kernel over NVLink peer memory (the communicator's
     exchange buffers) and the stop rule applied in-kernel.  Otherwise (RKAB, or fused=False):
     per outer iteration a local step, an in-place NCCL all-reduce and x = S / Q, enqueued on one
     stream without a host round trip; a device stop flag freezes x at the stopping iteration.
-    Same iteration counts as the host-driven loop; the same x bit for bit at one rank."""
+    Same iteration counts as the host-driven loop; the same x bit for bit at one rank.
+    Without a communicator (one rank) the library runs kz_solve's chunked kernels on the shard
+    unless ``loop`` asks for the per-iteration loop."""
     plan = shard.plan
     if comm is None and plan.world > 1:
         raise ValueError("a multi-rank sharded solve needs a ShardComm")
     if comm is not None and fused and cfg.variant == "rka":
         comm.connect_exchange(shard.ds.pitch)
     t0 = time.perf_counter()
-    r = shard.ds.solve_sharded(cfg, worker_offset=plan.worker_offset, comm=comm, budget=budget, fused=fused)
+    r = shard.ds.solve_sharded(cfg, worker_offset=plan.worker_offset, comm=comm, budget=budget, fused=fused,
+                               loop=loop)
     wall = time.perf_counter() - t0
     shard.rows += r["rows"]
     shard.kernel_ms += r["loop_ms"]
@@ -211,7 +214,8 @@ def solve_sharded_native(shard: "CudaShard", cfg, *, budget: int | None = None, 
                      final_residual=float("nan"), error_evals=r["error_evals"], x=r["x"],
                      gpu={"world": plan.world, "q_local": plan.q_local, "shard": (plan.lo, plan.hi),
                           "native": True, "fused": bool(fused and comm is not None and cfg.variant == "rka"),
-                          "loop_ms": r["loop_ms"], "launches": r["launches"]})
+                          "loop_ms": r["loop_ms"], "kernel_ms": r["kernel_ms"], "launches": r["launches"],
+                          "kernel": r["kernel"], "ctas": r["ctas"], "threads": r["threads"], "plan": r["plan"]})
 
 
 def solve_sharded(shard, cfg, *, budget: int | None = None, group=None) -> RunReport:

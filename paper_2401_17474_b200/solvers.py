@@ -184,13 +184,20 @@ class DeviceSystem:
         self._xref_set = True
         self._refresh_views()
 
-    def download(self, m2: int | None = None, n2: int | None = None):
-        """(A[:m2, :n2], b[:m2], x_ref[:n2]) copied to the host."""
+    def download(self, m2: int | None = None, n2: int | None = None, out=None):
+        """(A[:m2, :n2], b[:m2], x_ref[:n2]) copied to the host (into ``out`` = (A, b, x_ref)
+        C-contiguous float64 arrays of those shapes when given, e.g. pinned buffers)."""
         m2 = self.m if m2 is None else m2
         n2 = self.n if n2 is None else n2
-        A = np.empty((m2, n2))
-        b = np.empty(m2)
-        xr = np.empty(n2)
+        if out is not None:
+            A, b, xr = out
+            for a, shp in ((A, (m2, n2)), (b, (m2,)), (xr, (n2,))):
+                if a.shape != shp or a.dtype != np.float64 or not a.flags.c_contiguous:
+                    raise DimensionMismatchError(f"download buffer {a.shape} {a.dtype} does not match {shp} f64")
+        else:
+            A = np.empty((m2, n2))
+            b = np.empty(m2)
+            xr = np.empty(n2)
         N.check(self._lib.kz_system_download(self.handle, m2, n2, N.ptr(A), N.ptr(b), N.ptr(xr), None))
         return A, b, xr
 
@@ -289,7 +296,7 @@ class DeviceSystem:
                 "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches)}
 
     def solve_sharded(self, cfg: "SolverConfig", *, worker_offset: int, comm=None, budget: int | None = None,
-                      alphas=None, fused: bool = True) -> dict:
+                      alphas=None, fused: bool = True, loop: bool = False) -> dict:
         """The whole row-sharded _drive loop of this shard natively (kz_solve_sharded): per outer
         iteration the local step, an in-place all-reduce of the worker sum over ``comm`` (a
         :class:`ShardComm`; None = one rank) and x = S / (q * world) with the stop rule on the
@@ -311,16 +318,18 @@ class DeviceSystem:
         p.kernel = N.KERNELS[cfg.kernel]
         p.threads, p.ctas = int(cfg.threads), int(cfg.ctas)
         p.worker_offset = int(worker_offset)
-        p.flags = 0 if fused else 1  # KZ_FLAG_NO_FUSED_EXCHANGE
+        p.flags = (0 if fused else 1) | (4 if loop else 0)  # KZ_FLAG_NO_FUSED_EXCHANGE, KZ_FLAG_SHARDED_LOOP
         r = N.Result()
         x = np.empty(self.n, dtype=np.float64)
         N.check(self._lib.kz_solve_sharded(self.handle, None if comm is None else comm.handle, C.byref(p),
                                            C.byref(r), N.ptr(x), None))
         return {"iterations": int(r.iterations), "converged": bool(r.converged),
                 "final_error_sq": float(r.final_error_sq), "error_evals": int(r.error_evals), "x": x,
-                "rows": int(r.rows_projected), "loop_ms": float(r.loop_ms),
+                "rows": int(r.rows_projected), "loop_ms": float(r.loop_ms), "kernel_ms": float(r.kernel_ms),
                 "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches),
-                "ctas": int(r.ctas), "threads": int(r.threads)}
+                "ctas": int(r.ctas), "threads": int(r.threads),
+                "plan": {"ep": int(r.plan_ep), "rows": int(r.plan_rows), "cluster": int(r.plan_cluster),
+                         "stages": int(r.plan_stages)}}
 
     def set_x(self, x=None) -> None:
         """Overwrite the resident iterate (None = zeros)."""
@@ -388,6 +397,7 @@ class DeviceSystem:
             rc = self._lib.kz_system_view_refresh(v.handle)
             if rc not in (N.KZ_OK, N.KZ_EDEGENERATE):  # a zero row surfaces at solve time, as in the reference
                 N.check(rc)
+            v._xref_set = self._xref_set  # views alias the base's x_ref: its state, not the one at creation
 
     def view(self) -> "DeviceSystem":
         """A view for concurrent solves (kz_system_view): it shares this system's matrix, b,
@@ -604,6 +614,8 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
             "launches": int(r.kernel_launches),
             "ctas": int(r.ctas),
             "threads": int(r.threads),
+            "plan": {"ep": int(r.plan_ep), "rows": int(r.plan_rows), "cluster": int(r.plan_cluster),
+                     "stages": int(r.plan_stages)},
             "checkpoint_every": every,
         },
     )

@@ -89,9 +89,9 @@ def _native_vs_host(s, variant, q, bs, seed, budget=None, comm=None, kernel="aut
     shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
     cfg = SolverConfig(variant=variant, q=q, block_size=bs, base_seed=seed, sampling_scheme="distributed",
                        kernel=kernel)
-    rn = solve_sharded_native(shard, cfg, budget=budget, comm=comm)
+    rn = solve_sharded_native(shard, cfg, budget=budget, comm=comm, loop=True)
     rh = solve_sharded(shard, cfg, budget=budget)
-    rn2 = solve_sharded_native(shard, cfg, budget=budget, comm=comm)  # a second solve on the same shard
+    rn2 = solve_sharded_native(shard, cfg, budget=budget, comm=comm, loop=True)  # a second solve, same shard
     shard.close()
     return rn, rh, rn2
 
@@ -134,12 +134,37 @@ def test_native_sharded_max_iterations(gpu, oracle):
     plan = plan_shards(s.m, 1, 0, 8)
     shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
     cfg = SolverConfig(variant="rka", q=8, base_seed=1, sampling_scheme="distributed", max_iterations=150)
-    rn = solve_sharded_native(shard, cfg)
+    rn = solve_sharded_native(shard, cfg, loop=True)
     rh = solve_sharded(shard, cfg)
     shard.close()
     assert not rn.converged and rn.iterations == rh.iterations == 150
     assert rn.error_evals == rh.error_evals == 151
     assert np.array_equal(rn.x, rh.x)
+
+
+@pytest.mark.parametrize("variant,q,bs", [("rka", 8, 1), ("rkab", 4, 6)])
+def test_one_rank_without_comm_runs_kz_solve(gpu, oracle, variant, q, bs):
+    """With one rank and no communicator kz_solve_sharded delegates to kz_solve's chunked kernels
+    (the bench's N = 1 headline path): same iteration counts and iterates as the per-iteration
+    sharded loop and the oracle."""
+    from paper_2401_17474_b200 import SolverConfig
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards, solve_sharded_native
+
+    s = _system()
+    plan = plan_shards(s.m, 1, 0, q)
+    shard = CudaShard(s.A, s.b, s.x_star, plan, device=0)
+    cfg = SolverConfig(variant=variant, q=q, block_size=bs, base_seed=3, sampling_scheme="distributed")
+    rd = solve_sharded_native(shard, cfg)
+    rl = solve_sharded_native(shard, cfg, loop=True)
+    rb = solve_sharded_native(shard, cfg, budget=17)
+    shard.close()
+    o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=q, block_size=bs, base_seed=3, scheme="distributed")
+    ob = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=q, block_size=bs, base_seed=3, scheme="distributed",
+                      budget=17)
+    assert rd.converged and rd.iterations == rl.iterations == o["iterations"]
+    assert rd.error_evals == o["error_evals"]
+    assert rel_err(rd.x, rl.x) <= PARITY_TOL and rel_err(rd.x, o["x"]) <= PARITY_TOL
+    assert rb.iterations == 17 and rel_err(rb.x, ob["x"]) <= PARITY_TOL
 
 
 def test_native_sharded_nccl_world1(gpu):

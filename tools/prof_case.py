@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--profile-range", action="store_true",
+                    help="bracket the timed solves with cudaProfilerStart/Stop (ncu --replay-mode app-range)")
     args = ap.parse_args()
     from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, SolverConfig, generate_mother, run_solver
 
@@ -50,6 +52,11 @@ def main():
     print(f"system {m}x{n} ({args.gen}) ready in {time.perf_counter() - t0:.1f}s", flush=True)
     with ds:
         run_solver(ds, cfg, budget=args.budget)
+        if args.profile_range:
+            import torch
+
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         for s in range(args.solves):
             t0 = time.perf_counter()
             r = run_solver(ds, cfg.replace(base_seed=s), budget=args.budget)
@@ -61,6 +68,9 @@ def main():
                   f"thr={g['threads']}) rows/s={g['rows_projected'] / (g['loop_ms'] / 1e3):.3e} "
                   f"kernelGB/s={gbs:.0f} us/it={1e3 * g['kernel_ms'] / max(r.iterations, 1):.3f} host={dt * 1e3:.1f}ms",
                   flush=True)
+        if args.profile_range:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
 
 
 if __name__ == "__main__":
