@@ -37,7 +37,7 @@ enum kz_status {
     KZ_OK = 0,
     KZ_EINVAL = 1,      /* ValueError / DimensionMismatchError (solvers.py:85-101, linalg.py:30-47) */
     KZ_EDEGENERATE = 2, /* DegenerateRowError (linalg.py:84-86)                                      */
-    KZ_EEMPTYRANGE = 3, /* EmptyRangeError (sampling.py:194-195, 213-218)                            */
+    KZ_EEMPTYRANGE = 3, /* EmptyRangeError (sampling.py:106-107, 213-218)                            */
     KZ_ENOMEM = 4,      /* device allocation failed                                                  */
     KZ_ECUDA = 5,       /* CUDA runtime / launch error                                               */
     KZ_ENODEV = 6,      /* no CUDA device                                                            */
@@ -120,14 +120,14 @@ KZ_API int32_t kz_row_norms(kz_system* sys, double* sq_host, int64_t* bad_row, v
  * kernel restates (sysgen.einsum_order_matches); sampler and packed records are rebuilt from them. */
 KZ_API int32_t kz_row_norms_upload(kz_system* sys, const double* sq_host, void* stream);
 
-/* ---- sampler: make_sampler / worker_streams (sampling.py:189-199,
+/* ---- sampler: make_sampler / worker_streams (sampling.py:101-111,
  * solvers.py:162-171) ------------------------------------------------------
  * Builds the inclusive CDF(s) for (scheme, q): one CDF over all rows
  * (full_access) or one per block partition_bounds(m, q, t) (distributed).
  * cdf_host (m values, concatenated per block) may be NULL. */
 KZ_API int32_t kz_sampler_build(kz_system* sys, int32_t scheme, int64_t q, double* cdf_host, void* stream);
 /* Row draws `start .. start+count-1` of worker `worker` for Prng(base_seed,
- * worker) (RowSampler.sample, sampling.py:177-182): bit-exact indices. */
+ * worker) (RowSampler.sample, sampling.py:89-94): bit-exact indices. */
 KZ_API int32_t kz_dump_rows(kz_system* sys, int32_t scheme, int64_t q, uint64_t base_seed, int64_t worker,
                      int64_t start, int64_t count, int32_t* out_host, void* stream);
 

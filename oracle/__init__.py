@@ -106,7 +106,7 @@ def max_threads() -> int:
 
 
 def seedseq_state(entropy, n_words=8) -> np.ndarray:
-    """SeedSequence(entropy).generate_state(n_words, uint32) (sampling.py:135)."""
+    """SeedSequence(entropy).generate_state(n_words, uint32) (sampling.py:47)."""
     ent = (C.c_uint64 * len(entropy))(*[int(e) for e in entropy])
     out = np.empty(n_words, dtype=np.uint32)
     lib().kzo_seedseq_generate(ent, len(entropy), out.ctypes.data_as(C.POINTER(C.c_uint32)), n_words)
@@ -114,7 +114,7 @@ def seedseq_state(entropy, n_words=8) -> np.ndarray:
 
 
 def random_doubles(seed: int, stream: int, count: int) -> np.ndarray:
-    """Prng(seed, stream).random() repeated (sampling.py:132-140)."""
+    """Prng(seed, stream).random() repeated (sampling.py:44-52)."""
     out = np.empty(count)
     lib().kzo_random_doubles(seed, stream, count, _dp(out))
     return out
@@ -129,7 +129,7 @@ def row_sqnorms(a) -> np.ndarray:
 
 
 def cdf(sq, lo=0, hi=None) -> np.ndarray:
-    """make_sampler's cdf (sampling.py:189-199)."""
+    """make_sampler's cdf (sampling.py:101-111)."""
     sq = _f64(sq, 1)
     hi = sq.shape[0] - 1 if hi is None else hi
     out = np.empty(max(hi - lo + 1, 1))
@@ -140,7 +140,7 @@ def cdf(sq, lo=0, hi=None) -> np.ndarray:
 
 
 def dump_rows(sq, scheme: str, q: int, seed: int, worker: int, count: int) -> np.ndarray:
-    """First `count` draws of worker `worker` (solvers.py:162-171, sampling.py:177-182)."""
+    """First `count` draws of worker `worker` (solvers.py:162-171, sampling.py:89-94)."""
     sq = _f64(sq, 1)
     out = np.empty(count, dtype=np.int64)
     rc = lib().kzo_dump_rows(_dp(sq), sq.shape[0], SCHEMES[scheme], q, seed, worker, count,

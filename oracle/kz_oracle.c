@@ -5,10 +5,10 @@
  * -ffp-contract=off so every "a*b + c" is two roundings, as numpy does.
  *
  * Reference anchors (paths relative to /root/reference/pkg/src/kaczbench):
- *   Prng / worker_rng ............ sampling.py:122-162
- *   RowSampler.sample ............ sampling.py:177-182
- *   make_sampler ................. sampling.py:189-199
- *   partition_bounds ............. sampling.py:207-219
+ *   Prng / worker_rng ............ sampling.py:34-74
+ *   RowSampler.sample ............ sampling.py:89-94
+ *   make_sampler ................. sampling.py:101-111
+ *   partition_bounds ............. sampling.py:119-131
  *   row_norm_cache ............... linalg.py:80-88
  *   kaczmarz_step ................ solvers.py:107-117
  *   rka_combined_step ............ solvers.py:120-137
@@ -227,7 +227,7 @@ static int64_t first_zero(const double* sq, int64_t m) {
     return -1;
 }
 
-/* make_sampler (sampling.py:189-199): sequential cumsum, divide by last. */
+/* make_sampler (sampling.py:101-111): sequential cumsum, divide by last. */
 int32_t kzo_cdf_build(const double* sq, int64_t m, int64_t lo, int64_t hi, double* cdf) {
     if (!(0 <= lo && lo <= hi && hi < m)) return KZO_EEMPTYRANGE;
     int64_t len = hi - lo + 1;
@@ -241,7 +241,7 @@ int32_t kzo_cdf_build(const double* sq, int64_t m, int64_t lo, int64_t hi, doubl
     return KZO_OK;
 }
 
-/* searchsorted(cdf, u, side="right") (sampling.py:179) */
+/* searchsorted(cdf, u, side="right") (sampling.py:91) */
 int64_t kzo_upper_bound(const double* cdf, int64_t len, double u) {
     int64_t lo = 0, hi = len;
     while (lo < hi) {
@@ -254,7 +254,7 @@ int64_t kzo_upper_bound(const double* cdf, int64_t len, double u) {
     return lo;
 }
 
-/* partition_bounds (sampling.py:207-219) */
+/* partition_bounds (sampling.py:119-131) */
 static int bounds(int64_t m, int64_t parts, int64_t idx, int64_t* lo, int64_t* hi) {
     if (!(0 <= idx && idx < parts)) return KZO_EEMPTYRANGE;
     *lo = (idx * m) / parts;
@@ -268,7 +268,7 @@ typedef struct {
     int64_t lo, len;
 } sampler_t;
 
-/* RowSampler.sample (sampling.py:177-182) */
+/* RowSampler.sample (sampling.py:89-94) */
 static inline int64_t sampler_draw(const sampler_t* s, kzo_pcg64* g) {
     double u = kzo_pcg64_random(g);
     int64_t j = kzo_upper_bound(s->cdf, s->len, u);

@@ -14,10 +14,10 @@
  * Third-party arithmetic restated here (numpy 2.3.5, not vendored in the
  * reference; call sites in /root/reference/pkg/src/kaczbench):
  *   - SeedSequence(entropy=(seed, stream)) -> PCG64 -> Generator.random()
- *     (sampling.py:132-140)
+ *     (sampling.py:44-52)
  *   - np.einsum("ij,ij->i") row norms, SSE2 2-lane x4 order (linalg.py:83)
- *   - np.cumsum then "/= cdf[-1]" (sampling.py:196-197)
- *   - np.searchsorted(side="right") + clamp (sampling.py:177-182)
+ *   - np.cumsum then "/= cdf[-1]" (sampling.py:108-109)
+ *   - np.searchsorted(side="right") + clamp (sampling.py:89-94)
  *   - np.sum(v_all, axis=0) sequential over workers, then "/= q"
  *     (solvers.py:136-137, 366-367)
  * np.dot (OpenBLAS ddot, runtime-dispatched kernel) is restated as a
@@ -46,7 +46,7 @@ enum {
     KZO_OK = 0,
     KZO_EINVAL = 1,       /* ValueError (solvers.py:85-101)           */
     KZO_EDEGENERATE = 2,  /* DegenerateRowError (linalg.py:84-86)     */
-    KZO_EEMPTYRANGE = 3,  /* EmptyRangeError (sampling.py:194-195,213-218) */
+    KZO_EEMPTYRANGE = 3,  /* EmptyRangeError (sampling.py:106-107,213-218) */
     KZO_ENOMEM = 4
 };
 

@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE ONLY: lets tests/test_multirank_gloo.py run the
 production host logic (paper_2401_17474_b200.multigpu.solve_sharded) over
 gloo without a GPU.  It restates the reference's per-worker arithmetic
-(solvers.py:107-117, 140-145; sampling.py:177-199) in numpy on the shard:
+(solvers.py:107-117, 140-145; sampling.py:89-111) in numpy on the shard:
 worker t draws from Prng(seed, t) over its shard-local block and the local
 step returns the ordered sum S = sum_w v_w as a torch tensor.
 """

@@ -76,7 +76,7 @@ static int check_launch(const char* what) {
 
 // ---------------------------------------------------------------------------
 // SeedSequence -> PCG64 seeding on the host (numpy bit_generator.pyx / pcg64.c,
-// as used by Prng(seed, worker), sampling.py:132-136).  Integer-exact.
+// as used by Prng(seed, worker), sampling.py:44-48).  Integer-exact.
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -575,7 +575,7 @@ extern "C" int32_t kz_system_view_refresh(kz_system* v) {
 }
 
 // ---------------------------------------------------------------------------
-// samplers (sampling.py:189-219, solvers.py:162-171)
+// samplers (sampling.py:101-131, solvers.py:162-171)
 // ---------------------------------------------------------------------------
 static int ensure_sampler(kz_system* s, int scheme, int64_t q, cudaStream_t st) {
     KZ_TRY(ensure_norms(s, st));

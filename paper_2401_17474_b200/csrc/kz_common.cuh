@@ -1,6 +1,6 @@
 // kz_common.cuh -- shared device helpers for the sm_100a RK/RKA/RKAB kernels.
 //
-// PCG64 restatement (numpy's pcg64.h as used by Prng, sampling.py:132-140):
+// PCG64 restatement (numpy's pcg64.h as used by Prng, sampling.py:44-52):
 // 128-bit LCG, output = XSL-RR of the *stepped* state, random() =
 // (out >> 11) * 2^-53.  Everything here is integer-exact.
 #pragma once
@@ -61,7 +61,7 @@ __host__ __device__ __forceinline__ Pcg pcg_from_pod(const PcgPod& p) {
     return g;
 }
 
-// searchsorted(cdf, u, side="right") clamped to len-1 (sampling.py:177-182).
+// searchsorted(cdf, u, side="right") clamped to len-1 (sampling.py:89-94).
 __device__ __forceinline__ int64_t upper_bound_clamped(const double* __restrict__ cdf, int64_t len, double u) {
     int64_t lo = 0, hi = len;
     while (lo < hi) {

@@ -2,9 +2,9 @@
 // and the residual/error norms used by traces.
 //
 //   row_sqnorm_kernel  <- row_norm_cache  (linalg.py:80-88), bit-exact einsum order
-//   cdf_scan_kernel    <- make_sampler    (sampling.py:196: np.cumsum, sequential)
-//   cdf_div_kernel     <- make_sampler    (sampling.py:197: cdf /= cdf[-1])
-//   sample_rows_kernel <- RowSampler.sample x Prng.random (sampling.py:138-140, 177-182)
+//   cdf_scan_kernel    <- make_sampler    (sampling.py:108: np.cumsum, sequential)
+//   cdf_div_kernel     <- make_sampler    (sampling.py:109: cdf /= cdf[-1])
+//   sample_rows_kernel <- RowSampler.sample x Prng.random (sampling.py:50-52, 177-182)
 //   residual kernels   <- _trace_record / final residual (solvers.py:174-179, 246)
 #include "kz_kernels.cuh"
 
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(CDF_SCAN_THREADS) cdf_scan_kernel(const double
     }
 }
 
-// cdf_j /= cdf[last of its range]  (IEEE division, sampling.py:197)
+// cdf_j /= cdf[last of its range]  (IEEE division, sampling.py:109)
 __global__ void cdf_div_kernel(double* __restrict__ cdf, const int64_t* __restrict__ lo,
                                const int64_t* __restrict__ len) {
     const int64_t r = blockIdx.y;

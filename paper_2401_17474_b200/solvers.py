@@ -227,7 +227,7 @@ class DeviceSystem:
         return out
 
     def cdf(self, scheme: str = "full_access", q: int = 1) -> np.ndarray:
-        """make_sampler cdf(s) (sampling.py:189-199), concatenated per block."""
+        """make_sampler cdf(s) (sampling.py:101-111), concatenated per block."""
         out = np.empty(self.m)
         N.check(self._lib.kz_sampler_build(self.handle, N.SCHEME_IDS[scheme], int(q), N.ptr(out), None))
         return out
@@ -650,7 +650,7 @@ def solve_rkab_seq(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_
 
 
 def _run_cgls(system, cfg, x_ref):
-    """harness._run_cgls (harness.py:343-366): CGLS on the device (kz_cgls)."""
+    """harness._run_cgls (harness.py:72-95): CGLS on the device (kz_cgls)."""
     import time
 
     own = not isinstance(system, DeviceSystem)
@@ -779,7 +779,7 @@ def solve_concurrent(system, cfgs, *, budget=None, lanes: int | None = None, x_r
 
 def run_solver(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step=None, capture=None,
                checkpoint_every=None) -> RunReport:
-    """Dispatch on cfg.variant / cfg.engine (harness.py:369-385)."""
+    """Dispatch on cfg.variant / cfg.engine (harness.py:98-114)."""
     cfg.validate()
     if cfg.variant == "cgls":
         if budget is not None or trace_step is not None:

@@ -9,14 +9,14 @@ numpy 2.3.5 / OpenBLAS 0.3.30 (third-party, pkg/pyproject.toml:10).  The
 fixtures pin:
 
 * prng.npz     -- Prng(seed, stream).random() streams and SeedSequence words
-                  (sampling.py:122-162)
+                  (sampling.py:34-74)
 * norms.npz    -- row_norm_cache(A).sq_norms for seeded matrices of many widths
                   (linalg.py:80-88)
 * systems.npz  -- sha256 of generate_mother / crop / make_inconsistent outputs
                   (sysgen.py:118-187), so the package's generator restatement
                   can be checked bitwise without the reference
 * rows.npz     -- RowSampler.sample streams per worker (solvers.py:162-171,
-                  sampling.py:177-199) for RK / RKA / RKAB configurations
+                  sampling.py:89-111) for RK / RKA / RKAB configurations
 * solves.npz   -- full reference solves: iteration counts, error_evals,
                   final_error_sq, final x and x checkpoints (capture lists)
                   for the BASELINE configs c0, c1, c2 and desk-scale cases

@@ -1,5 +1,5 @@
 """T1: the B200 sampler subsystem is bit-exact -- row norms (linalg.py:80-88),
-CDFs (sampling.py:189-199) and row-index streams (sampling.py:177-182,
+CDFs (sampling.py:101-111) and row-index streams (sampling.py:89-94,
 solvers.py:162-171) -- against the reference fixtures and the oracle."""
 
 import numpy as np
