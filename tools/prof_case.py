@@ -12,7 +12,11 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from bench import WORKLOADS  # noqa: E402
+WORKLOADS = {  # BASELINE.json configs[0..2]: (m, n, solver kwargs, description)
+    "c0": (2000, 50, dict(variant="rk", q=1), "c0: RK 2000x50"),
+    "c1": (20000, 500, dict(variant="rka", q=64), "c1: RKA q=64 20000x500"),
+    "c2": (80000, 1000, dict(variant="rkab", q=64, block_size=500), "c2: RKAB q=64 bs=500 80000x1000"),
+}
 
 
 def main():

@@ -1,14 +1,17 @@
 #!/bin/bash
-# Round profile set (run under gpurun): bench line, ncu launch list of the bench command, and
-# ncu --set full captures of the dominant kernels.  Outputs in gpurun_out/.
+# Round profile set (run under gpurun, one GPU): the bench line, the reference arm, the ncu launch
+# list of the bench command and one ncu --set full capture of the headline kernel (one c3 outer
+# iteration).  Outputs in gpurun_out/.  KZ_NO_COOP: ncu cannot replay the cooperative cluster launch.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/bench_round.json 2> gpurun_out/bench_round.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference > gpurun_out/bench_round_ref.json 2> gpurun_out/bench_round_ref.err; echo "ref rc=$?"
+export KZ_EXPERIMENTS=1 KZ_NO_COOP=1
+BCMD="python bench.py --steps 2 --warmup 3 --no-extra --no-cpu-baseline"
+$BCMD > gpurun_out/plain_bench.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv \
-  python bench.py --steps 2 --warmup 1 --no-extra --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo "launches rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:rka_kernel -c 1 -f -o gpurun_out/rka_c1 \
-  python tools/prof_case.py --workload c1 --solves 1 > gpurun_out/ncu_c1.log 2>&1; echo "c1 rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:rka_kernel -c 1 -f -o gpurun_out/rka_c4q64 \
-  python tools/prof_case.py --m 80000 --n 2000 --variant rka --q 64 --budget 2000 --solves 1 > gpurun_out/ncu_c4.log 2>&1; echo "c4q64 rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:rka_kernel -c 1 -f -o gpurun_out/rka_c4q512_wg \
-  python tools/prof_case.py --m 80000 --n 2000 --variant rka --q 512 --budget 500 --solves 1 > gpurun_out/ncu_c4wg.log 2>&1; echo "c4q512 rc=$?"
+  $BCMD > gpurun_out/ncu_launches.log 2>&1; echo "launches rc=$?"
+CMD="python tools/prof_case.py --m 160000 --n 20000 --gen counter --variant rkab --q 64 --bs 1000 --scheme distributed --budget 1 --solves 1"
+$CMD > gpurun_out/plain_c3.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:chain_kernel -s 1 -c 1 \
+  -f -o gpurun_out/c3_rkab_full $CMD > gpurun_out/ncu_c3_full.log 2>&1; echo "c3 rc=$?"
