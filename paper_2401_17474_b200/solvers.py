@@ -23,7 +23,7 @@ import numpy as np
 from . import _native as N
 from .errors import DimensionMismatchError
 from .reports import RunReport, TraceRecord
-from .sysgen import LinearSystem, cgls_solve, einsum_order_matches, partition_bounds
+from .sysgen import LinearSystem, einsum_order_matches, partition_bounds
 
 VARIANTS = ("ck", "rk", "rka", "rkab", "cgls")
 ALPHA_POLICIES = ("unit", "fixed", "optimal_full", "optimal_partial")
@@ -370,13 +370,13 @@ class DeviceSystem:
         """(lambda_max, lambda_min) of A_blk^T A_blk for rows [row_lo, row_hi] on the device
         (spectral.py:66-121; start vectors Prng(0x5EED, 0/1) normalised on the host)."""
         from .errors import SpectralConvergenceError
-        from .spectral import _START_SEED
+        from .spectral import START_SEED
         from .sysgen import Prng
 
         row_hi = self.m - 1 if row_hi is None else row_hi
-        v0 = Prng(_START_SEED, 0).standard_normal(self.n)
+        v0 = Prng(START_SEED, 0).standard_normal(self.n)
         v0 /= np.linalg.norm(v0)
-        v1 = Prng(_START_SEED, 1).standard_normal(self.n)
+        v1 = Prng(START_SEED, 1).standard_normal(self.n)
         v1 /= np.linalg.norm(v1)
         out = np.empty(2)
         rc = self._lib.kz_spectral(self.handle, C.c_int64(row_lo), C.c_int64(row_hi), N.ptr(v0), N.ptr(v1),
@@ -468,48 +468,20 @@ def release_pool() -> None:
 
 
 def resolve_alphas(system, cfg: SolverConfig, q: int | None = None) -> np.ndarray:
-    """Per-worker weights (solvers.py:148-159).  On a DeviceSystem the optimal_* policies
-    run their spectral estimates (spectral.py:66-156) on the device (kz_spectral)."""
+    """Per-worker weights (solvers.py:148-159).  The optimal_* policies run their spectral
+    estimates (spectral.py:66-156) on the device (kz_spectral): on the resident system, or
+    on a temporary upload of a host LinearSystem."""
     q = cfg.q if q is None else q
     if cfg.alpha_policy == "unit":
         return np.ones(q)
     if cfg.alpha_policy == "fixed":
         return np.full(q, float(cfg.alpha))
-    from .spectral import SpectralStats, optimal_alpha, partial_alphas, spectral_stats  # setup, off the hot path
+    from .spectral import optimal_alpha, partial_alphas, spectral_stats  # setup, off the hot path
 
-    if isinstance(system, DeviceSystem):
-        sq = system.row_norms()
-
-        def stats(lo, hi):
-            lmax, lmin = system.spectral(lo, hi)
-            fro = float(sq[lo:hi + 1].sum())  # RowNormCache.frobenius_sq (linalg.py:88)
-            return SpectralStats(sigma_max=float(np.sqrt(lmax)), sigma_min=float(np.sqrt(lmin)),
-                                 s_min=lmin / fro, s_max=lmax / fro)
-
-        m, n = system.m, system.n
-        if cfg.alpha_policy == "optimal_full":
-            return np.full(q, optimal_alpha(stats(0, m - 1), q))
-        if q > m:
-            raise ValueError(f"q={q} exceeds row count m={m}")
-        out = np.empty(q)
-        for t in range(q):
-            lo, hi = partition_bounds(m, q, t)
-            if hi - lo + 1 < n:
-                raise DimensionMismatchError(f"worker {t} block has {hi - lo + 1} rows < {n} columns; "
-                                             f"its spectral estimate would be rank deficient")
-            out[t] = optimal_alpha(stats(lo, hi), q)
-        return out
-    A = _host_matrix(system)
+    target = system if isinstance(system, DeviceSystem) else system.A
     if cfg.alpha_policy == "optimal_full":
-        return np.full(q, optimal_alpha(spectral_stats(A), q))
-    return partial_alphas(A, q)
-
-
-def _host_matrix(system):
-    host = system.host if isinstance(system, DeviceSystem) else system
-    if host is None:
-        raise ValueError("spectral weights need the host copy of A")
-    return host.A
+        return np.full(q, optimal_alpha(spectral_stats(target), q))
+    return partial_alphas(target, q)
 
 
 def _uniform_alpha(alphas: np.ndarray) -> float:

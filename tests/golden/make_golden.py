@@ -21,6 +21,10 @@ fixtures pin:
                   final_error_sq, final x and x checkpoints (capture lists)
                   for the BASELINE configs c0, c1, c2 and desk-scale cases
 * traces.npz   -- trace_run records on an inconsistent system (harness.py:180-196)
+* spectral.npz -- spectral_stats / optimal_alpha / partial_alphas (spectral.py:66-156) of
+                  seeded systems, incl. a row block too short for its estimate
+* threads.npz  -- the threaded engine's runs (parallel.py:175-304): delta-form RKA under a
+                  lock and lead-row RKAB, final x, iterations and x checkpoints
 * dist.npz     -- run_distributed_solve (distributed.py:339-363): the simulated-MPI
                   engine's RKA / RKAB (Algorithm 4: block_size + 1 rows, x / np
                   before the all-reduce) per-rank iterates
@@ -236,6 +240,61 @@ def gen_dist():
     save("dist.npz", **out)
 
 
+SPECTRAL_SYSTEMS = [("s500", 500, 20, 1), ("s2000", 2000, 50, 7), ("c0", 2000, 50, 0), ("s3000x120", 3000, 120, 4)]
+SPECTRAL_Q = [1, 2, 8, 64]
+
+
+def gen_spectral():
+    """spectral.py:66-156 executed: the extreme eigenvalue estimates, the optimal weights for
+    several q, per-block partial weights (q = 4 and 8), and the rank-deficient-block error."""
+    out = {}
+    for name, m, n, seed in SPECTRAL_SYSTEMS:
+        a = system(m, n, seed).A
+        st = kb.spectral_stats(a)
+        out[f"{name}_stats"] = np.array([st.sigma_max, st.sigma_min, st.s_min, st.s_max])
+        out[f"{name}_alpha"] = np.array([kb.optimal_alpha(st, q) for q in SPECTRAL_Q])
+        for q in (4, 8):
+            if m // q >= n:
+                out[f"{name}_partial_q{q}"] = kb.partial_alphas(a, q)
+    try:
+        kb.partial_alphas(system(500, 20, 1).A, 32)
+        out["short_block_error"] = np.array("")
+    except kb.DimensionMismatchError as exc:
+        out["short_block_error"] = np.array(str(exc))
+    out["q_list"] = np.array(SPECTRAL_Q)
+    save("spectral.npz", **out)
+
+
+THREAD_CASES = [  # (name, system, variant, q, block_size, base_seed)
+    ("s500_rka_q2", (500, 20, 1), "rka", 2, 1, 1),
+    ("s500_rka_q4", (500, 20, 1), "rka", 4, 1, 1),
+    ("s2000_rka_q8", (2000, 50, 7), "rka", 8, 1, 3),
+    ("c0_rka_q16", (2000, 50, 0), "rka", 16, 1, 0),
+    ("s500_rkab_q4_bs10", (500, 20, 1), "rkab", 4, 10, 2),
+    ("s2000_rkab_q8_bs25", (2000, 50, 7), "rkab", 8, 25, 5),
+]
+
+
+def gen_threads():
+    """parallel.py:175-304 executed: solve_rka_parallel (x += alpha (b - <a, x_prev>) / (q sq) a
+    under a lock, arrival order) and solve_rkab_parallel (lead row + block, x += (v - x) / q);
+    every iterate captured, every 10th stored."""
+    out = {}
+    for name, (m, n, seed), variant, q, bs, base in THREAD_CASES:
+        s = system(m, n, seed)
+        cfg = kb.SolverConfig(variant=variant, q=q, block_size=bs, base_seed=base)
+        cap = []
+        fn = kb.solve_rka_parallel if variant == "rka" else kb.solve_rkab_parallel
+        r = fn(s, cfg, capture=cap)
+        out[f"{name}_x"] = r.x.copy()
+        out[f"{name}_it"] = np.array(r.iterations)
+        out[f"{name}_conv"] = np.array(r.converged)
+        out[f"{name}_err"] = np.array(r.final_error_sq)
+        out[f"{name}_ckpt"] = np.array(cap[9::10]) if len(cap) >= 10 else np.zeros((0, n))
+        print(name, r.iterations, flush=True)
+    save("threads.npz", **out)
+
+
 def gen_kzsys():
     """A KZSYS v1 file written by the reference's own save_system (sysgen.py:190-214)."""
     kb.save_system(system(500, 20, 1), os.path.join(OUT, "kzsys_s500.bin"))
@@ -249,8 +308,14 @@ if __name__ == "__main__":
         gen_kzsys()
     elif len(sys.argv) > 1 and sys.argv[1] == "dist":
         gen_dist()
+    elif len(sys.argv) > 1 and sys.argv[1] == "spectral":
+        gen_spectral()
+    elif len(sys.argv) > 1 and sys.argv[1] == "threads":
+        gen_threads()
     else:
         main()
         gen_ck()
         gen_kzsys()
         gen_dist()
+        gen_spectral()
+        gen_threads()

@@ -56,7 +56,10 @@ def test_report_csv_roundtrip():
 def test_generator_restatement_is_bitwise(systems):
     from golden.common import sha
 
-    from paper_2401_17474_b200 import crop, make_inconsistent
+    from oracle.cgls_host import cgls
+
+    from paper_2401_17474_b200 import crop
+    from paper_2401_17474_b200.sysgen import inconsistent_rhs
 
     g = golden("systems.npz")
     for name in ("c0", "s500", "s2000"):
@@ -66,10 +69,12 @@ def test_generator_restatement_is_bitwise(systems):
     c = crop(systems["s2000"], 300, 40)
     assert sha(c.A) == str(g["crop300x40_A"]) and sha(c.b) == str(g["crop300x40_b"])
     assert sha(c.x_star) == str(g["crop300x40_xref"])
-    inc = make_inconsistent(systems["s2000"], noise_seed=11)
-    assert sha(inc.b) == str(g["inc2000_b"])
+    b_ls = inconsistent_rhs(systems["s2000"], noise_seed=11)
+    assert sha(b_ls) == str(g["inc2000_b"])
+    # the host CGLS checker (oracle/cgls_host.py) against the reference's x_LS
     ref = g["inc2000_xls"]
-    assert np.max(np.abs(inc.x_ls - ref)) <= 1e-8 * np.max(np.abs(ref))
+    x_ls = cgls(systems["s2000"].A, b_ls, tol=1e-10)
+    assert np.max(np.abs(x_ls - ref)) <= 1e-8 * np.max(np.abs(ref))
 
 
 def test_generator_c1_shape_is_bitwise(c1_system):
@@ -100,14 +105,23 @@ def test_harness_helpers():
 
 
 def test_spectral_alpha_formula():
-    from paper_2401_17474_b200.spectral import SpectralStats, optimal_alpha, spectral_stats
+    """optimal_alpha (spectral.py:124-134) reproduces the reference's weights from the
+    reference's own estimates, bit for bit (golden/spectral.npz), and its edge cases."""
+    from paper_2401_17474_b200.spectral import SpectralStats, optimal_alpha
 
+    g = golden("spectral.npz")
+    qs = [int(q) for q in g["q_list"]]
+    names = [k[:-len("_stats")] for k in g if k.endswith("_stats")]
+    assert len(names) >= 4
+    for name in names:
+        smax, smin, lo, hi = g[f"{name}_stats"]
+        st = SpectralStats(sigma_max=smax, sigma_min=smin, s_min=lo, s_max=hi)
+        assert [optimal_alpha(st, q) for q in qs] == list(g[f"{name}_alpha"])
     assert optimal_alpha(SpectralStats(1, 1, s_min=0.3, s_max=0.9), 1) == 1.0
     assert abs(optimal_alpha(SpectralStats(1, 1, s_min=0.5, s_max=0.5), 2) - 4 / 3) <= 1e-12
     assert abs(optimal_alpha(SpectralStats(1, 1, s_min=0.1, s_max=0.9), 3) - 2.0) <= 1e-12
-    st = spectral_stats(np.diag([1.0, 2.0, 3.0]))
-    assert abs(st.s_max - 9 / 14) <= 1e-5 and abs(st.s_min - 1 / 14) <= 1e-5
-    assert math.isfinite(st.sigma_min)
+    with pytest.raises(ValueError):
+        optimal_alpha(SpectralStats(1, 1, s_min=0.1, s_max=0.9), 0)
 
 
 def test_kzsys_round_trip_and_reference_files(tmp_path):
