@@ -54,7 +54,10 @@ enum kz_kernel {                                                  /* engine sele
     KZ_KERNEL_CHAIN = 1,        /* worker-per-CTA persistent kernel (RK, RKAB)                   */
     KZ_KERNEL_SYNC_CLUSTER = 2, /* column-sliced kernel, one thread-block cluster, DSMEM reduce  */
     KZ_KERNEL_SYNC_GRID = 3,    /* column-sliced kernel, whole grid, global-memory reduce        */
-    KZ_KERNEL_WARP = 4          /* one warp, register-resident x: RK / CK on rows of <= 256 columns */
+    KZ_KERNEL_WARP = 4,         /* one warp, register-resident x: RK / CK on rows of <= 256 columns */
+    KZ_KERNEL_RKA = 5           /* column-sliced TMA kernel (rka_kernel): the plan SYNC_CLUSTER tries
+                                   first; as a selector it has no fallback, and kz_result.kernel_used
+                                   reports it whenever it ran                                     */
 };
 
 typedef struct kz_system kz_system;
@@ -177,6 +180,11 @@ typedef struct {
 /* kz_params.flags: kz_solve_sharded without a communicator (one rank) runs its per-iteration
  * sharded loop instead of delegating to kz_solve's chunked kernels (tests of the loop itself). */
 #define KZ_FLAG_SHARDED_LOOP 4
+/* kz_params.flags: the threaded engine's combine (engine="threads", parallel.py:175-304):
+ * RKA adds alpha (b - <a_t, x>) / (q sq_t) a_t to x, RKAB adds (v_t - x) / q, in worker
+ * order, instead of the sequential engine's average.  RKA / RKAB with q > 1 only; runs
+ * on the chain kernel. */
+#define KZ_FLAG_THREADS_COMBINE 8
 
 typedef struct {
     int64_t iterations;     /* RunReport.iterations                                           */

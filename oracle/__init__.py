@@ -42,7 +42,7 @@ class _Params(C.Structure):
         ("ckpt_every", C.c_int64),
         ("ckpt_capacity", C.c_int64),
         ("nthreads", C.c_int32),
-        ("pad", C.c_int32),
+        ("combine", C.c_int32),
     ]
 
 
@@ -152,8 +152,15 @@ def dump_rows(sq, scheme: str, q: int, seed: int, worker: int, count: int) -> np
 
 def solve(A, b, x_ref, *, variant="rk", q=1, block_size=1, alphas=None, base_seed=0,
           scheme="full_access", epsilon=1e-8, max_iterations=1_000_000, budget=None,
-          ckpt_every=0, ckpt_capacity=None, nthreads=1) -> dict:
-    """The reference solve protocol (solvers.py:182-263, 294-371)."""
+          ckpt_every=0, ckpt_capacity=None, nthreads=1, engine="seq") -> dict:
+    """The reference solve protocol (solvers.py:182-263, 294-371).  engine="threads": the
+    threaded engine's combine in worker order (parallel.py:175-304); RKAB then draws
+    block_size + 1 rows per worker (the lead row), as solve_rkab_parallel does."""
+    if engine not in ("seq", "threads"):
+        raise ValueError(f"unknown engine {engine!r}")
+    threads = engine == "threads" and variant in ("rka", "rkab") and q > 1
+    if engine == "threads" and variant == "rkab":
+        block_size += 1
     A = _f64(A, 2)
     b = _f64(b, 1)
     m, n = A.shape
@@ -166,7 +173,7 @@ def solve(A, b, x_ref, *, variant="rk", q=1, block_size=1, alphas=None, base_see
     p = _Params(VARIANTS[variant], SCHEMES[scheme], q, block_size,
                 _dp(al) if al is not None else None, int(base_seed), float(epsilon),
                 int(max_iterations), int(budget or 0), int(ckpt_every), ckpt_capacity,
-                int(nthreads), 0)
+                int(nthreads), int(threads))
     r = _Result()
     x = np.empty(n)
     rc = lib().kzo_solve(_dp(A), _dp(b), _dp(xr), m, n, C.byref(p), C.byref(r), _dp(x), _dp(ck))

@@ -359,7 +359,7 @@ static double err_sq(const double* x, const double* xr, int64_t n) {
 typedef struct {
     const double *A, *b, *sq;
     int64_t m, n, q, bs;
-    int32_t variant, nthreads;
+    int32_t variant, nthreads, combine;
     const double* alphas;
     sampler_t* samplers;
     kzo_pcg64* rngs;
@@ -387,6 +387,25 @@ static void rka_average(run_t* R, double* x, int64_t c0, int64_t c1) {
     }
 }
 
+/* Threaded engine, RKA (parallel.py:214-226): the workers' increments
+ * fl(s_t a_tj), s_t = alpha (b - <a, x_prev>) / (q sq), added to x in worker order. */
+static void rka_delta(run_t* R, double* x, int64_t c0, int64_t c1) {
+    const int64_t n = R->n, q = R->q;
+    for (int64_t j = c0; j < c1; ++j)
+        for (int64_t t = 0; t < q; ++t) x[j] = x[j] + R->scales[t] * R->A[R->rows[t] * n + j];
+}
+
+/* Threaded engine, RKAB (parallel.py:286-298): v -= x_prev; x += v / q, worker order. */
+static void rkab_delta(run_t* R, double* x, int64_t c0, int64_t c1) {
+    const int64_t n = R->n, q = R->q;
+    for (int64_t j = c0; j < c1; ++j) {
+        const double xp = x[j];
+        double acc = xp;
+        for (int64_t t = 0; t < q; ++t) acc = acc + (R->vbuf[t * n + j] - xp) / (double)q;
+        x[j] = acc;
+    }
+}
+
 /* RKAB averaging (solvers.py:366-367) */
 static void rkab_average(run_t* R, double* x, int64_t c0, int64_t c1) {
     const int64_t n = R->n, q = R->q;
@@ -397,6 +416,13 @@ static void rkab_average(run_t* R, double* x, int64_t c0, int64_t c1) {
     }
 }
 
+static void combine(run_t* R, double* x, int64_t c0, int64_t c1) {
+    if (R->variant == KZO_RKA)
+        (R->combine ? rka_delta : rka_average)(R, x, c0, c1);
+    else
+        (R->combine ? rkab_delta : rkab_average)(R, x, c0, c1);
+}
+
 /* Worker part of one outer iteration (parallel over t). */
 static void worker_part(run_t* R, const double* x, int64_t t) {
     const int64_t n = R->n;
@@ -404,7 +430,10 @@ static void worker_part(run_t* R, const double* x, int64_t t) {
     if (R->variant == KZO_RKA) {
         int64_t i = sampler_draw(&R->samplers[t], &R->rngs[t]);
         R->rows[t] = i;
-        R->scales[t] = proj_scale(R->A, R->b, R->sq, n, i, x, alpha);
+        if (R->combine) /* parallel.py:221: the weight carries 1/q */
+            R->scales[t] = alpha * (R->b[i] - row_dot(R->A + i * n, x, n)) / ((double)R->q * R->sq[i]);
+        else
+            R->scales[t] = proj_scale(R->A, R->b, R->sq, n, i, x, alpha);
     } else { /* RKAB: v = x; bs chained projections (solvers.py:140-145) */
         double* v = R->vbuf + t * n;
         memcpy(v, x, sizeof(double) * (size_t)n);
@@ -428,10 +457,7 @@ static void advance_serial(run_t* R, double* x) {
         return;
     }
     for (int64_t t = 0; t < R->q; ++t) worker_part(R, x, t);
-    if (R->variant == KZO_RKA)
-        rka_average(R, x, 0, R->n);
-    else
-        rkab_average(R, x, 0, R->n);
+    combine(R, x, 0, R->n);
 }
 
 /* ---------------------------------------------------------------------
@@ -483,10 +509,7 @@ static void* mt_body(void* argp) {
         if (S->stop) break;
         for (int64_t t = tid; t < R->q; t += nt) worker_part(R, S->x, t);
         pthread_barrier_wait(&S->bar);
-        if (R->variant == KZO_RKA)
-            rka_average(R, S->x, c0, c1);
-        else
-            rkab_average(R, S->x, c0, c1);
+        combine(R, S->x, c0, c1);
         pthread_barrier_wait(&S->bar);
         if (tid == 0) {
             ++S->k;
@@ -523,6 +546,7 @@ int32_t kzo_solve(const double* A, const double* b, const double* x_ref, int64_t
     R.variant = p->variant;
     R.alphas = p->alphas;
     R.nthreads = p->nthreads;
+    R.combine = p->combine;
 
     double* sq = (double*)malloc(sizeof(double) * (size_t)m);
     double* cdf = (double*)malloc(sizeof(double) * (size_t)m);

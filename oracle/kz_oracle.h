@@ -63,7 +63,8 @@ typedef struct {
     int64_t ckpt_every;       /* > 0: store x after every ckpt_every iters  */
     int64_t ckpt_capacity;    /* rows available in ckpt_out                  */
     int32_t nthreads;         /* <= 1 serial; > 1 pthreads (bitwise identical) */
-    int32_t pad;
+    int32_t combine;          /* 0: sequential engine's average; 1: threaded engine's
+                                 increments in worker order (parallel.py:214-226, 286-298) */
 } kzo_params;
 
 typedef struct {

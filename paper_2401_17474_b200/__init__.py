@@ -9,7 +9,8 @@ from .harness import (MeasureResult, Protocol, ReplayResult, bench, measure_iter
                       timed_replay, trace_run)
 from .reports import REPORT_HEADER, TRACE_HEADER, RunReport, TraceRecord
 from .solvers import (ALPHA_POLICIES, ENGINES, SAMPLING_SCHEMES, VARIANTS, DeviceSystem, SolverConfig,
-                      resolve_alphas, run_solver, solve_ck, solve_concurrent, solve_rk, solve_seeds, solve_rka_seq, solve_rkab_seq)
+                      resolve_alphas, run_solver, solve_ck, solve_concurrent, solve_rk, solve_rka_parallel, solve_rka_seq,
+                      solve_rkab_parallel, solve_rkab_seq, solve_seeds)
 from .sysgen import (GeneratorConfig, LinearSystem, Prng, cgls_solve, crop, generate_mother, make_inconsistent,
                      partition_bounds, worker_rng)
 

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libkz_b200.so")
 
 KZ_OK, KZ_EINVAL, KZ_EDEGENERATE, KZ_EEMPTYRANGE, KZ_ENOMEM, KZ_ECUDA, KZ_ENODEV, KZ_ENOCONV, KZ_ESPECTRAL, \
     KZ_EFORMAT, KZ_EVERSION = range(11)
-KERNELS = {"auto": 0, "chain": 1, "sync_cluster": 2, "sync_grid": 3, "warp": 4}
+KERNELS = {"auto": 0, "chain": 1, "sync_cluster": 2, "sync_grid": 3, "warp": 4, "rka": 5}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 VARIANT_IDS = {"rk": 0, "rka": 1, "rkab": 2, "ck": 3}
 SCHEME_IDS = {"full_access": 0, "distributed": 1, "ranges": 2}

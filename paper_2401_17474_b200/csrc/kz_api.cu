@@ -1435,6 +1435,15 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     // --- kernel plan ---
     Plan pl;
     int kern = p->kernel;
+    const bool threads_combine = (p->flags & KZ_FLAG_THREADS_COMBINE) != 0 && q > 1;
+    if (threads_combine) {
+        if (p->variant != KZ_RKA && p->variant != KZ_RKAB)
+            return fail(KZ_EINVAL, "the threaded engine's combine applies to RKA / RKAB");
+        if (partial_mode || cx.sharded) return fail(KZ_EINVAL, "the threaded engine's combine is single-system only");
+        if (kern != KZ_KERNEL_AUTO && kern != KZ_KERNEL_CHAIN)
+            return fail(KZ_EINVAL, "the threaded engine's combine runs on the chain kernel");
+        kern = KZ_KERNEL_CHAIN;
+    }
     if (kern == KZ_KERNEL_AUTO) {
         if (q == 1 && bs == 1 && s->ld <= 128 && p->partial_dev == nullptr && p->threads == 0) {
             // short rows: one warp beats the chain kernel's block machinery (measured, budget mode:
@@ -1467,6 +1476,9 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         pl.smem = 0;
     } else if (kern == KZ_KERNEL_CHAIN) {
         KZ_TRY(plan_chain(s, p, q, pl));
+    } else if (kern == KZ_KERNEL_RKA) {
+        if (bs != 1 || q < 2) return fail(KZ_EINVAL, "the rka kernel runs RKA / RKAB with q > 1, block_size 1");
+        KZ_TRY(plan_rka(s, p, q, pl));
     } else if (kern == KZ_KERNEL_SYNC_CLUSTER || kern == KZ_KERNEL_SYNC_GRID) {
         if (bs != 1) return fail(KZ_EINVAL, "the sync kernels run RKA / RKAB with block_size 1 only");
         int rc = kern == KZ_KERNEL_SYNC_CLUSTER ? plan_rka(s, p, q, pl) : KZ_EINVAL;
@@ -1481,7 +1493,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     }
     memcpy(s->plan_blob, &pl, sizeof(Plan));
     std::copy(key, key + 6, s->plan_key);
-    r->kernel_used = pl.kernel;
+    r->kernel_used = pl.tma ? KZ_KERNEL_RKA : pl.kernel;
     r->ctas = pl.ctas;
     r->threads = pl.threads;
     r->plan_ep = pl.kernel == KZ_KERNEL_CHAIN || pl.kernel == KZ_KERNEL_WARP ? pl.ep : pl.epl;
@@ -1532,6 +1544,8 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     args.stages = pl.stages;
     args.box = pl.box;
     args.wg = pl.wg ? 1 : 0;
+    args.combine = !threads_combine ? KZ_COMBINE_AVERAGE
+                   : (p->variant == KZ_RKA ? KZ_COMBINE_RKA_DELTA : KZ_COMBINE_RKAB_DELTA);
     if (pl.tma) KZ_TRY(ensure_tmaps(s, pl.box));
     const bool phase_timing = dbg_env("KZ_PHASE_TIMING") != nullptr;
     args.ablate = dbg_env("KZ_ABLATE") ? atoi(dbg_env("KZ_ABLATE")) : 0;
@@ -1594,7 +1608,7 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
         KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
         args.part = s->part.p;
         args.stages = pl.stages;
-        r->kernel_used = pl.kernel;
+        r->kernel_used = pl.tma ? KZ_KERNEL_RKA : pl.kernel;
         r->ctas = pl.ctas;
         KZ_CUDA(cudaMemsetAsync(s->barrier.p, 0, sizeof(unsigned), st));
         lrc = launch_solve(s, pl, args, st);
@@ -2555,7 +2569,7 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     r->rows_projected = k * q * bs;  // this rank's projections
     r->loop_ms = loop_ms;
     r->kernel_ms = loop_ms;  // steps, collectives and averages interleave on one stream
-    r->kernel_used = cx.pl.kernel;
+    r->kernel_used = cx.pl.tma ? KZ_KERNEL_RKA : cx.pl.kernel;
     r->ctas = cx.pl.ctas;
     r->threads = cx.pl.threads;
     if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -35,6 +35,15 @@
 //
 // RKAB with q > 1 averages the worker estimates in worker order behind two
 // grid barriers (cooperative launch) and checks the averaged x directly.
+//
+// The threaded engine's combine (parallel.py:175-304, engine="threads") runs on
+// the same machinery: its workers add increments to the shared x under a lock in
+// arrival order; here the order is the worker order, one valid schedule.
+//   RKA  (KZ_COMBINE_RKA_DELTA, bs = 1): s_t = alpha (b - <a, x>) / (q sq) with the
+//        reference's division; the worker publishes fl(s_t a_t) and
+//        x_j <- fl(x_j + inc_tj), t ascending            (parallel.py:214-226)
+//   RKAB (KZ_COMBINE_RKAB_DELTA): the worker publishes v_t; inc_tj = fl(fl(v_tj - x_j) / q)
+//        against the pre-combine x, x_j <- fl(x_j + inc_tj)  (parallel.py:286-298)
 #include "kz_kernels.cuh"
 
 namespace kz {
@@ -299,6 +308,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     int conv = 0, checks = 0;
     double err_last = 0.0;
     const double qd = (double)q;
+    const bool rka_delta = q > 1 && a.combine == KZ_COMBINE_RKA_DELTA;
     const bool use_stop = a.use_stop != 0;
     const bool ckpt_on = a.ckpt_every > 0;
     int nblk = 0;                 // blocks processed (phase timing)
@@ -429,7 +439,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 }
                 if (r < Reff) {
                     if (CHECK && d + r == next_check) next_check += bs;
-                    s[r] = __dmul_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), invr);
+                    s[r] = rka_delta ? __ddiv_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), __dmul_rn(qd, sqr))
+                                     : __dmul_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), invr);
                     if (CHECK) e = fma(s[r] * s[r], sqr, fma(2.0 * s[r], dr - vals[Blk<R>::NVN + r], e));
                 }
             }
@@ -442,7 +453,10 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
 #pragma unroll
                 for (int p = 0; p < EP; ++p) {
                     const int64_t lc = 2 * ((int64_t)p * T + tid);
-                    if (lc < ldc) {
+                    if (lc < ldc && rka_delta) {  // the increment itself; v is reloaded from x
+                        v[2 * p] = __dmul_rn(s[r], rr[r][p].x);
+                        v[2 * p + 1] = __dmul_rn(s[r], rr[r][p].y);
+                    } else if (lc < ldc) {
                         v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], rr[r][p].x));
                         v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], rr[r][p].y));
                     }
@@ -532,7 +546,19 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             const int64_t G = gridDim.x;
             const int64_t cw = ((ld + G - 1) / G + 1) & ~(int64_t)1;
             const int64_t c0 = blockIdx.x * cw, c1 = (c0 + cw < ld) ? c0 + cw : ld;
-            for (int64_t col = c0 + tid; col < c1; col += T) {
+            if (a.combine != KZ_COMBINE_AVERAGE) {  // threaded engine: increments in worker order
+                for (int64_t col = c0 + tid; col < c1; col += T) {
+                    const double xp = __ldcg(a.x + col);
+                    double acc = xp;
+                    for (int64_t t = 0; t < q; ++t) {
+                        const double vt = __ldcg(a.V + t * ld + col);
+                        acc = __dadd_rn(acc, rka_delta ? vt : __ddiv_rn(__dsub_rn(vt, xp), qd));
+                    }
+                    __stcg(a.x + col, acc);
+                    if (ck && col < a.n) a.ckpt[slot * a.n + col] = acc;
+                }
+            }
+            for (int64_t col = c0 + tid; a.combine == KZ_COMBINE_AVERAGE && col < c1; col += T) {
                 double acc = __ldcg(a.V + col);
                 for (int64_t t = 1; t < q; ++t) acc = __dadd_rn(acc, __ldcg(a.V + t * ld + col));
                 if (a.partial) {  // row-sharded step: the un-normalised local sum, x untouched

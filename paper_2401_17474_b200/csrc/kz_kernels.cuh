@@ -55,6 +55,15 @@ struct SolveArgs {
     unsigned long long* const* xr_peers;  // device array: each rank's exchange buffer (own rank's is local)
     int xr_ranks, xr_rank;
     unsigned xr_tag0;      // tag of iteration k0 (unique across launches and solves of the communicator)
+    // chain kernel, q > 1: how the worker estimates meet (KZ_COMBINE_*): the sequential engine's
+    // ordered average, or the threaded engine's increments added to x in worker order
+    int combine;
+};
+
+enum {
+    KZ_COMBINE_AVERAGE = 0,    // x = (sum_t v_t) / q                         (solvers.py:131-137, 366-367)
+    KZ_COMBINE_RKA_DELTA = 1,  // x += alpha (b_t - <a_t, x>) / (q sq_t) a_t   (parallel.py:214-226)
+    KZ_COMBINE_RKAB_DELTA = 2  // x += (v_t - x) / q                           (parallel.py:286-298)
 };
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,

@@ -29,7 +29,8 @@ VARIANTS = ("ck", "rk", "rka", "rkab", "cgls")
 ALPHA_POLICIES = ("unit", "fixed", "optimal_full", "optimal_partial")
 SAMPLING_SCHEMES = ("full_access", "distributed")
 # "seq" and "threads" name the reference engines whose semantics are honoured
-# (threads: RKAB gets the leading row, solvers.py:346-350); all run on the B200.
+# (threads: the delta-form combine in worker order and RKAB's leading row,
+# parallel.py:175-304; solve_rka_parallel / solve_rkab_parallel); all run on the B200.
 ENGINES = ("b200", "seq", "threads")
 KERNELS = tuple(N.KERNELS)
 
@@ -489,7 +490,7 @@ def _uniform_alpha(alphas: np.ndarray) -> float:
 
 
 def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, trace_step=None, capture=None,
-           lead_row: bool = False, checkpoint_every: int | None = None) -> RunReport:
+           lead_row: bool = False, checkpoint_every: int | None = None, threads_combine: bool = False) -> RunReport:
     cfg.validate()
     q = 1 if variant in ("rk", "ck") else cfg.q
     steps = cfg.block_size + (1 if lead_row else 0) if variant == "rkab" else 1
@@ -536,7 +537,7 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
         p.kernel = N.KERNELS[cfg.kernel]
         p.threads = int(cfg.threads)
         p.ctas = int(cfg.ctas)
-        p.flags = 2 if cfg.short_launches else 0  # KZ_FLAG_SHORT_LAUNCHES
+        p.flags = (2 if cfg.short_launches else 0) | (8 if threads_combine else 0)  # KZ_FLAG_SHORT_LAUNCHES, _THREADS_COMBINE
         p.want_residual = 1
         r = N.Result()
         x = np.empty(ds.n)
@@ -619,6 +620,25 @@ def solve_rkab_seq(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_
     """Block-averaged RK: q private chains of block_size rows (solvers.py:337-371)."""
     return _solve(system, cfg, "rkab", x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture,
                   lead_row=lead_row, checkpoint_every=checkpoint_every)
+
+
+def solve_rka_parallel(system, cfg: SolverConfig, *, x_ref=None, budget=None, capture=None,
+                       checkpoint_every=None) -> RunReport:
+    """The threaded engine's RKA (parallel.py:175-235): every worker projects against the
+    iteration's snapshot and adds alpha (b_i - <a_i, x_prev>) / (q sq_i) a_i to the shared x;
+    the increments are added in worker order (one of the reference's arrival orders)."""
+    r = _solve(system, cfg, "rka", x_ref=x_ref, budget=budget, capture=capture, checkpoint_every=checkpoint_every,
+               threads_combine=True)
+    return dataclasses.replace(r, barrier_events=2 * (r.iterations + 1)) if budget is None else r
+
+
+def solve_rkab_parallel(system, cfg: SolverConfig, *, x_ref=None, budget=None, capture=None,
+                        checkpoint_every=None) -> RunReport:
+    """The threaded engine's RKAB (parallel.py:238-304): block_size + 1 rows per worker (a lead
+    row from the shared x, then the chain) and x += (v - x) / q in worker order."""
+    r = _solve(system, cfg, "rkab", x_ref=x_ref, budget=budget, capture=capture, lead_row=True,
+               checkpoint_every=checkpoint_every, threads_combine=True)
+    return dataclasses.replace(r, barrier_events=2 * (r.iterations + 1)) if budget is None else r
 
 
 def _run_cgls(system, cfg, x_ref):
@@ -765,6 +785,9 @@ def run_solver(system, cfg: SolverConfig, *, x_ref=None, budget=None, trace_step
     kw = dict(x_ref=x_ref, budget=budget, trace_step=trace_step, capture=capture, checkpoint_every=checkpoint_every)
     if cfg.variant == "rk":
         return solve_rk(system, cfg, **kw)
+    if cfg.engine == "threads":
+        del kw["trace_step"]
+        return (solve_rka_parallel if cfg.variant == "rka" else solve_rkab_parallel)(system, cfg, **kw)
     if cfg.variant == "rka":
         return solve_rka_seq(system, cfg, **kw)
-    return solve_rkab_seq(system, cfg, lead_row=(cfg.engine == "threads"), **kw)
+    return solve_rkab_seq(system, cfg, **kw)

@@ -25,6 +25,7 @@ fixtures pin:
                   seeded systems, incl. a row block too short for its estimate
 * threads.npz  -- the threaded engine's runs (parallel.py:175-304): delta-form RKA under a
                   lock and lead-row RKAB, final x, iterations and x checkpoints
+* c1_ckpt100.npz -- c1 RKA q=64 seeds 0-2, the iterate every 100 iterations
 * dist.npz     -- run_distributed_solve (distributed.py:339-363): the simulated-MPI
                   engine's RKA / RKAB (Algorithm 4: block_size + 1 rows, x / np
                   before the all-reduce) per-rank iterates
@@ -45,7 +46,7 @@ if REF not in sys.path:
 import kaczbench as kb  # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from common import NORM_WIDTHS, norm_matrix, sha  # noqa: E402
+from common import NORM_WIDTHS, THREAD_CASES, norm_matrix, sha  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 META = {"numpy_version": np.__version__, "generator": "tests/golden/make_golden.py"}
@@ -265,16 +266,6 @@ def gen_spectral():
     save("spectral.npz", **out)
 
 
-THREAD_CASES = [  # (name, system, variant, q, block_size, base_seed)
-    ("s500_rka_q2", (500, 20, 1), "rka", 2, 1, 1),
-    ("s500_rka_q4", (500, 20, 1), "rka", 4, 1, 1),
-    ("s2000_rka_q8", (2000, 50, 7), "rka", 8, 1, 3),
-    ("c0_rka_q16", (2000, 50, 0), "rka", 16, 1, 0),
-    ("s500_rkab_q4_bs10", (500, 20, 1), "rkab", 4, 10, 2),
-    ("s2000_rkab_q8_bs25", (2000, 50, 7), "rkab", 8, 25, 5),
-]
-
-
 def gen_threads():
     """parallel.py:175-304 executed: solve_rka_parallel (x += alpha (b - <a, x_prev>) / (q sq) a
     under a lock, arrival order) and solve_rkab_parallel (lead row + block, x += (v - x) / q);
@@ -295,6 +286,20 @@ def gen_threads():
     save("threads.npz", **out)
 
 
+def gen_c1_ckpt100():
+    """c1 (RKA q=64, 20000 x 500) seeds 0-2: the reference's iterate every 100 iterations
+    (SURVEY 8(c) T3 cadence; solves.npz keeps every 1000th)."""
+    c1 = system(20000, 500, 0)
+    out = {}
+    for seed in range(3):
+        cap = []
+        r = kb.run_solver(c1, kb.SolverConfig(variant="rka", q=64, base_seed=seed), capture=cap)
+        out[f"s{seed}_iterations"] = np.array(r.iterations)
+        out[f"s{seed}_ckpt"] = np.array(cap[99::100])
+        print("c1 ckpt100", seed, r.iterations, flush=True)
+    save("c1_ckpt100.npz", **out)
+
+
 def gen_kzsys():
     """A KZSYS v1 file written by the reference's own save_system (sysgen.py:190-214)."""
     kb.save_system(system(500, 20, 1), os.path.join(OUT, "kzsys_s500.bin"))
@@ -312,6 +317,8 @@ if __name__ == "__main__":
         gen_spectral()
     elif len(sys.argv) > 1 and sys.argv[1] == "threads":
         gen_threads()
+    elif len(sys.argv) > 1 and sys.argv[1] == "c1ckpt":
+        gen_c1_ckpt100()
     else:
         main()
         gen_ck()
@@ -319,3 +326,4 @@ if __name__ == "__main__":
         gen_dist()
         gen_spectral()
         gen_threads()
+        gen_c1_ckpt100()

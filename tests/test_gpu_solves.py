@@ -61,6 +61,13 @@ def test_c1_rka_q64(gpu, c1_system, kernel):
             assert r2.iterations == r.iterations and np.array_equal(r2.x, r.x)  # deterministic
             for j, b in enumerate(ck):
                 assert rel_err(cap[1000 * (j + 1) - 1], b) <= PARITY_TOL, (kernel, seed, j)
+            # the reference's iterate every 100 iterations (golden/c1_ckpt100.npz)
+            g100 = golden("c1_ckpt100.npz")
+            assert r.iterations == int(g100[f"s{seed}_iterations"])
+            ck100 = g100[f"s{seed}_ckpt"]
+            assert len(ck100) == r.iterations // 100
+            for j, b in enumerate(ck100):
+                assert rel_err(cap[100 * (j + 1) - 1], b) <= PARITY_TOL, (kernel, seed, 100 * (j + 1))
 
 
 def test_c2_rkab_q64_bs500(gpu, c2_system):
@@ -207,7 +214,7 @@ def test_oracle_agreement_random_configs(gpu, oracle, systems):
 @pytest.mark.parametrize("ctas", [32, 80, 112])
 def test_multi_cluster_matches_reference(gpu, c1_system, ctas):
     """Several 16-CTA clusters exchanging cluster totals through tagged words
-    (kz_sync.cu): same iterates and stop decisions as the reference's c1 solve."""
+    (rka_kernel, kz_rka.cu): same iterates and stop decisions as the reference's c1 solve."""
     from paper_2401_17474_b200 import DeviceSystem, solve_rka_seq
 
     g = golden("solves.npz")
@@ -215,7 +222,7 @@ def test_multi_cluster_matches_reference(gpu, c1_system, ctas):
     with DeviceSystem(c1_system) as ds:
         r = solve_rka_seq(ds, _cfg(variant="rka", q=64, base_seed=0, kernel="sync_cluster", ctas=ctas),
                           checkpoint_every=1000)
-        assert r.gpu["kernel"] == "sync_cluster" and r.gpu["ctas"] == ctas
+        assert r.gpu["kernel"] == "rka" and r.gpu["ctas"] == ctas
         _check(r, g, tag)
         cap = []
         solve_rka_seq(ds, _cfg(variant="rka", q=64, base_seed=0, kernel="sync_cluster", ctas=ctas), capture=cap)

@@ -152,3 +152,26 @@ def test_distributed_engine_is_distributed_scheme(oracle, systems, tag):
     assert rel_err(o["x"], g[f"{tag}_x"]) <= PARITY_TOL
     for j, ck in enumerate(g[f"{tag}_ckpt"]):
         assert rel_err(o["checkpoints"][j], ck) <= PARITY_TOL, j
+
+
+def test_oracle_threaded_engine_matches_reference(oracle):
+    """The oracle's threaded-engine combine (parallel.py:214-226, 286-298 in worker order)
+    against the reference's threaded runs: iterations equal, x and every 10th iterate within
+    the reference's own threads-vs-seq tolerance; serial and pthreads oracles bitwise equal."""
+    from golden.common import THREAD_CASES, THREADS_TOL
+
+    from paper_2401_17474_b200 import GeneratorConfig, generate_mother
+
+    g = golden("threads.npz")
+    for name, (m, n, seed), variant, q, bs, base in THREAD_CASES:
+        s = generate_mother(GeneratorConfig(m_max=m, n_max=n, seed=seed))
+        o = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=q, block_size=bs, base_seed=base, engine="threads",
+                         ckpt_every=10)
+        assert o["iterations"] == int(g[f"{name}_it"]) and o["converged"]
+        assert rel_err(o["x"], g[f"{name}_x"]) <= THREADS_TOL, name
+        assert len(o["checkpoints"]) == len(g[f"{name}_ckpt"])
+        for a, b in zip(o["checkpoints"], g[f"{name}_ckpt"]):
+            assert rel_err(a, b) <= THREADS_TOL, name
+        o4 = oracle.solve(s.A, s.b, s.x_star, variant=variant, q=q, block_size=bs, base_seed=base, engine="threads",
+                          nthreads=4)
+        assert np.array_equal(o4["x"], o["x"])
