@@ -211,6 +211,39 @@ def x_digest(x) -> str:
     return hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()[:16]
 
 
+# top-level keys of the b200 arm's line at any N (the dry run emits the same set)
+HEADLINE_KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                 "scaling", "vs_baseline", "dtype", "data", "config", "time_to_eps_ms", "iterations", "seeds",
+                 "roofline", "clocks", "e2e", "gpu_launches", "setup_s")
+
+
+def run_dry(args, rank, world):
+    """The launcher path without GPU work (--dry-run; CPU, gloo): every rank plans its c3 shard,
+    the plans are all-gathered and must tile [0, m) in rank order, rank 0 prints a line with
+    the b200 arm's keys (values null)."""
+    import torch.distributed as dist
+
+    from paper_2401_17474_b200.multigpu import plan_shards
+
+    plan = plan_shards(C3_M, world, rank, C3_Q)
+    mine = (rank, plan.lo, plan.hi, len(plan.worker_lo))
+    every = [mine] * world
+    if world > 1:
+        dist.all_gather_object(every, mine)
+    assert [e[0] for e in every] == list(range(world))
+    assert every[0][1] == 0 and every[-1][2] == C3_M - 1
+    assert all(every[g][2] + 1 == every[g + 1][1] for g in range(world - 1))
+    assert all(e[3] == C3_Q for e in every)
+    if rank != 0:
+        return
+    line = {k: None for k in HEADLINE_KEYS}
+    line.update(metric=METRIC, unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup,
+                higher_is_better=True, scaling="weak", dtype="f64", config=c3_config(world),
+                dry_run={"shards": [list(e[1:3]) for e in every], "launcher": "torch.distributed.run"
+                         if os.environ.get("TORCHELASTIC_RUN_ID") else "direct"})
+    emit(line)
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -307,7 +340,7 @@ def run_b200(args, rank, world, local_rank):
     if world == 1 and not args.no_extra:
         extras = extra_workloads(local_rank, read_peak()[0])
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # cpu_baseline: rank 0 at N = 1 only
         import oracle as O
 
         cores = O.max_threads()
@@ -366,6 +399,7 @@ def run_b200(args, rank, world, local_rank):
         line["extra_workloads"] = extras
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    assert set(HEADLINE_KEYS) <= set(line), set(HEADLINE_KEYS) - set(line)
     emit(line)
 
 
@@ -542,6 +576,8 @@ def parse_args(argv=None):
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE workloads")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher path only (CPU, gloo): shard plans, rank agreement, the line's keys")
     return ap.parse_args(argv)
 
 
@@ -570,10 +606,17 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if args.dry_run:
+            dist.init_process_group("gloo")
+        else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the init log names every communicator's nranks
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
-        run_b200(args, rank, world, local_rank)
+        if args.dry_run:
+            run_dry(args, rank, world)
+        else:
+            run_b200(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
