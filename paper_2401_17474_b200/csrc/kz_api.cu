@@ -22,10 +22,20 @@
 #include <fcntl.h>
 #include <unistd.h>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool attaches
 #include <nccl.h>  // types only: the library is dlopen'ed (the process's already-loaded libnccl.so.2 if any)
 
 #include "../../include/kz_b200.h"
 #include "kz_kernels.cuh"
+
+// NVTX ranges around every entry point and every chunk launch (nsys / ncu --nvtx show the
+// solve's setup, chunks and host round trips on the timeline)
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+    NvtxScope(const NvtxScope&) = delete;
+    NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 using namespace kz;
 
@@ -353,12 +363,14 @@ static int upload_common(kz_system* s, const double* A, int64_t lda, const doubl
 
 extern "C" int32_t kz_system_upload(kz_system* s, const double* A, int64_t lda, const double* b, const double* xref,
                                     void* stream) {
+    NvtxScope nvtx_("kz_system_upload");
     if (!s || !A || !b) return fail(KZ_EINVAL, "null argument");
     return upload_common(s, A, lda, b, xref, (cudaStream_t)stream, cudaMemcpyHostToDevice);
 }
 
 extern "C" int32_t kz_system_upload_device(kz_system* s, const double* A, int64_t lda, const double* b,
                                            const double* xref, void* stream) {
+    NvtxScope nvtx_("kz_system_upload_device");
     if (!s || !A || !b) return fail(KZ_EINVAL, "null argument");
     return upload_common(s, A, lda, b, xref, (cudaStream_t)stream, cudaMemcpyDeviceToDevice);
 }
@@ -385,11 +397,13 @@ extern "C" int32_t kz_system_set_xref(kz_system* s, const double* xref, void* st
 
 extern "C" int32_t kz_generate_counter(kz_system* s, uint64_t seed, double mu_lo, double mu_hi, double sg_lo,
                                        double sg_hi, void* stream) {
+    NvtxScope nvtx_("kz_generate_counter");
     return kz_generate_counter_rows(s, seed, 0, mu_lo, mu_hi, sg_lo, sg_hi, stream);
 }
 
 extern "C" int32_t kz_generate_counter_rows(kz_system* s, uint64_t seed, int64_t row0, double mu_lo, double mu_hi,
                                             double sg_lo, double sg_hi, void* stream) {
+    NvtxScope nvtx_("kz_generate_counter_rows");
     if (row0 < 0) return fail(KZ_EINVAL, "row0 must be >= 0");
     if (!s) return fail(KZ_EINVAL, "null system");
     KZ_NOT_VIEW(s);
@@ -415,6 +429,7 @@ extern "C" int32_t kz_generate_counter_rows(kz_system* s, uint64_t seed, int64_t
 
 extern "C" int32_t kz_system_download(kz_system* s, int64_t m2, int64_t n2, double* A_host, double* b_host,
                                       double* xref_host, void* stream) {
+    NvtxScope nvtx_("kz_system_download");
     if (!s || m2 < 0 || n2 < 0 || m2 > s->m || n2 > s->n) return fail(KZ_EINVAL, "bad crop");
     cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
@@ -485,6 +500,7 @@ extern "C" int32_t kz_row_norms_upload(kz_system* s, const double* sq_host, void
 }
 
 extern "C" int32_t kz_row_norms(kz_system* s, double* sq_host, int64_t* bad_row, void* stream) {
+    NvtxScope nvtx_("kz_row_norms");
     if (!s) return fail(KZ_EINVAL, "null system");
     cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
@@ -650,6 +666,7 @@ extern "C" int32_t kz_sampler_set_ranges(kz_system* s, int64_t q, const int64_t*
 }
 
 extern "C" int32_t kz_sampler_build(kz_system* s, int32_t scheme, int64_t q, double* cdf_host, void* stream) {
+    NvtxScope nvtx_("kz_sampler_build");
     if (!s) return fail(KZ_EINVAL, "null system");
     cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
@@ -673,6 +690,7 @@ static int launch_sampler(kz_system* s, const PcgPod* states_dev, const int64_t*
 
 extern "C" int32_t kz_dump_rows(kz_system* s, int32_t scheme, int64_t q, uint64_t seed, int64_t worker, int64_t start,
                                 int64_t count, int32_t* out_host, void* stream) {
+    NvtxScope nvtx_("kz_dump_rows");
     if (!s || !out_host) return fail(KZ_EINVAL, "null argument");
     if (worker < 0 || worker >= q) return fail(KZ_EINVAL, "worker %lld out of range for q=%lld", (long long)worker, (long long)q);
     if (start < 0 || count < 0) return fail(KZ_EINVAL, "negative range");
@@ -723,6 +741,7 @@ static int device_norms(kz_system* s, const double* xdev, double* residual, doub
 }
 
 extern "C" int32_t kz_norms(kz_system* s, const double* x_host, double* residual, double* error, void* stream) {
+    NvtxScope nvtx_("kz_norms");
     if (!s || !x_host) return fail(KZ_EINVAL, "null argument");
     cudaStream_t st = pick_stream(s, stream);
     KZ_CUDA(cudaSetDevice(s->device));
@@ -1617,6 +1636,7 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
 }
 
 extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, double* x_host, void* stream) {
+    NvtxScope nvtx_("kz_solve");
     if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
     memset(r, 0, sizeof(*r));
     r->final_error_sq = NAN;
@@ -1717,6 +1737,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
         args.idx_stride = c * bs;
         args.final_check = (stop_mode && k + c == p->max_iterations) ? 1 : 0;
         KZ_CUDA(cudaEventRecord(s->ev[2], st));
+        NvtxScope nvtx_chunk("kz_solve chunk");
         KZ_TRY(launch_step(s, p, r, cx, k == 0, st));
         if (partial_mode) {
             // row-sharded local step: exactly one iteration, left in flight on the stream (the
@@ -1853,6 +1874,7 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
 // ---------------------------------------------------------------------------
 extern "C" int32_t kz_cgls(kz_system* s, const double* b_host, double tol, int64_t max_it, double* x_out,
                            int64_t* iterations, void* stream) {
+    NvtxScope nvtx_("kz_cgls");
     if (!s || !x_out) return fail(KZ_EINVAL, "null argument");
     if (!(tol > 0)) return fail(KZ_EINVAL, "tol must be > 0, got %g", tol);
     cudaStream_t st = pick_stream(s, stream);
@@ -1963,6 +1985,7 @@ extern "C" int32_t kz_cgls(kz_system* s, const double* b_host, double tol, int64
 // ---------------------------------------------------------------------------
 extern "C" int32_t kz_spectral(kz_system* s, int64_t row_lo, int64_t row_hi, const double* v0_host,
                                const double* v1_host, double tol, int64_t max_it, double* out, void* stream) {
+    NvtxScope nvtx_("kz_spectral");
     if (!s || !v0_host || !v1_host || !out) return fail(KZ_EINVAL, "null argument");
     if (row_lo < 0 || row_hi >= s->m || row_hi < row_lo) return fail(KZ_EINVAL, "bad row range");
     cudaStream_t st = pick_stream(s, stream);
@@ -2103,6 +2126,7 @@ extern "C" int32_t kz_spectral(kz_system* s, int64_t row_lo, int64_t row_hi, con
 extern "C" int32_t kz_system_load_file(int32_t device, const char* path, int64_t row_lo, int64_t row_hi,
                                        kz_system** out, int64_t* m_total, int64_t* n_out, uint32_t* flags_out,
                                        double* meta5) {
+    NvtxScope nvtx_("kz_system_load_file");
     if (!path || !out) return fail(KZ_EINVAL, "null argument");
     *out = nullptr;
     const int fd = open(path, O_RDONLY);
@@ -2304,6 +2328,7 @@ extern "C" int32_t kz_comm_unique_id(uint8_t* id_out) {
 }
 
 extern "C" int32_t kz_comm_create(int32_t device, const uint8_t* id, int32_t world, int32_t rank, kz_comm** out) {
+    NvtxScope nvtx_("kz_comm_create");
     if (!id || !out) return fail(KZ_EINVAL, "null argument");
     if (world < 1 || rank < 0 || rank >= world) return fail(KZ_EINVAL, "rank %d out of range for world %d", rank, world);
     *out = nullptr;
@@ -2344,6 +2369,7 @@ extern "C" int32_t kz_comm_exchange_handle(kz_comm* c, int64_t ld, uint8_t* hand
 }
 
 extern "C" int32_t kz_comm_exchange_connect(kz_comm* c, const uint8_t* handles) {
+    NvtxScope nvtx_("kz_comm_exchange_connect");
     if (!c || !handles) return fail(KZ_EINVAL, "null argument");
     if (!c->xbuf) return fail(KZ_EINVAL, "kz_comm_exchange_handle first");
     KZ_CUDA(cudaSetDevice(c->device));
@@ -2382,6 +2408,7 @@ extern "C" int32_t kz_comm_destroy(kz_comm* c) {
 
 extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params* p, kz_result* r, double* x_host,
                                     void* stream) {
+    NvtxScope nvtx_("kz_solve_sharded");
     if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
     memset(r, 0, sizeof(*r));
     r->final_error_sq = NAN;
@@ -2586,6 +2613,7 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
 // ---------------------------------------------------------------------------
 extern "C" int32_t kz_solve_seeds(kz_system* s, const kz_params* p, const uint64_t* seeds, int64_t S,
                                   kz_result* results, double* x_host, void* stream) {
+    NvtxScope nvtx_("kz_solve_seeds");
     if (!s || !p || !seeds || !results) return fail(KZ_EINVAL, "null argument");
     if (S < 1) return fail(KZ_EINVAL, "need at least one seed");
     if (p->variant != KZ_RK) return fail(KZ_EINVAL, "kz_solve_seeds runs RK (variant %d)", p->variant);
