@@ -825,6 +825,7 @@ struct Plan {
     bool sr = false;    // rka kernel: single round of 8 rows per warp (<= 64 workers per cluster)
     bool wg = false;    // rka kernel: worker groups (cluster g runs q/G workers over all columns)
     bool xr = false;    // rka kernel: cross-rank column sums (set per launch by kz_solve_sharded, not planned)
+    bool delta = false; // chain: the threaded engine's RKA increments (chain_kernel<..., DELTA = true>)
     size_t smem = 0;
 };
 
@@ -852,14 +853,27 @@ void* rkw_fn(int epl) {
     return epl == 1 ? (void*)rkw_kernel<1, 8> : epl == 2 ? (void*)rkw_kernel<2, 8> : (void*)rkw_kernel<4, 8>;
 }
 
-void* chain_fn(int ep, int R, int C) {
+void* chain_fn(int ep, int R, int C, bool delta = false) {
+    if (delta) {  // the threaded engine's RKA (one CTA per worker)
+        switch (C * 10000 + ep * 100 + R) {
+            case 10101: return (void*)chain_kernel<1, 1, 1, true>;
+            case 10104: return (void*)chain_kernel<1, 4, 1, true>;
+            case 10201: return (void*)chain_kernel<2, 1, 1, true>;
+            case 10204: return (void*)chain_kernel<2, 4, 1, true>;
+            case 10401: return (void*)chain_kernel<4, 1, 1, true>;
+            case 10402: return (void*)chain_kernel<4, 2, 1, true>;
+            case 10404: return (void*)chain_kernel<4, 4, 1, true>;
+            case 10801: return (void*)chain_kernel<8, 1, 1, true>;
+            case 10802: return (void*)chain_kernel<8, 2, 1, true>;
+            case 11601: return (void*)chain_kernel<16, 1, 1, true>;
+            default: return nullptr;
+        }
+    }
     switch (C * 10000 + ep * 100 + R) {
         case 10101: return (void*)chain_kernel<1, 1, 1>;
         case 10104: return (void*)chain_kernel<1, 4, 1>;
-        case 10108: return (void*)chain_kernel<1, 8, 1>;
         case 10201: return (void*)chain_kernel<2, 1, 1>;
         case 10204: return (void*)chain_kernel<2, 4, 1>;
-        case 10208: return (void*)chain_kernel<2, 8, 1>;
         case 10401: return (void*)chain_kernel<4, 1, 1>;
         case 10402: return (void*)chain_kernel<4, 2, 1>;
         case 10404: return (void*)chain_kernel<4, 4, 1>;
@@ -919,7 +933,7 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     if (ep == 0 || T > chain_max_threads(ep) || (int64_t)ep * T < pairs)
         return fail(KZ_EINVAL, "n=%lld too large for the chain kernel", (long long)s->n);
     // rows per reduction: as many as registers allow (EP small) and the ring holds (> R rows)
-    int R = ep <= 4 ? 4 : (ep == 8 ? 2 : 1);  // R = 8 measured slower since the reduction got cheap
+    int R = ep <= 4 ? 4 : (ep == 8 ? 2 : 1);  // R = 8 measured slower since the reduction got cheap (not built)
     if (C == 2) R = std::min(R, 4);
     if (C > 2) R = std::min(R, 4);
     if (const char* e = dbg_env("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
@@ -927,7 +941,7 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     const int64_t stage_bytes = ldc * (int64_t)sizeof(double);
     int stages = 0;
     for (;;) {
-        while (R > 1 && !chain_fn(ep, R, C)) R /= 2;
+        while (R > 1 && !chain_fn(ep, R, C, pl.delta)) R /= 2;
         const int64_t fixed = chain_smem(ldc, 0, R, T, C);
         stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
         if (const char* e = dbg_env("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
@@ -936,7 +950,10 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     }
     if (stages < 1 || (size_t)chain_smem(ldc, stages, R, T, C) > kSmemLimit)
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
-    void* fn = chain_fn(ep, R, C);
+    void* fn = chain_fn(ep, R, C, pl.delta);
+    // the instantiations carry one driver each for these shapes (kz_chain.cu ONE_CHAIN / AVERAGED)
+    if ((q == 1 && C == 2 && ep >= 8) || (q > 1 && C > 2))
+        return fail(KZ_EINVAL, "no chain kernel drives q=%lld on %d-CTA workers with EP=%d", (long long)q, C, ep);
     if (!fn) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d C=%d", ep, R, C);
     pl.kernel = KZ_KERNEL_CHAIN;
     pl.threads = T + 32;  // + the producer warp
@@ -964,6 +981,7 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
 // 16 pairs x 320 threads x 2 columns per CTA, i.e. n <= 10240 C (C = 1, 2, or 4 for q = 1).
 static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     int C = (s->ld >= 1024 && 2 * q <= s->sms && !s->no_pairs) ? 2 : 1;  // measured: pairs win from n ~ 1000
+    if (pl.delta) C = 1;  // the threaded engine's RKA runs on one CTA per worker (its own instantiations)
     // one chain (RK, CK) over long rows: a cluster of 4 (measured on 80000 x 2000 with the
     // producer warp: 0.40 us per row against 0.42 for 8 CTAs and 0.45 for a pair; at n = 512
     // the pair is best)
@@ -1336,7 +1354,7 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
     void* fn;
     cudaLaunchAttribute attr2[2];
     if (pl.kernel == KZ_KERNEL_CHAIN) {
-        fn = chain_fn(pl.ep, pl.rows, pl.pair);
+        fn = chain_fn(pl.ep, pl.rows, pl.pair, pl.delta);
         int na = 0;
         // KZ_NO_COOP (experiments): drop the cooperative attribute so a profiler can replay the
         // launch; safe only when every CTA fits at once (one per SM, ctas <= SMs)
@@ -1410,6 +1428,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     if (p->variant < KZ_RK || p->variant > KZ_CK) return fail(KZ_EINVAL, "unknown variant %d", p->variant);
     if (p->q < 1) return fail(KZ_EINVAL, "q must be >= 1, got %lld", (long long)p->q);
     if (p->block_size < 1) return fail(KZ_EINVAL, "block_size must be >= 1, got %lld", (long long)p->block_size);
+    if (p->block_size > (1 << 28)) return fail(KZ_EINVAL, "block_size %lld exceeds 2^28", (long long)p->block_size);
     if (!(p->epsilon > 0)) return fail(KZ_EINVAL, "epsilon must be > 0, got %g", p->epsilon);
     if (p->max_iterations < 1) return fail(KZ_EINVAL, "max_iterations must be >= 1, got %lld", (long long)p->max_iterations);
     if (p->budget < 0) return fail(KZ_EINVAL, "fixed iteration budget must be >= 1, got %lld", (long long)p->budget);
@@ -1474,14 +1493,15 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
             kern = KZ_KERNEL_SYNC_CLUSTER;  // one or several clusters; grid barrier as the fallback
         }
     }
-    const int64_t key[6] = {kern, q, bs, p->ctas, p->threads, p->kernel};
+    pl.delta = threads_combine && p->variant == KZ_RKA;
+    const int64_t key[6] = {kern + (pl.delta ? 100 : 0), q, bs, p->ctas, p->threads, p->kernel};
     static_assert(sizeof(Plan) <= sizeof(s->plan_blob), "plan cache");
     if (std::equal(key, key + 6, s->plan_key)) {
         memcpy(&pl, s->plan_blob, sizeof(Plan));  // same shape as the previous call: reuse its plan
         // the dynamic shared-memory limit is a property of the kernel function, which another
         // system may have lowered since: restore it for this plan
         void* fn = pl.kernel == KZ_KERNEL_WARP    ? rkw_fn(pl.ep)
-                   : pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair)
+                   : pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair, pl.delta)
                    : pl.tma                     ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg ? 1 : (pl.xr ? 2 : 0))
                                                 : sync_fn(pl.kernel == KZ_KERNEL_SYNC_CLUSTER, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));

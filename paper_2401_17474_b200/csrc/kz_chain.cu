@@ -39,8 +39,8 @@
 // The threaded engine's combine (parallel.py:175-304, engine="threads") runs on
 // the same machinery: its workers add increments to the shared x under a lock in
 // arrival order; here the order is the worker order, one valid schedule.
-//   RKA  (KZ_COMBINE_RKA_DELTA, bs = 1): s_t = alpha (b - <a, x>) / (q sq) with the
-//        reference's division; the worker publishes fl(s_t a_t) and
+//   RKA  (KZ_COMBINE_RKA_DELTA, bs = 1): s_t = alpha (b - <a, x>) / (q sq) (by the
+//        reciprocal of fl(q sq), like every scale here); the worker publishes fl(s_t a_t) and
 //        x_j <- fl(x_j + inc_tj), t ascending            (parallel.py:214-226)
 //   RKAB (KZ_COMBINE_RKAB_DELTA): the worker publishes v_t; inc_tj = fl(fl(v_tj - x_j) / q)
 //        against the pre-combine x, x_j <- fl(x_j + inc_tj)  (parallel.py:286-298)
@@ -68,13 +68,31 @@ struct ChainSmem {
 };
 
 // CTA-wide sums of NV per-thread values; every thread receives every total,
-// bit-identical.  (1) Inside each warp a transposed shuffle reduction: the NV
-// values (padded to NP = 32 or 64) are halved across lanes at xor offsets
-// 16, 8, 4, 2, 1 -- a lane keeps one half and adds its partner's copy -- so
-// after NP - NP/32 shuffles lane l holds the warp sums of values
-// l * (NP/32) .. +NP/32 (no shared-memory traffic, 5 dependent levels).
-// (2) Those land in scr[warp][NP]; one barrier; thread v < NV adds the nw warp
-// sums in a fixed tree into tot[v]; one barrier; everyone reads tot.
+// bit-identical.  (1) Inside each warp a transposed shuffle reduction per 32
+// values: they are halved across lanes at xor offsets 16, 8, 4, 2, 1 -- a lane
+// keeps one half and adds its partner's copy -- so after 31 shuffles lane l
+// holds the warp sum of value l (no shared-memory traffic, 5 dependent levels);
+// more than 32 values take a second pass.  (2) Those land in scr[warp][NP]; one
+// barrier; thread v < NV adds the nw warp sums in a fixed tree into tot[v]; one
+// barrier; everyone reads tot.
+template <int NV32>
+__device__ __forceinline__ void warp_transpose32(const double* v, double* dst, int lane) {
+    double w[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = i < NV32 ? v[i] : 0.0;
+#pragma unroll
+    for (int h = 16, o = 16; o >= 1; h >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = up ? w[i] : w[i + h];
+            const double keep = up ? w[i + h] : w[i];
+            w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    if (lane < NV32) dst[lane] = w[0];
+}
+
 template <int NV>
 __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double* tot, int tid, int T, int nw) {
     constexpr int NP = NV <= 32 ? 32 : 64;
@@ -88,24 +106,11 @@ __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double*
             for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
             if (lane == i) scr[warp * NP + i] = x;
         }
-    } else {
-        double w[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) w[i] = i < NV ? v[i] : 0.0;
-#pragma unroll
-        for (int h = NP / 2, o = 16; o >= 1; h >>= 1, o >>= 1) {
-            const bool up = (lane & o) != 0;
-#pragma unroll
-            for (int i = 0; i < h; ++i) {
-                const double send = up ? w[i] : w[i + h];
-                const double keep = up ? w[i + h] : w[i];
-                w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-        }
-        constexpr int PER = NP / 32;  // values per lane after the reduction: indices lane*PER + j
-#pragma unroll
-        for (int j = 0; j < PER; ++j)
-            if (lane * PER + j < NV) scr[warp * NP + lane * PER + j] = w[j];
+    } else if (NV <= 32) {
+        warp_transpose32<NV>(v, scr + warp * NP, lane);
+    } else {  // two passes of 32: the padded 64-value transpose would hold 128 registers at once
+        warp_transpose32<32>(v, scr + warp * NP, lane);
+        warp_transpose32<NV - 32>(v + 32, scr + warp * NP + 32, lane);
     }
     named_sync(1, T);  // the compute threads (the producer warp is not in the reduction)
     for (int u = tid; u < NV; u += T) {
@@ -134,7 +139,10 @@ struct FalseT {
 
 template <int EP>
 struct ChainMaxThreads {  // compute threads; the CTA adds one producer warp
-    static constexpr int value = EP <= 8 ? 128 : 320;  // the plan keeps CTAs <= 128 threads below EP 16
+    // the plan keeps CTAs <= 128 threads below EP 16.  Registers go to warps in groups of four,
+    // so the 11 warps of an EP = 16 CTA get 168 registers per thread (an EP = 24 variant on 7 + 1
+    // warps with 255 registers spilled more: 2 x 24 pairs of v and row leave too little)
+    static constexpr int value = EP <= 8 ? 128 : 320;
 };
 
 // grid barrier over the compute threads of every CTA (the producer warps keep streaming)
@@ -151,7 +159,7 @@ __device__ __forceinline__ void grid_barrier_c(unsigned* counter, unsigned targe
     named_sync(1, T);
 }
 
-template <int EP, int R, int C>
+template <int EP, int R, int C, bool DELTA>
 __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
@@ -163,7 +171,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     // 8 for one long RK chain); CTA h owns columns [h*ld/C, (h+1)*ld/C) and the C slices of
     // every reduction are joined through distributed shared memory (st.async + mbarrier).
     const int h = (C >= 2) ? (int)cluster_rank() : 0;
-    const int64_t ldc = ld / C, cb = h * ldc;  // this CTA's columns
+    const int ldc = (int)(ld / C);  // this CTA's columns [cb, cb + ldc): 32-bit offsets within the slice
+    const int64_t cb = (int64_t)h * ldc;
     ChainSmem sm;
     unsigned long long* xbar = reinterpret_cast<unsigned long long*>(smem_raw);  // 2 exchange mbarriers
     unsigned long long* full = xbar + 2;                                         // 16 row-stage mbarriers
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     const int64_t w = blockIdx.x / C;  // worker id
     const int32_t* idx = a.idx + w * a.idx_stride;
     const double alpha = a.alphas[w];
-    const int64_t total = a.count * bs;  // draws of this worker in the launch
+    const int total = (int)(a.count * bs);  // draws of this worker in the launch (< 2^31, kz_solve checks)
     const double2* bs2 = reinterpret_cast<const double2*>(a.bs2);
     const unsigned row_bytes = (unsigned)(ldc * sizeof(double));
 
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     double v[2 * EP];
 #pragma unroll
     for (int p = 0; p < EP; ++p) {
-        const int64_t lc = 2 * ((int64_t)p * T + tid);
+        const int lc = 2 * (p * T + tid);
         double2 xv = make_double2(0.0, 0.0);
         if (lc < ldc) xv = __ldcg(reinterpret_cast<const double2*>(a.x + cb + lc));
         v[2 * p] = xv.x;
@@ -271,7 +280,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         const unsigned ph = (unsigned)((nex >> 1) & 1);
         ++nex;
         if (tid == 0) mbar_arrive_expect_tx(&xbar[xp], (unsigned)((C - 1) * nv * sizeof(double)));
-        for (int i = tid; i < (C - 1) * nv; i += T) {
+        // tid through an opaque move: the slot arithmetic below is formed here, not hoisted out
+        // of the row loop into registers the EP = 16 kernels would spill
+        for (int i = opaque_i32(tid); i < (C - 1) * nv; i += T) {
             const int vi = i % nv, pk = i / nv;
             const unsigned peer = (unsigned)(pk < h ? pk : pk + 1);
             st_async_f64(mapa_u32(smem_u32(xbuf + (xp * C + h) * Blk<R>::NVC + vi), peer), sm.tot[vi],
@@ -285,11 +296,15 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         }
     };
 
+    // Cold paths (stop rule, checkpoints, publishing v, reloading x) form their column offsets from
+    // an opaque tid: otherwise the compiler hoists EP 64-bit addresses out of the row loop and
+    // keeps them live across it, which the EP = 16 kernels pay for in spills.
     auto err_direct = [&]() {
         double e[1] = {0.0};
+        const int tid_o = opaque_i32(tid);
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
-            const int64_t lc = 2 * ((int64_t)p * T + tid);
+            const int lc = 2 * (p * T + tid_o);
             const int64_t col = cb + lc;
             if (lc < ldc) {
                 const double2 r = __ldg(reinterpret_cast<const double2*>(a.xref + col));
@@ -308,13 +323,15 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     int conv = 0, checks = 0;
     double err_last = 0.0;
     const double qd = (double)q;
-    const bool rka_delta = q > 1 && a.combine == KZ_COMBINE_RKA_DELTA;
+    // the threaded engine's RKA has instantiations of its own (DELTA): a runtime switch in the row
+    // loop cost the other engines 7 % (c2)
+    const bool rka_delta = DELTA && q > 1 && a.combine == KZ_COMBINE_RKA_DELTA;
     const bool use_stop = a.use_stop != 0;
     const bool ckpt_on = a.ckpt_every > 0;
     int nblk = 0;                 // blocks processed (phase timing)
-    int64_t d = 0;                // rows consumed
-    int64_t next_check = 0;       // q == 1: next row preceded by a stop-rule check (multiple of bs)
-    int64_t outer_end = bs;       // q == 1: row count at which the current outer iteration completes
+    int d = 0;                    // rows consumed
+    int next_check = 0;           // q == 1: next row preceded by a stop-rule check (multiple of bs)
+    int outer_end = (int)bs;      // q == 1: row count at which the current outer iteration completes
     int64_t kdone = a.k0;         // q == 1: outer iterations completed (global index)
     int64_t next_ck = ckpt_on ? (a.k0 / a.ckpt_every + 1) * a.ckpt_every : 0;
     int c_stage = 0;              // ring stage of row d
@@ -352,17 +369,35 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 if (!okr[r]) mbar_wait(&full[stg[r]], prs[r]);
         }
         if (rec) a.dbg[nblk * 8 + 2] = clock64();
-        // rows -> registers (kept for the update), (b, sq) -> lane r
-        double2 rr[R][EP];
+        // rows -> registers (kept for the update), (b, sq) -> lane r.  EP = 16 (168 registers per
+        // thread at 352 threads) cannot hold 16 pairs of v and 16 of the row across the reduction
+        // without spilling: its update re-reads the row from the ring (the stage is released after
+        // the update), a second pass over shared memory instead of local-memory traffic
+        constexpr bool KEEP_ROW = EP < 16;
+        constexpr int EPK = KEEP_ROW ? EP : 1;
+        double2 rr[R][EPK];
+        if constexpr (KEEP_ROW) {
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+            for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int p = 0; p < EP; ++p) {
-                const int64_t lc = 2 * ((int64_t)p * T + tid);
-                rr[r][p] = (r < Rp && lc < ldc)
-                               ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldc + lc)
-                               : make_double2(0.0, 0.0);
-            }
+                for (int p = 0; p < EP; ++p) {
+                    const int lc = 2 * (p * T + tid);
+                    rr[r][p < EPK ? p : 0] =
+                        (r < Rp && lc < ldc) ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldc + lc)
+                                             : make_double2(0.0, 0.0);
+                }
+        }
+        auto row = [&](int r, int p) -> double2 {  // the dot's read
+            if constexpr (KEEP_ROW) return rr[r][p < EPK ? p : 0];
+            const int lc = 2 * (p * T + tid);
+            return r < Rp ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldc + lc)
+                          : make_double2(0.0, 0.0);
+        };
+        auto row_again = [&](int r, int p) -> double2 {  // the update's read
+            if constexpr (KEEP_ROW) return rr[r][p < EPK ? p : 0];
+            const int lc = 2 * (p * T + tid);
+            return lds_reread_f64x2(sm.ring + (size_t)stg[r] * ldc + lc);
+        };
         double2 bq = make_double2(0.0, 1.0);
         if (lane < Rp) {
             int sl = c_stage + lane;
@@ -371,30 +406,33 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         }
         // (b_r, sq_r) sit in lane r; 1/sq_r formed there now (off the critical path: the division
         // overlaps the partial dots and the reduction)
-        const double inv_l = 1.0 / bq.y;
+        // (the threaded engine's RKA divides by q sq, parallel.py:221: its reciprocal instead)
+        const double inv_l = 1.0 / (rka_delta ? __dmul_rn(qd, bq.y) : bq.y);
         double vals[NV];
 #pragma unroll
         for (int i = 0; i < NV; ++i) vals[i] = 0.0;
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
-            const int64_t lc = 2 * ((int64_t)p * T + tid);
+            const int lc = 2 * (p * T + tid);
             const int64_t col = cb + lc;
             if (lc < ldc) {
                 const double vx = v[2 * p], vy = v[2 * p + 1];
 #pragma unroll
-                for (int r = 0; r < R; ++r) vals[r] = fma(rr[r][p].y, vy, fma(rr[r][p].x, vx, vals[r]));
+                double2 ar[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) ar[r] = row(r, p);
+#pragma unroll
+                for (int r = 0; r < R; ++r) vals[r] = fma(ar[r].y, vy, fma(ar[r].x, vx, vals[r]));
 #pragma unroll
                 for (int r = 1; r < R; ++r)
 #pragma unroll
                     for (int l = 0; l < r; ++l)
-                        vals[R + gidx(r, l)] =
-                            fma(rr[r][p].y, rr[l][p].y, fma(rr[r][p].x, rr[l][p].x, vals[R + gidx(r, l)]));
+                        vals[R + gidx(r, l)] = fma(ar[r].y, ar[l].y, fma(ar[r].x, ar[l].x, vals[R + gidx(r, l)]));
                 if (CHECK) {
                     const double2 xr = __ldg(reinterpret_cast<const double2*>(a.xref + col));
 #pragma unroll
                     for (int r = 0; r < R; ++r)
-                        vals[Blk<R>::NVN + r] =
-                            fma(rr[r][p].y, xr.y, fma(rr[r][p].x, xr.x, vals[Blk<R>::NVN + r]));
+                        vals[Blk<R>::NVN + r] = fma(ar[r].y, xr.y, fma(ar[r].x, xr.x, vals[Blk<R>::NVN + r]));
                     const double d0 = vx - xr.x, d1 = vy - xr.y;
                     vals[NV - 1] = fma(d1, d1, fma(d0, d0, vals[NV - 1]));
                 }
@@ -439,26 +477,29 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 }
                 if (r < Reff) {
                     if (CHECK && d + r == next_check) next_check += bs;
-                    s[r] = rka_delta ? __ddiv_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), __dmul_rn(qd, sqr))
-                                     : __dmul_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), invr);
+                    s[r] = __dmul_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), invr);
                     if (CHECK) e = fma(s[r] * s[r], sqr, fma(2.0 * s[r], dr - vals[Blk<R>::NVN + r], e));
                 }
             }
         }
         if (rec) a.dbg[nblk * 8 + 5] = clock64();
-        // apply the Reff projections in order with the reference's rounding
+        // apply the Reff projections in order with the reference's rounding.  The threaded RKA
+        // publishes the increment itself: v restarts from 0 (0 + fl(s a) is exact; v is reloaded
+        // from x after the combine), so the row loop below is the same for every engine
+        if (rka_delta) {
+#pragma unroll
+            for (int i = 0; i < 2 * EP; ++i) v[i] = 0.0;
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (r < Reff) {
 #pragma unroll
                 for (int p = 0; p < EP; ++p) {
-                    const int64_t lc = 2 * ((int64_t)p * T + tid);
-                    if (lc < ldc && rka_delta) {  // the increment itself; v is reloaded from x
-                        v[2 * p] = __dmul_rn(s[r], rr[r][p].x);
-                        v[2 * p + 1] = __dmul_rn(s[r], rr[r][p].y);
-                    } else if (lc < ldc) {
-                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], rr[r][p].x));
-                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], rr[r][p].y));
+                    const int lc = 2 * (p * T + tid);
+                    if (lc < ldc) {
+                        const double2 ap = row_again(r, p);
+                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], ap.x));
+                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], ap.y));
                     }
                 }
                 if (q == 1 && d + r + 1 == outer_end) {  // outer iteration kdone completes here
@@ -468,9 +509,10 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                         next_ck += a.ckpt_every;
                         const int64_t slot = kdone / a.ckpt_every - 1;
                         if (slot < a.ckpt_cap) {
+                            const int tid_o = opaque_i32(tid);
 #pragma unroll
                             for (int p = 0; p < EP; ++p) {
-                                const int64_t lc = 2 * ((int64_t)p * T + tid);
+                                const int lc = 2 * (p * T + tid_o);
                                 const int64_t col = cb + lc;
                                 if (lc >= ldc) continue;  // lanes past this CTA's slice own nothing
                                 if (col < a.n) a.ckpt[slot * a.n + col] = v[2 * p];
@@ -500,7 +542,13 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         return Reff;
     };
 
-    if (q == 1) {
+    // Which drivers an instantiation carries (the plan guarantees the pairing): one chain (q = 1)
+    // never runs on a pair with EP >= 8 (rows of < 1536 columns) and workers averaged (q > 1)
+    // never run on 4- or 8-CTA clusters.  Compiling the unused driver out leaves the register
+    // allocator one loop to fit (the EP = 16 pair kernel then keeps v and the row without spilling).
+    constexpr bool ONE_CHAIN = !(C == 2 && EP >= 8);
+    constexpr bool AVERAGED = C <= 2;
+    if (ONE_CHAIN && (q == 1 || !AVERAGED)) {
         // one chain: outer iteration k = rows [k*bs, (k+1)*bs); x = v after each
         while (d < total) {
             const int Rp = (int)((total - d) < R ? (total - d) : R);
@@ -517,7 +565,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             err_last = e;
             if (e < a.eps) conv = 1;
         }
-    } else {
+    } else if (AVERAGED) {
         for (int64_t kk = 0;; ++kk) {
             const bool last = (kk == a.count);
             if (use_stop && (!last || a.final_check)) {
@@ -530,17 +578,21 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 }
             }
             if (last) break;
-            const int64_t end = (kk + 1) * bs;
+            const int end = (int)((kk + 1) * bs);
             while (d < end) block((int)((end - d) < R ? (end - d) : R), FalseT{});
             // publish v_w, average column slices in worker order, redistribute x
             const int64_t k = a.k0 + kk;
             const bool ck = ckpt_on && ((k + 1) % a.ckpt_every) == 0 && ((k + 1) / a.ckpt_every) <= a.ckpt_cap;
             const int64_t slot = ck ? (k + 1) / a.ckpt_every - 1 : 0;
             double* vw = a.V + w * ld;
+            {
+                const int tid_o = opaque_i32(tid);
 #pragma unroll
-            for (int p = 0; p < EP; ++p) {
-                const int64_t lc = 2 * ((int64_t)p * T + tid);
-                if (lc < ldc) __stcg(reinterpret_cast<double2*>(vw + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
+                for (int p = 0; p < EP; ++p) {
+                    const int lc = 2 * (p * T + tid_o);
+                    if (lc < ldc)
+                        __stcg(reinterpret_cast<double2*>(vw + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
+                }
             }
             grid_barrier_c(a.barrier, (++epoch) * gridDim.x, T);
             const int64_t G = gridDim.x;
@@ -570,9 +622,10 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 if (ck && col < a.n) a.ckpt[slot * a.n + col] = xn;
             }
             grid_barrier_c(a.barrier, (++epoch) * gridDim.x, T);
+            const int tid_o = opaque_i32(tid);
 #pragma unroll
             for (int p = 0; p < EP; ++p) {
-                const int64_t lc = 2 * ((int64_t)p * T + tid);
+                const int lc = 2 * (p * T + tid_o);
                 if (lc < ldc) {
                     const double2 xv = __ldcg(reinterpret_cast<const double2*>(a.x + cb + lc));
                     v[2 * p] = xv.x;
@@ -587,7 +640,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         double* dst = a.partial ? a.partial : a.x;
 #pragma unroll
         for (int p = 0; p < EP; ++p) {
-            const int64_t lc = 2 * ((int64_t)p * T + tid);
+            const int lc = 2 * (p * T + tid);
             if (lc < ldc) __stcg(reinterpret_cast<double2*>(dst + cb + lc), make_double2(v[2 * p], v[2 * p + 1]));
         }
     }
@@ -600,13 +653,12 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     }
 }
 
-#define KZ_CHAIN(EP, R, C) template __global__ void chain_kernel<EP, R, C>(SolveArgs);
+#define KZ_CHAIN(EP, R, C) template __global__ void chain_kernel<EP, R, C, false>(SolveArgs);
+#define KZ_CHAIN_DELTA(EP, R) template __global__ void chain_kernel<EP, R, 1, true>(SolveArgs);
 KZ_CHAIN(1, 1, 1)
 KZ_CHAIN(1, 4, 1)
-KZ_CHAIN(1, 8, 1)
 KZ_CHAIN(2, 1, 1)
 KZ_CHAIN(2, 4, 1)
-KZ_CHAIN(2, 8, 1)
 KZ_CHAIN(4, 1, 1)
 KZ_CHAIN(4, 2, 1)
 KZ_CHAIN(4, 4, 1)
@@ -629,6 +681,18 @@ KZ_CHAIN(8, 2, 4)
 KZ_CHAIN(16, 1, 4)
 KZ_CHAIN(1, 4, 8)
 KZ_CHAIN(2, 4, 8)
+// the threaded engine's RKA (one CTA per worker)
+KZ_CHAIN_DELTA(1, 1)
+KZ_CHAIN_DELTA(1, 4)
+KZ_CHAIN_DELTA(2, 1)
+KZ_CHAIN_DELTA(2, 4)
+KZ_CHAIN_DELTA(4, 1)
+KZ_CHAIN_DELTA(4, 2)
+KZ_CHAIN_DELTA(4, 4)
+KZ_CHAIN_DELTA(8, 1)
+KZ_CHAIN_DELTA(8, 2)
+KZ_CHAIN_DELTA(16, 1)
 #undef KZ_CHAIN
+#undef KZ_CHAIN_DELTA
 
 }  // namespace kz

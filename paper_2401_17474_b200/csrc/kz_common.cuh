@@ -435,6 +435,14 @@ namespace kz {
 
 // An int the compiler cannot re-derive (e.g. from the kernel-parameter bank):
 // loop-invariant offsets stay in registers.
+// a shared-memory load the compiler may not merge with an earlier load of the same address (a
+// deliberate re-read that keeps a value out of registers across a long stretch of code)
+__device__ __forceinline__ double2 lds_reread_f64x2(const double* p) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int opaque_i32(int v) {
     int r;
     asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));

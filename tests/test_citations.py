@@ -51,7 +51,7 @@ SKIP = {"SURVEY.md", "BASELINE.md", "VERDICT.md", "ADVICE.md", "PAPERS.md", "SNI
 def _repo_files():
     for f in glob.glob(os.path.join(ROOT, "**", "*"), recursive=True):
         rel = os.path.relpath(f, ROOT)
-        if not os.path.isfile(f) or rel in SKIP or rel.startswith(("gpurun_out", ".git")):
+        if not os.path.isfile(f) or rel in SKIP or rel.startswith(("gpurun_out", ".git", "wt_", "baseline")):
             continue
         if rel.rsplit(".", 1)[-1] in ("py", "c", "h", "cu", "cuh", "md", "sh"):
             yield rel

@@ -1,7 +1,9 @@
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
-lscpu > gpurun_out/lscpu.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu4.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu4.log
+timeout 900 python bench.py > gpurun_out/bench4.json 2> gpurun_out/bench4.err; echo "bench rc=$?"
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench4.json').read().strip().splitlines()[-1])
+print({k:d[k] for k in ('value','ms_per_step','iterations')}, d['roofline']['achieved'], d['roofline']['frac'], d['e2e']['value'], d['clocks'])
+for e in d.get('extra_workloads',[]): print(e.get('workload'), e.get('ms_per_step'), (e.get('roofline') or {}).get('frac'), e.get('error'))
+PY
