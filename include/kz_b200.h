@@ -205,6 +205,9 @@ typedef struct {
     int32_t plan_rows;      /* chain kernel: rows per CTA reduction (R)                        */
     int32_t plan_cluster;   /* CTAs per thread-block cluster (chain: CTAs per worker)           */
     int32_t plan_stages;    /* shared-memory ring stages                                        */
+    int32_t plan_waves;     /* chain kernel: launches per outer iteration (workers beyond the
+                               co-resident CTAs run in waves; 1 = all workers at once)          */
+    int32_t pad;
 } kz_result;
 
 /* Full solve with host output x_host (n values, may be NULL). */

@@ -98,6 +98,8 @@ class Result(C.Structure):
         ("plan_rows", C.c_int32),
         ("plan_cluster", C.c_int32),
         ("plan_stages", C.c_int32),
+        ("plan_waves", C.c_int32),
+        ("pad", C.c_int32),
     ]
 
 

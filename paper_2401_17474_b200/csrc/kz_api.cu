@@ -826,6 +826,7 @@ struct Plan {
     bool wg = false;    // rka kernel: worker groups (cluster g runs q/G workers over all columns)
     bool xr = false;    // rka kernel: cross-rank column sums (set per launch by kz_solve_sharded, not planned)
     bool delta = false; // chain: the threaded engine's RKA increments (chain_kernel<..., DELTA = true>)
+    int waves = 1;      // chain: launches per outer iteration when the workers exceed the co-resident CTAs
     size_t smem = 0;
 };
 
@@ -964,12 +965,23 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     pl.smem = chain_smem(ldc, stages, R, T, C);
     pl.ctas = (int)(q * C);
     KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    pl.waves = 1;
     if (pl.ctas > 1) {
         int per_sm = 0;
         KZ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, T + 32, pl.smem));
-        if ((int64_t)per_sm * s->sms < pl.ctas)
-            return fail(KZ_EINVAL, "q=%lld workers exceed the %d co-resident CTAs of the chain kernel", (long long)q,
-                        per_sm * s->sms);
+        const int64_t cap = (int64_t)per_sm * s->sms / C;  // co-resident workers
+        if (cap * C < pl.ctas) {
+            // more workers than co-resident CTAs: each outer iteration runs its workers in waves of
+            // at most `cap`, every wave adding its ordered worker sum to the previous waves'
+            // (the per-iteration driver, kz_solve_sharded's loop); waves of one worker would take
+            // the single-chain path, so every wave keeps at least two
+            const int64_t W = (q + cap - 1) / std::max<int64_t>(cap, 1);
+            if (cap < 2 || q / W < 2 || pl.delta || p->variant == KZ_CK)
+                return fail(KZ_EINVAL, "q=%lld workers exceed the %lld co-resident workers of the chain kernel",
+                            (long long)q, (long long)cap);
+            pl.waves = (int)W;
+            pl.ctas = (int)((q + W - 1) / W * C);
+        }
     }
     return KZ_OK;
 }
@@ -992,8 +1004,14 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     }
     int rc = KZ_EINVAL;
     std::string first_err;
-    for (int c = C; c >= 1; c /= 2) {
-        if (c > 1 && (s->ld % (2 * c) != 0 || s->no_pairs || c * q > s->sms)) continue;  // whole 16-byte pairs
+    // the preferred width, narrower ones, then (workers averaged over long rows) pairs in waves
+    int cand[6], nc = 0;
+    for (int c = C; c >= 1; c /= 2) cand[nc++] = c;
+    if (q > 1 && C < 2 && !pl.delta) cand[nc++] = 2;
+    for (int i = 0; i < nc; ++i) {
+        const int c = cand[i];
+        if (c > 1 && (s->ld % (2 * c) != 0 || s->no_pairs)) continue;  // whole 16-byte pairs
+        if (c > 1 && i == 0 && c * q > s->sms) continue;  // preferred pairs: only without waves
         rc = plan_chain_c(s, p, q, c, pl);
         if (rc == KZ_OK) return KZ_OK;
         if (first_err.empty()) first_err = g_err;
@@ -1539,13 +1557,14 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     r->plan_rows = pl.kernel == KZ_KERNEL_CHAIN ? pl.rows : 1;
     r->plan_cluster = pl.kernel == KZ_KERNEL_CHAIN ? pl.pair : pl.cluster;
     r->plan_stages = pl.stages;
+    r->plan_waves = pl.waves;
 
     // --- scratch ---
     const int64_t draws_per_iter = q * bs;
     const int64_t idx_cap = std::max<int64_t>(draws_per_iter, (int64_t)8 << 20);
     const int64_t chunk_cap = std::max<int64_t>(1, idx_cap / draws_per_iter);
     KZ_TRY(s->idx.ensure(std::min<int64_t>(idx_cap, chunk_cap * draws_per_iter)));
-    if (pl.kernel == KZ_KERNEL_CHAIN && q > 1) KZ_TRY(s->V.ensure((size_t)q * s->ld));
+    if (pl.kernel == KZ_KERNEL_CHAIN && q > 1) KZ_TRY(s->V.ensure((size_t)((q + pl.waves - 1) / pl.waves) * s->ld));
     KZ_TRY(s->part.ensure(std::max<size_t>(16, 2 * (size_t)pl.ctas * (q + 1))));
     if (pl.tma && pl.ctas > pl.cluster) {
         // tagged words of the rka kernel's cluster exchange (a buffer of their own; tags restart
@@ -1589,8 +1608,8 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     const bool phase_timing = dbg_env("KZ_PHASE_TIMING") != nullptr;
     args.ablate = dbg_env("KZ_ABLATE") ? atoi(dbg_env("KZ_ABLATE")) : 0;
     if (phase_timing) {
-        KZ_TRY(s->dbg.ensure(32 * 128));
-        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 128 * sizeof(long long), st));
+        KZ_TRY(s->dbg.ensure(32 * 128 * 16));
+        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 128 * 16 * sizeof(long long), st));
         args.dbg = s->dbg.p;
     }
 
@@ -1627,7 +1646,10 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
     if (lrc != KZ_OK && pl.kernel == KZ_KERNEL_CHAIN && pl.pair >= 2 && first) {
         // CTA-pair clusters not launchable cooperatively here: one CTA per worker
         s->no_pairs = true;  // remembered for this system (no process-wide side effects)
+        const int waves_before = pl.waves;
         KZ_TRY(plan_chain(s, p, q, pl));
+        if (pl.waves != waves_before)
+            return fail(KZ_ECUDA, "CTA pairs not launchable here and one CTA per worker changes the wave count");
         memcpy(s->plan_blob, &pl, sizeof(Plan));
         args.stages = pl.stages;
         r->ctas = pl.ctas;
@@ -1655,6 +1677,35 @@ static int launch_step(kz_system* s, const kz_params* p, kz_result* r, SolveCtx&
     return lrc;
 }
 
+// One outer iteration's local step in waves of co-resident workers (chain kernel, partial mode):
+// wave j runs workers [q j / W, q (j + 1) / W) and adds their ordered sum to the previous waves'
+// (SolveArgs::accumulate), so S is bit-identical to one launch over all q workers.
+static int launch_waves(kz_system* s, const kz_params* p, kz_result* r, SolveCtx& cx, bool first, cudaStream_t st) {
+    Plan& pl = cx.pl;
+    SolveArgs& a = cx.args;
+    const int W = pl.waves;
+    if (W <= 1) {
+        a.accumulate = 0;
+        return launch_step(s, p, r, cx, first, st);
+    }
+    const SolveArgs saved = a;
+    const int ctas = pl.ctas;
+    const int64_t q = cx.q;
+    int rc = KZ_OK;
+    for (int j = 0; j < W && rc == KZ_OK; ++j) {
+        const int64_t w0 = q * j / W, w1 = q * (j + 1) / W;
+        a.q = w1 - w0;
+        a.alphas = saved.alphas + w0;
+        a.idx = saved.idx + w0 * saved.idx_stride;
+        a.accumulate = j > 0 ? 1 : 0;
+        pl.ctas = (int)((w1 - w0) * pl.pair);
+        rc = launch_step(s, p, r, cx, first && j == 0, st);
+        pl.ctas = ctas;
+    }
+    a = saved;
+    return rc;
+}
+
 extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, double* x_host, void* stream) {
     NvtxScope nvtx_("kz_solve");
     if (!s || !p || !r) return fail(KZ_EINVAL, "null argument");
@@ -1664,6 +1715,14 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
     cudaStream_t st = pick_stream(s, stream);
     SolveCtx cx;
     KZ_TRY(solve_setup(s, p, r, st, cx));
+    if (cx.pl.waves > 1) {
+        // more workers than co-resident CTAs: the per-outer-iteration driver runs them in waves
+        if (cx.trace_mode) return fail(KZ_EINVAL, "trace mode with more workers than co-resident CTAs");
+        if (cx.partial_mode) return fail(KZ_EINVAL, "partial steps with more workers than co-resident CTAs");
+        kz_params pp = *p;
+        pp.flags |= KZ_FLAG_SHARDED_LOOP;
+        return kz_solve_sharded(s, nullptr, &pp, r, x_host, stream);
+    }
     const int64_t q = cx.q, bs = cx.bs;
     const bool budget_mode = cx.budget_mode, trace_mode = cx.trace_mode, stop_mode = cx.stop_mode,
                cyclic = cx.cyclic, partial_mode = cx.partial_mode, phase_timing = cx.phase_timing;
@@ -1861,6 +1920,50 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             fprintf(stderr, "[kz phase end, max over warps, cycles from start] top %.0f issued %.0f dots %.0f waited %.0f "
                             "err %.0f scales %.0f update %.0f | iteration %.0f (n=%d)\n", acc[0] / nrec, acc[1] / nrec,
                     acc[2] / nrec, acc[3] / nrec, acc[4] / nrec, acc[5] / nrec, acc[6] / nrec, span / nrec, nrec);
+        if (atoi(dbg_env("KZ_PHASE_TIMING")) >= 3 && pl.tma) {
+            // every cluster's rank-0 CTA: owner-warp and warp-0 stamps relative to its own iteration
+            // start, and the spread of the iteration starts across clusters (globaltimer, ns)
+            const int G = pl.ctas / pl.cluster;
+            std::vector<long long> hh((size_t)32 * 128 * 16);
+            KZ_CUDA(cudaMemcpy(hh.data(), s->dbg.p, hh.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+            auto at = [&](int g, int k, int w, int sl) { return hh[(((size_t)g * 32 + k) * 8 + w) * 16 + sl]; };
+            double spread = 0;
+            int ns = 0;
+            for (int k = 4; k < 31; ++k) {
+                long long lo = -1, hi = -1;
+                for (int g = 0; g < G; ++g) {
+                    const long long t = at(g, k, 0, 14);
+                    if (!t) continue;
+                    lo = lo < 0 || t < lo ? t : lo;
+                    hi = hi < 0 || t > hi ? t : hi;
+                }
+                if (lo >= 0) spread += (double)(hi - lo), ++ns;
+            }
+            fprintf(stderr, "[kz clusters] %d clusters; iteration-start spread across clusters %.0f ns (mean)\n", G,
+                    ns ? spread / ns : 0.0);
+            const int ow = 6;
+            for (int g = 0; g < G; ++g) {
+                double m[8] = {0};
+                int nk = 0;
+                for (int k = 4; k < 31; ++k) {
+                    const long long t0 = at(g, k, 0, 0), t0o = at(g, k, ow, 0), tn = at(g, k + 1, 0, 0);
+                    if (!t0 || !tn || !t0o) continue;
+                    m[0] += (double)(at(g, k, 0, 13) - t0);    // dots + pushes done (warp 0)
+                    m[1] += (double)(at(g, k, ow, 7) - t0o);   // partials at the owner
+                    m[2] += (double)(at(g, k, ow, 10) - t0o);  // owner total
+                    m[3] += (double)(at(g, k, ow, 11) - t0o);  // scale formed (after the cross-cluster sum)
+                    m[4] += (double)(at(g, k, ow, 9) - t0o);   // broadcast issued
+                    m[5] += (double)(at(g, k, 0, 3) - t0);     // scales arrived (warp 0)
+                    m[6] += (double)(at(g, k, 0, 5) - t0);     // average done
+                    m[7] += (double)(tn - t0);                 // iteration
+                    ++nk;
+                }
+                if (nk)
+                    fprintf(stderr, "[kz cluster %d] dots %.0f partials %.0f owner %.0f xsum %.0f bcast %.0f scales %.0f "
+                                    "avg %.0f | iteration %.0f cycles\n", g, m[0] / nk, m[1] / nk, m[2] / nk, m[3] / nk,
+                            m[4] / nk, m[5] / nk, m[6] / nk, m[7] / nk);
+            }
+        }
         if (atoi(dbg_env("KZ_PHASE_TIMING")) >= 2) {  // per-warp mean stamps relative to the earliest warp start
             double pw[8][16] = {{0}};
             int nk = 0;
@@ -2435,8 +2538,8 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     r->final_residual = NAN;
     if (p->variant != KZ_RKA && p->variant != KZ_RKAB)
         return fail(KZ_EINVAL, "row-sharded solves run RKA or RKAB (variant %d)", p->variant);
-    if (p->trace_step > 0 || p->ckpt_every > 0)
-        return fail(KZ_EINVAL, "row-sharded solves have no trace or checkpoint mode");
+    if (p->trace_step > 0) return fail(KZ_EINVAL, "row-sharded solves have no trace mode");
+    if (p->ckpt_every > 0 && comm) return fail(KZ_EINVAL, "row-sharded solves have no checkpoint mode");
     if (comm && comm->device != s->device)
         return fail(KZ_EINVAL, "communicator on device %d, shard on device %d", comm->device, s->device);
     const int world = comm ? comm->world : 1;
@@ -2544,6 +2647,8 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
         args.x_div = (double)Q;
     }
     int64_t chunk = stop_mode ? 64 : chunk_max;
+    const int64_t ck_cap = (!comm && p->ckpt_every > 0) ? cx.n_ck_cap : 0;  // waves of one GPU: checkpoints
+    if (ck_cap > 0 && fused) return fail(KZ_EINVAL, "checkpoints of the per-iteration rka loop");
     while (!xr && !converged && k < limit) {
         const int64_t c = std::min<int64_t>(chunk, limit - k);
         // row draws of the whole chunk: one sampler launch (x-independent)
@@ -2561,12 +2666,15 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
             args.idx_stride = chain ? count : q;
             args.partial = Sk;
             if (fused) args.x_sum = kk == 0 ? nullptr : s->S.p + ((kk - 1) & 1) * s->ld;  // x_0: resident
-            KZ_TRY(launch_step(s, &pp, r, cx, kk == 0, st));
+            KZ_TRY(launch_waves(s, &pp, r, cx, kk == 0, st));
             if (comm) KZ_NCCL(g_nccl.all_reduce(Sk, Sk, (size_t)s->ld, ncclFloat64, ncclSum, comm->nccl, st));
             if (!fused) {
                 shard_average_kernel<<<1, 1024, 0, st>>>(Sk, (double)Q, s->n, s->ld, s->xref.p, s->x.p, p->epsilon,
                                                          stop_mode ? 1 : 0, kk + 1, s->errs.p + i, s->halt.p);
                 KZ_TRY(check_launch("shard_average_kernel"));
+                if (ck_cap > 0 && (kk + 1) % p->ckpt_every == 0 && (kk + 1) / p->ckpt_every <= ck_cap)
+                    KZ_CUDA(cudaMemcpyAsync(s->ckpt.p + ((kk + 1) / p->ckpt_every - 1) * s->n, s->x.p,
+                                            s->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
             }
         }
         const bool last_chunk = k + c >= limit;
@@ -2619,6 +2727,17 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
     r->kernel_used = cx.pl.tma ? KZ_KERNEL_RKA : cx.pl.kernel;
     r->ctas = cx.pl.ctas;
     r->threads = cx.pl.threads;
+    if (ck_cap > 0) {
+        r->n_ckpt = std::min<int64_t>(ck_cap, k / p->ckpt_every);
+        if (r->n_ckpt > 0 && p->ckpt_host)
+            KZ_CUDA(cudaMemcpyAsync(p->ckpt_host, s->ckpt.p, (size_t)r->n_ckpt * s->n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    r->plan_ep = cx.pl.kernel == KZ_KERNEL_CHAIN ? cx.pl.ep : cx.pl.epl;
+    r->plan_rows = cx.pl.kernel == KZ_KERNEL_CHAIN ? cx.pl.rows : 1;
+    r->plan_cluster = cx.pl.kernel == KZ_KERNEL_CHAIN ? cx.pl.pair : cx.pl.cluster;
+    r->plan_stages = cx.pl.stages;
+    r->plan_waves = cx.pl.waves;
     if (x_host) KZ_CUDA(cudaMemcpyAsync(x_host, s->x.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, st));
     KZ_CUDA(cudaStreamSynchronize(st));
     r->kernel_launches = g_launches.load() - launches0;

@@ -611,7 +611,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 }
             }
             for (int64_t col = c0 + tid; a.combine == KZ_COMBINE_AVERAGE && col < c1; col += T) {
-                double acc = __ldcg(a.V + col);
+                // ((S + v_0) + v_1) + ...: a later wave continues the earlier waves' ordered sum
+                double acc = a.accumulate ? __dadd_rn(__ldcg(a.partial + col), __ldcg(a.V + col)) : __ldcg(a.V + col);
                 for (int64_t t = 1; t < q; ++t) acc = __dadd_rn(acc, __ldcg(a.V + t * ld + col));
                 if (a.partial) {  // row-sharded step: the un-normalised local sum, x untouched
                     __stcg(a.partial + col, acc);

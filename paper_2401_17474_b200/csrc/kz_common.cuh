@@ -443,6 +443,13 @@ __device__ __forceinline__ double2 lds_reread_f64x2(const double* p) {
     return v;
 }
 
+// the GPU-wide nanosecond timer (comparable across SMs, unlike clock64)
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ int opaque_i32(int v) {
     int r;
     asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));

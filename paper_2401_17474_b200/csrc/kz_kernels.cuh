@@ -58,6 +58,10 @@ struct SolveArgs {
     // chain kernel, q > 1: how the worker estimates meet (KZ_COMBINE_*): the sequential engine's
     // ordered average, or the threaded engine's increments added to x in worker order
     int combine;
+    // chain kernel, row-sharded / wave steps (partial != nullptr): 1 = add this launch's worker sum to
+    // the sum already in partial, in worker order (the workers of one outer iteration in several
+    // launches when they are more than the co-resident CTAs)
+    int accumulate;
 };
 
 enum {

@@ -279,8 +279,14 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         if (last && !want_check) break;
         const int par = kk & 1;
         const unsigned bpar = (unsigned)((kk >> 1) & 1);
-        const bool rec = TIMING && a.dbg != nullptr && c == 0 && lane == 0 && kk < 32;
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 0] = clock64();
+        // phase stamps (KZ_PHASE_TIMING): rank 0 of every cluster, lane 0 of every warp, iterations < 32,
+        // slot [cluster][iteration][warp][16]
+        const bool rec = TIMING && a.dbg != nullptr && cr == 0 && lane == 0 && kk < 32;
+        long long* const stamp = TIMING ? a.dbg + ((size_t)(gid * 32 + kk) * 8 + warp) * 16 : nullptr;
+        if (TIMING && rec) {
+            stamp[0] = clock64();
+            stamp[14] = (long long)globaltimer_ns();
+        }
         if (tid == 32) {  // warp 1: not on the producer warp's scheduler (warps 0, 4, 8 share one)
             if (!last) {
                 if (n_own > 0) mbar_arrive_expect_tx(&xbar[par], (unsigned)(n_own * Pc * (int)sizeof(double)));
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         const double* rows = reinterpret_cast<const double*>(ring + st * stage_bytes);
         const double* bsr = reinterpret_cast<const double*>(ring + st * stage_bytes + rows_bytes);
         if (!last && !ready) mbar_wait(&full[st], fph);
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 1] = clock64();
+        if (TIMING && rec) stamp[1] = clock64();
         // ---- 1-2. partial dots of this warp's rows -> their owners ------------------------
         if (!last) {
             int o_push = o_push0, s_push = s_push0;  // owner, slot of round 0
@@ -316,7 +322,6 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                             }
                     }
                 }
-                if (TIMING && rec && rb == wb) a.dbg[(kk * 8 + warp) * 16 + 14] = clock64() + (long long)(acc[0] * 0.0);
 #pragma unroll
                 for (int h = NR / 2, o = LG / 2; h >= 1; h >>= 1, o >>= 1) {
                     const bool up = (gl & o) != 0;
@@ -330,7 +335,6 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
                 acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
                 const double odd = __shfl_xor_sync(0xffffffffu, acc[0], 4);
-                if (TIMING && rec && rb == wb) a.dbg[(kk * 8 + warp) * 16 + 15] = clock64() + (long long)(odd * 0.0);
                 const int t = rb + grp * NR + ri;
                 if (SR ? push_ok : (t < we && pusher)) {
                     const unsigned off = (unsigned)(((par * Pc + cr) * RPO + s_push) * (int)sizeof(double));
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     for (s_push += 8; s_push >= RPO; s_push -= RPO) ++o_push;  // next round: 8 rows on
             }
         }
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 13] = clock64();
+        if (TIMING && rec) stamp[13] = clock64();
         // ---- error piece of x_k (needed only at the end of the iteration) -----------------
         if (want_check && warp == 0 && !(TIMING && (a.ablate & 1))) {
             double e2 = 0.0;
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             st_async_f64(mapa_u32(ein_u, (unsigned)eown) + (unsigned)((par * Pc + cr) * (int)sizeof(double)), 0.0,
                          mapa_u32(ebin_u + 8u * par, (unsigned)eown));
         }
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 2] = clock64();
+        if (TIMING && rec) stamp[2] = clock64();
         // the next stage's rows are awaited now, while the exchange is in flight
         ready = false;
         if (warp < NW - NOWN && kk + 1 < count) {
@@ -385,7 +389,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             const int my_pairs = npair > ow ? (npair - ow + NOWN - 1) / NOWN : 0;
             if (!last && my_pairs > 0) {
                 mbar_wait(&xbar[par], bpar);
-                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 7] = clock64();
+                if (TIMING && rec) stamp[7] = clock64();
                 const double* ib = inbuf + par * Pc * RPO;
                 for (int l0 = 0; l0 < 2 * my_pairs; l0 += 16) {  // 16 items per pass, 2 lanes each
                     const int li = l0 + (lane >> 1);
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     const int t = my_lo + i;
                     double tot = owner_total(ib + i, RPO, live);
                     if (TIMING && rec && warp == NW - NOWN && l0 == 0)
-                        a.dbg[(kk * 8 + warp) * 16 + 10] = clock64() + (long long)(tot * 0.0);
+                        stamp[10] = clock64() + (long long)(tot * 0.0);
                     if (Gx > 1 && u == 0 && live) {
                         // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
                         ll_store(ll + ((size_t)gx * q1 + t) * 2, tot, tag);
@@ -405,13 +409,12 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                         const double d = __dsub_rn(rec4[0], tot);
                         const double nume = unit_alpha ? d : __dmul_rn(alp[t], d);  // 1 * d == d exactly
                         sout[i] = div_rn_fast(nume, rec4[1], rec4[2]);
-                        if (TIMING && a.dbg != nullptr && c == 0 && lane == 0 && kk < 32 && warp == NW - NOWN &&
-                            l0 == 0)
-                            a.dbg[(kk * 8 + warp) * 16 + 11] = clock64() + (long long)(sout[i] * 0.0);
+                        if (TIMING && rec && warp == NW - NOWN && l0 == 0)
+                            stamp[11] = clock64() + (long long)(sout[i] * 0.0);
                     }
                 }
                 __syncwarp();
-                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 8] = clock64();
+                if (TIMING && rec) stamp[8] = clock64();
                 // broadcast: this warp's worker pairs as 16-byte pushes to every CTA of the cluster
                 for (int k = lane; k < my_pairs * Pc; k += 32) {
                     const int pi = ow + NOWN * (k >> pcs), peer = k & (Pc - 1);
@@ -424,11 +427,11 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     else
                         st_async_f64(dst, sout[i], bar);
                 }
-                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 9] = clock64();
+                if (TIMING && rec) stamp[9] = clock64();
             }
             if (warp == OW && want_check && cr == eown) {
                 mbar_wait(&ebin[par], bpar);
-                if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 10] = clock64();
+                if (TIMING && rec) stamp[10] = clock64();
                 double tot = owner_total(ein + par * Pc, 1, lane < 2);
                 if (Gx > 1 && lane == 0) {
                     ll_store(ll + ((size_t)gx * q1 + q) * 2, tot, tag);
@@ -450,9 +453,9 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         }
         // ---- 4. scales arrive ------------------------------------------------------------
         mbar_wait(&sbar[par], bpar);
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 3] = clock64();
+        if (TIMING && rec) stamp[3] = clock64();
         const double* sc = scal + par * q4;
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 4] = clock64();
+        if (TIMING && rec) stamp[4] = clock64();
         // ---- 5. average over this warp's workers -----------------------------------------
         double2 acc[EPL];
 #pragma unroll
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             for (int e = 0; e < EPL; ++e)
                 if (vld[e]) *reinterpret_cast<double2*>(upd + warp * cwb + 2 * (gl + LG * e)) = acc[e];
         }
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 5] = clock64();
+        if (TIMING && rec) stamp[5] = clock64();
         named_sync(CBAR, NW * 32);
         // ---- combine: x_{k+1} = (fixed tree over the warps' sums) / q ----------------------
         // narrow slices: every warp forms its own lanes' columns (no second barrier);
@@ -644,9 +647,9 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         }
         // ---- stop rule on x_k (its error total arrived while x_{k+1} was formed) ----------
         if (want_check) {
-            if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 11] = clock64();
+            if (TIMING && rec) stamp[11] = clock64();
             mbar_wait(&ebar[par], bpar);
-            if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 12] = clock64();
+            if (TIMING && rec) stamp[12] = clock64();
             const double err = errs[par];
             ++checks;
             err_last = err;
@@ -657,7 +660,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         }
 #pragma unroll
         for (int e = 0; e < EPL; ++e) xv[e] = xn[e];
-        if (TIMING && rec) a.dbg[(kk * 8 + warp) * 16 + 6] = clock64();
+        if (TIMING && rec) stamp[6] = clock64();
         if (++st == D) {
             st = 0;
             fph ^= 1u;

@@ -330,7 +330,7 @@ class DeviceSystem:
                 "kernel": N.KERNEL_NAMES.get(int(r.kernel_used), "?"), "launches": int(r.kernel_launches),
                 "ctas": int(r.ctas), "threads": int(r.threads),
                 "plan": {"ep": int(r.plan_ep), "rows": int(r.plan_rows), "cluster": int(r.plan_cluster),
-                         "stages": int(r.plan_stages)}}
+                         "stages": int(r.plan_stages), "waves": int(r.plan_waves)}}
 
     def set_x(self, x=None) -> None:
         """Overwrite the resident iterate (None = zeros)."""
@@ -588,7 +588,7 @@ def _solve(system, cfg: SolverConfig, variant: str, *, x_ref=None, budget=None, 
             "ctas": int(r.ctas),
             "threads": int(r.threads),
             "plan": {"ep": int(r.plan_ep), "rows": int(r.plan_rows), "cluster": int(r.plan_cluster),
-                     "stages": int(r.plan_stages)},
+                     "stages": int(r.plan_stages), "waves": int(r.plan_waves)},
             "checkpoint_every": every,
         },
     )
