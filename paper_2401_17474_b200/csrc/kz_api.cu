@@ -2646,7 +2646,9 @@ extern "C" int32_t kz_solve_sharded(kz_system* s, kz_comm* comm, const kz_params
         args.use_stop = stop_mode ? 1 : 0;
         args.x_div = (double)Q;
     }
-    int64_t chunk = stop_mode ? 64 : chunk_max;
+    // chunks never exceed chunk_max: the row-index buffer holds chunk_cap iterations of draws and
+    // the error buffers chunk_max + 1 values
+    int64_t chunk = stop_mode ? std::min<int64_t>(64, chunk_max) : chunk_max;
     const int64_t ck_cap = (!comm && p->ckpt_every > 0) ? cx.n_ck_cap : 0;  // waves of one GPU: checkpoints
     if (ck_cap > 0 && fused) return fail(KZ_EINVAL, "checkpoints of the per-iteration rka loop");
     while (!xr && !converged && k < limit) {
