@@ -1399,7 +1399,8 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
         attr2[na].val.clusterDim.y = 1;
         attr2[na].val.clusterDim.z = 1;
         ++na;
-        if (pl.ctas > pl.cluster) {  // clusters poll each other: all must be co-resident
+        static const bool no_coop_rka = dbg_env("KZ_NO_COOP") != nullptr;  // experiments: ncu replay
+        if (pl.ctas > pl.cluster && !(no_coop_rka && pl.ctas <= s->sms)) {  // clusters poll each other: co-resident
             attr2[na].id = cudaLaunchAttributeCooperative;
             attr2[na].val.cooperative = 1;
             ++na;
