@@ -7,6 +7,8 @@ depend only on (seed, i, j), so these are exact crops of the 160000 x 20000 matr
   checkpointed (solvers.py:361-367 averaging) and compared at 1e-10.
 * RK and CK (q = 1) on a cluster of 4 CTAs at n = 4100, 8192, 20000: EP 8 / 16 with
   R 2 / 1 (solvers.py:294-310, 271-291), checkpoints every 100 iterations (T2).
+* BASELINE c4 at full shape (80000 x 2000 inconsistent): the horizon runs' iterates (RK, RKA
+  q = 64, q = 512) every 1000 iterations.
 """
 
 import numpy as np
@@ -106,3 +108,40 @@ def test_chain_limits_are_errors_not_crashes(gpu):
         ds.generate_counter(0)
         with pytest.raises(ValueError):
             run_solver(ds, SolverConfig(variant="rk"), budget=1)
+
+
+@pytest.fixture(scope="module")
+def c4_inconsistent():
+    """BASELINE c4: generate_mother(80000, 2000, seed 0), b_LS = b + xi (sysgen.py:175-176, noise seed 0),
+    x_LS by the device CGLS (pinned to the reference's CGLS in test_gpu_solves / test_host)."""
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, LinearSystem, generate_mother
+    from paper_2401_17474_b200.sysgen import inconsistent_rhs
+
+    s = generate_mother(GeneratorConfig(m_max=80000, n_max=2000, seed=0))
+    b_ls = inconsistent_rhs(s, 0)
+    inc = LinearSystem(A=s.A, b=b_ls, x_star=None, x_ls=None, consistent=False, seed=0)
+    ds = DeviceSystem(inc)
+    x_ls = ds.cgls(tol=1e-12)
+    yield ds, inc, x_ls
+    ds.close()
+
+
+@pytest.mark.parametrize("variant,q,budget", [("rk", 1, 120000), ("rka", 64, 60000), ("rka", 512, 48000)])
+def test_c4_horizon_iterates_match_oracle(gpu, oracle, c4_inconsistent, variant, q, budget):
+    """The full c4 horizon runs (80000 x 2000 inconsistent, the SURVEY 8(d) budgets, seed 0): the iterate every 1000
+    iterations against the oracle at 1e-10 (the bench's trace records are ||x - x_LS|| of these
+    iterates), and the distance to x_LS at the last checkpoint equal to the oracle's."""
+    from paper_2401_17474_b200 import SolverConfig, run_solver
+
+    ds, inc, x_ls = c4_inconsistent
+    cfg = SolverConfig(variant=variant, q=q, base_seed=0)
+    cap = []
+    r = run_solver(ds, cfg, budget=budget, checkpoint_every=1000, capture=cap)
+    o = oracle.solve(inc.A, inc.b, x_ls, variant=variant, q=q, base_seed=0, budget=budget, ckpt_every=1000,
+                     nthreads=oracle.max_threads())
+    assert r.iterations == budget and len(o["checkpoints"]) == budget // 1000 == len(cap)
+    for j, ck in enumerate(o["checkpoints"]):  # cap[j]: the iterate after 1000 (j + 1) iterations
+        assert rel_err(cap[j], ck) <= PARITY_TOL, (variant, q, j)
+    h_gpu = float(np.linalg.norm(cap[-1] - x_ls))
+    h_ora = float(np.linalg.norm(o["checkpoints"][-1] - x_ls))
+    assert abs(h_gpu - h_ora) <= 1e-8 * h_ora
