@@ -1570,7 +1570,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     if (pl.tma && pl.ctas > pl.cluster) {
         // tagged words of the rka kernel's cluster exchange (a buffer of their own; tags restart
         // at 1 every launch, so launch_step zeroes the words before each launch)
-        s->ll_words = 4 * (size_t)(pl.ctas / pl.cluster) * (pl.wg ? (size_t)s->ld : (size_t)(q + 1));
+        s->ll_words = (size_t)2 * (pl.ctas / pl.cluster) * (pl.wg ? 2 * (size_t)s->ld : (size_t)RKA_LL_PAD * (q + 1));
         KZ_TRY(s->ll.ensure(s->ll_words));
         KZ_CUDA(cudaMemsetAsync(&s->status.p->aborted, 0, sizeof(int), st));
     }
@@ -1609,8 +1609,8 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
     const bool phase_timing = dbg_env("KZ_PHASE_TIMING") != nullptr;
     args.ablate = dbg_env("KZ_ABLATE") ? atoi(dbg_env("KZ_ABLATE")) : 0;
     if (phase_timing) {
-        KZ_TRY(s->dbg.ensure(32 * 128 * 16));
-        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, 32 * 128 * 16 * sizeof(long long), st));
+        KZ_TRY(s->dbg.ensure(32 * 128 * 16 + 32768));
+        KZ_CUDA(cudaMemsetAsync(s->dbg.p, 0, (32 * 128 * 16 + 32768) * sizeof(long long), st));
         args.dbg = s->dbg.p;
     }
 
@@ -1942,6 +1942,36 @@ extern "C" int32_t kz_solve(kz_system* s, const kz_params* p, kz_result* r, doub
             }
             fprintf(stderr, "[kz clusters] %d clusters; iteration-start spread across clusters %.0f ns (mean)\n", G,
                     ns ? spread / ns : 0.0);
+            {  // every CTA's events (globaltimer): spread across CTAs and the latest CTA relative to the earliest
+                std::vector<long long> gg((size_t)32768);
+                KZ_CUDA(cudaMemcpy(gg.data(), s->dbg.p + 65536, gg.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+                const char* names[4] = {"dots done", "owner total", "cross-cluster sum", "scales arrived"};
+                double sp[4] = {0}, lat[4] = {0};
+                int nk2 = 0;
+                for (int k = 4; k < 31; ++k) {
+                    long long lo[4], hi[4];
+                    bool ok = true;
+                    for (int ev = 0; ev < 4; ++ev) {
+                        lo[ev] = -1, hi[ev] = -1;
+                        for (int c = 0; c < pl.ctas; ++c) {
+                            const long long t = gg[((size_t)c * 32 + k) * 4 + ev];
+                            if (!t) continue;
+                            lo[ev] = lo[ev] < 0 || t < lo[ev] ? t : lo[ev];
+                            hi[ev] = hi[ev] < 0 || t > hi[ev] ? t : hi[ev];
+                        }
+                        ok = ok && lo[ev] > 0;
+                    }
+                    if (!ok) continue;
+                    for (int ev = 0; ev < 4; ++ev) {
+                        sp[ev] += (double)(hi[ev] - lo[ev]);
+                        lat[ev] += (double)(hi[ev] - lo[0]);
+                    }
+                    ++nk2;
+                }
+                for (int ev = 0; ev < 4 && nk2; ++ev)
+                    fprintf(stderr, "[kz all CTAs] %-18s spread %6.0f ns, latest %6.0f ns after the earliest dots done\n",
+                            names[ev], sp[ev] / nk2, lat[ev] / nk2);
+            }
             const int ow = 6;
             for (int g = 0; g < G; ++g) {
                 double m[8] = {0};

@@ -283,6 +283,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         // slot [cluster][iteration][warp][16]
         const bool rec = TIMING && a.dbg != nullptr && cr == 0 && lane == 0 && kk < 32;
         long long* const stamp = TIMING ? a.dbg + ((size_t)(gid * 32 + kk) * 8 + warp) * 16 : nullptr;
+        // every CTA: globaltimer at 4 events of the iteration (dots done, owner total, cross-cluster sum,
+        // scales arrived), slot [65536 + (c * 32 + kk) * 4 + event]
+        const bool rec_all = TIMING && a.dbg != nullptr && lane == 0 && kk < 32;
+        long long* const gstamp = TIMING ? a.dbg + 65536 + ((size_t)c * 32 + kk) * 4 : nullptr;
         if (TIMING && rec) {
             stamp[0] = clock64();
             stamp[14] = (long long)globaltimer_ns();
@@ -350,6 +354,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             }
         }
         if (TIMING && rec) stamp[13] = clock64();
+        if (TIMING && rec_all && warp == 0) gstamp[0] = (long long)globaltimer_ns();
         // ---- error piece of x_k (needed only at the end of the iteration) -----------------
         if (want_check && warp == 0 && !(TIMING && (a.ablate & 1))) {
             double e2 = 0.0;
@@ -384,7 +389,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             // NOWN owner warps: warp ow takes the worker pairs ow, ow + NOWN, ... of this CTA
             const int ow = warp - (NW - NOWN);
             const unsigned tag = (unsigned)kk + 1u;  // the words are zeroed before every launch
-            unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * Gx * q1 * 2;
+            constexpr int lp = RKA_LL_PAD;  // u64 words per slot
+            unsigned long long* ll = reinterpret_cast<unsigned long long*>(a.part) + (size_t)par * Gx * q1 * lp;
             const int npair = (n_own + 1) / 2;
             const int my_pairs = npair > ow ? (npair - ow + NOWN - 1) / NOWN : 0;
             if (!last && my_pairs > 0) {
@@ -399,10 +405,12 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     double tot = owner_total(ib + i, RPO, live);
                     if (TIMING && rec && warp == NW - NOWN && l0 == 0)
                         stamp[10] = clock64() + (long long)(tot * 0.0);
+                    if (TIMING && rec_all && warp == NW - NOWN && l0 == 0)
+                        gstamp[1] = (long long)globaltimer_ns() + (long long)(tot * 0.0);
                     if (Gx > 1 && u == 0 && live) {
                         // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
-                        ll_store(ll + ((size_t)gx * q1 + t) * 2, tot, tag);
-                        tot = ll_sum<RKA_MAXG>(ll + 2 * t, 2 * q1, Gx, tag, &a.status->aborted);
+                        ll_store(ll + ((size_t)gx * q1 + t) * lp, tot, tag);
+                        tot = ll_sum<RKA_MAXG>(ll + lp * t, lp * q1, Gx, tag, &a.status->aborted);
                     }
                     if (live && u == 0) {
                         const double* rec4 = bsr + 4 * i;  // (b, sq, 1/sq, 0) of owned worker i
@@ -411,6 +419,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                         sout[i] = div_rn_fast(nume, rec4[1], rec4[2]);
                         if (TIMING && rec && warp == NW - NOWN && l0 == 0)
                             stamp[11] = clock64() + (long long)(sout[i] * 0.0);
+                        if (TIMING && rec_all && warp == NW - NOWN && l0 == 0)
+                            gstamp[2] = (long long)globaltimer_ns() + (long long)(sout[i] * 0.0);
                     }
                 }
                 __syncwarp();
@@ -434,8 +444,8 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 if (TIMING && rec) stamp[10] = clock64();
                 double tot = owner_total(ein + par * Pc, 1, lane < 2);
                 if (Gx > 1 && lane == 0) {
-                    ll_store(ll + ((size_t)gx * q1 + q) * 2, tot, tag);
-                    tot = ll_sum<RKA_MAXG>(ll + 2 * q, 2 * q1, Gx, tag, &a.status->aborted);
+                    ll_store(ll + ((size_t)gx * q1 + q) * lp, tot, tag);
+                    tot = ll_sum<RKA_MAXG>(ll + lp * q, lp * q1, Gx, tag, &a.status->aborted);
                 }
                 tot = __shfl_sync(0xffffffffu, tot, 0);
                 if (lane < Pc)
@@ -454,6 +464,7 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
         // ---- 4. scales arrive ------------------------------------------------------------
         mbar_wait(&sbar[par], bpar);
         if (TIMING && rec) stamp[3] = clock64();
+        if (TIMING && rec_all && warp == 0) gstamp[3] = (long long)globaltimer_ns();
         const double* sc = scal + par * q4;
         if (TIMING && rec) stamp[4] = clock64();
         // ---- 5. average over this warp's workers -----------------------------------------

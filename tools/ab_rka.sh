@@ -1,0 +1,6 @@
+#!/bin/bash
+# A/B of rka-kernel builds (wt_*/ and the working tree), alternating, on the c3 RKA and c4 q=512 shapes
+cd "$(dirname "$0")/.."
+for rep in 1 2; do for d in ${AB_DIRS:-$(ls -d wt_* 2>/dev/null) .}; do
+  echo "$d c3: $(python $d/tools/prof_case.py --m 160000 --n 20000 --gen counter --variant rka --q 64 --scheme distributed --budget 400 --solves 3 2>&1 | grep 'us/it' | sed 's/.*us\/it=//;s/ host.*//' | tr '\n' ' ')  c4q512: $(python $d/tools/prof_case.py --m 80000 --n 2000 --variant rka --q 512 --budget 500 --solves 2 2>&1 | grep 'us/it' | sed 's/.*us\/it=//;s/ host.*//' | tr '\n' ' ')"
+done; done
