@@ -256,6 +256,42 @@ __device__ __noinline__ double ll_sum(const unsigned long long* p, int stride, i
     return s;
 }
 
+// Lane-parallel twin of ll_sum: every lane polls ONE tagged word (act lanes; the others pass) until
+// all lanes of the warp hold theirs.  A thread's successive strong loads go out one after another
+// (B200, tools/mb_l2xchg.cu: 7 words polled by one lane ~5500 cycles per exchange round with 112
+// CTAs, one word per lane ~1650), so a sum over G clusters spreads its G polls over G lanes.
+// Warp-uniform call; the same spin bound and abort protocol as ll_sum.
+__device__ __forceinline__ double ll_poll_lane(const unsigned long long* p, bool act, unsigned tag, int* abort) {
+    unsigned long long w0 = 0, w1 = 0;
+    bool ok = !act;
+    if (act) {
+        ll_load_raw(p, w0, w1);
+        ok = ll_ok(w0, w1, tag);
+    }
+    unsigned spins = 0;
+    while (!__all_sync(0xffffffffu, ok)) {
+        ++spins;
+        if ((spins & 1023u) == 0 && *(volatile int*)abort) break;
+        if (spins > (1u << 22)) {
+            atomicExch(abort, 1);
+            break;
+        }
+        if (!ok) {
+            ll_load_raw(p, w0, w1);
+            ok = ll_ok(w0, w1, tag);
+        }
+    }
+    return act ? ll_value(w0, w1) : 0.0;
+}
+
+// The ordered sum v_0 + v_1 + ... + v_{G-1} of the values held by lanes base .. base + G - 1
+// (left to right, like ll_sum), returned to every lane of the group.  Warp-uniform G.
+__device__ __forceinline__ double ordered_group_sum(double v, int base, int G) {
+    double s = __shfl_sync(0xffffffffu, v, base);
+    for (int h = 1; h < G; ++h) s = __dadd_rn(s, __shfl_sync(0xffffffffu, v, base + h));
+    return s;
+}
+
 // inlined twin (no call ABI around it: the rka kernel's combine phase keeps many live registers)
 template <int GMAX, bool SYS = false>
 __device__ __forceinline__ double ll_sum_inl(const unsigned long long* p, int stride, int G, unsigned tag, int* abort) {

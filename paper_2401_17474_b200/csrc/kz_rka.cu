@@ -407,10 +407,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                         stamp[10] = clock64() + (long long)(tot * 0.0);
                     if (TIMING && rec_all && warp == NW - NOWN && l0 == 0)
                         gstamp[1] = (long long)globaltimer_ns() + (long long)(tot * 0.0);
-                    if (Gx > 1 && u == 0 && live) {
-                        // cluster totals -> tagged words [par][cluster][t]; sum over clusters in order
-                        ll_store(ll + ((size_t)gx * q1 + t) * lp, tot, tag);
-                        tot = ll_sum<RKA_MAXG>(ll + lp * t, lp * q1, Gx, tag, &a.status->aborted);
+                    if (Gx > 1) {
+                        // cluster totals -> tagged words [par][cluster][t] (summed in the pass below)
+                        if (u == 0 && live) ll_store(ll + ((size_t)gx * q1 + t) * lp, tot, tag);
+                        continue;
                     }
                     if (live && u == 0) {
                         const double* rec4 = bsr + 4 * i;  // (b, sq, 1/sq, 0) of owned worker i
@@ -421,6 +421,30 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                             stamp[11] = clock64() + (long long)(sout[i] * 0.0);
                         if (TIMING && rec_all && warp == NW - NOWN && l0 == 0)
                             gstamp[2] = (long long)globaltimer_ns() + (long long)(sout[i] * 0.0);
+                    }
+                }
+                if (Gx > 1) {
+                    // the clusters' totals of each item, LPI lanes per item (lane h polls cluster h's
+                    // word), added in cluster order; then the scale
+                    const int LPI = Gx <= 8 ? 8 : 16, ipr = 32 / LPI, h = lane & (LPI - 1);
+                    for (int j0 = 0; j0 < 2 * my_pairs; j0 += ipr) {
+                        const int li = j0 + lane / LPI;
+                        const int i = 2 * (ow + NOWN * (li >> 1)) + (li & 1);
+                        const bool live = li < 2 * my_pairs && i < n_own;
+                        const int t = my_lo + i;
+                        const double v = ll_poll_lane(ll + ((size_t)h * q1 + t) * lp, live && h < Gx, tag,
+                                                      &a.status->aborted);
+                        const double tot = ordered_group_sum(v, lane & ~(LPI - 1), Gx);
+                        if (live && h == 0) {
+                            const double* rec4 = bsr + 4 * i;  // (b, sq, 1/sq, 0) of owned worker i
+                            const double d = __dsub_rn(rec4[0], tot);
+                            const double nume = unit_alpha ? d : __dmul_rn(alp[t], d);  // 1 * d == d exactly
+                            sout[i] = div_rn_fast(nume, rec4[1], rec4[2]);
+                            if (TIMING && rec && warp == NW - NOWN && j0 == 0)
+                                stamp[11] = clock64() + (long long)(sout[i] * 0.0);
+                            if (TIMING && rec_all && warp == NW - NOWN && j0 == 0)
+                                gstamp[2] = (long long)globaltimer_ns() + (long long)(sout[i] * 0.0);
+                        }
                     }
                 }
                 __syncwarp();
@@ -443,9 +467,10 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 mbar_wait(&ebin[par], bpar);
                 if (TIMING && rec) stamp[10] = clock64();
                 double tot = owner_total(ein + par * Pc, 1, lane < 2);
-                if (Gx > 1 && lane == 0) {
-                    ll_store(ll + ((size_t)gx * q1 + q) * lp, tot, tag);
-                    tot = ll_sum<RKA_MAXG>(ll + lp * q, lp * q1, Gx, tag, &a.status->aborted);
+                if (Gx > 1) {  // lane h polls cluster h's error total; added in cluster order
+                    if (lane == 0) ll_store(ll + ((size_t)gx * q1 + q) * lp, tot, tag);
+                    const double v = ll_poll_lane(ll + ((size_t)lane * q1 + q) * lp, lane < Gx, tag, &a.status->aborted);
+                    tot = ordered_group_sum(v, 0, Gx);
                 }
                 tot = __shfl_sync(0xffffffffu, tot, 0);
                 if (lane < Pc)
