@@ -827,6 +827,7 @@ struct Plan {
     bool xr = false;    // rka kernel: cross-rank column sums (set per launch by kz_solve_sharded, not planned)
     bool delta = false; // chain: the threaded engine's RKA increments (chain_kernel<..., DELTA = true>)
     int waves = 1;      // chain: launches per outer iteration when the workers exceed the co-resident CTAs
+    bool wide = false;  // chain: averaged workers of 4 CTAs (chain_kernel<..., WIDE = true>)
     size_t smem = 0;
 };
 
@@ -854,7 +855,15 @@ void* rkw_fn(int epl) {
     return epl == 1 ? (void*)rkw_kernel<1, 8> : epl == 2 ? (void*)rkw_kernel<2, 8> : (void*)rkw_kernel<4, 8>;
 }
 
-void* chain_fn(int ep, int R, int C, bool delta = false) {
+void* chain_fn(int ep, int R, int C, bool delta = false, bool wide = false) {
+    if (wide) {  // averaged workers on clusters of 4 (RKAB rows beyond a pair's reach)
+        switch (C * 10000 + ep * 100 + R) {
+            case 40801: return (void*)chain_kernel<8, 1, 4, false, true>;
+            case 40802: return (void*)chain_kernel<8, 2, 4, false, true>;
+            case 41601: return (void*)chain_kernel<16, 1, 4, false, true>;
+            default: return nullptr;
+        }
+    }
     if (delta) {  // the threaded engine's RKA (one CTA per worker)
         switch (C * 10000 + ep * 100 + R) {
             case 10101: return (void*)chain_kernel<1, 1, 1, true>;
@@ -914,6 +923,7 @@ constexpr int MAXG_CLUSTERS = 10;  // = MAXG in kz_sync.cu
 
 // Chain-kernel plan for a worker of C CTAs (a thread-block cluster of C column slices).
 static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan& pl) {
+    pl.wide = q > 1 && C == 4;
     const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
     int ep = 0, T = 0;
@@ -942,7 +952,7 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     const int64_t stage_bytes = ldc * (int64_t)sizeof(double);
     int stages = 0;
     for (;;) {
-        while (R > 1 && !chain_fn(ep, R, C, pl.delta)) R /= 2;
+        while (R > 1 && !chain_fn(ep, R, C, pl.delta, pl.wide)) R /= 2;
         const int64_t fixed = chain_smem(ldc, 0, R, T, C);
         stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
         if (const char* e = dbg_env("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
@@ -951,9 +961,9 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     }
     if (stages < 1 || (size_t)chain_smem(ldc, stages, R, T, C) > kSmemLimit)
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
-    void* fn = chain_fn(ep, R, C, pl.delta);
+    void* fn = chain_fn(ep, R, C, pl.delta, pl.wide);
     // the instantiations carry one driver each for these shapes (kz_chain.cu ONE_CHAIN / AVERAGED)
-    if ((q == 1 && C == 2 && ep >= 8) || (q > 1 && C > 2))
+    if ((q == 1 && C == 2 && ep >= 8) || (q > 1 && C > 4))
         return fail(KZ_EINVAL, "no chain kernel drives q=%lld on %d-CTA workers with EP=%d", (long long)q, C, ep);
     if (!fn) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d C=%d", ep, R, C);
     pl.kernel = KZ_KERNEL_CHAIN;
@@ -1008,6 +1018,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     int cand[6], nc = 0;
     for (int c = C; c >= 1; c /= 2) cand[nc++] = c;
     if (q > 1 && C < 2 && !pl.delta) cand[nc++] = 2;
+    if (q > 1 && !pl.delta) cand[nc++] = 4;  // rows beyond a pair's reach: workers of 4 CTAs (in waves)
     for (int i = 0; i < nc; ++i) {
         const int c = cand[i];
         if (c > 1 && (s->ld % (2 * c) != 0 || s->no_pairs)) continue;  // whole 16-byte pairs
@@ -1372,7 +1383,7 @@ static int launch_solve(kz_system* s, const Plan& pl, SolveArgs& args, cudaStrea
     void* fn;
     cudaLaunchAttribute attr2[2];
     if (pl.kernel == KZ_KERNEL_CHAIN) {
-        fn = chain_fn(pl.ep, pl.rows, pl.pair, pl.delta);
+        fn = chain_fn(pl.ep, pl.rows, pl.pair, pl.delta, pl.wide);
         int na = 0;
         // KZ_NO_COOP (experiments): drop the cooperative attribute so a profiler can replay the
         // launch; safe only when every CTA fits at once (one per SM, ctas <= SMs)
@@ -1520,7 +1531,7 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         // the dynamic shared-memory limit is a property of the kernel function, which another
         // system may have lowered since: restore it for this plan
         void* fn = pl.kernel == KZ_KERNEL_WARP    ? rkw_fn(pl.ep)
-                   : pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair, pl.delta)
+                   : pl.kernel == KZ_KERNEL_CHAIN ? chain_fn(pl.ep, pl.rows, pl.pair, pl.delta, pl.wide)
                    : pl.tma                     ? rka_fn(pl.lg, pl.epl, pl.sr, pl.wg ? 1 : (pl.xr ? 2 : 0))
                                                 : sync_fn(pl.kernel == KZ_KERNEL_SYNC_CLUSTER, pl.lpr);
         KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
@@ -1545,6 +1556,9 @@ static int solve_setup(kz_system* s, const kz_params* p, kz_result* r, cudaStrea
         if (rc != KZ_OK) rc = plan_sync(s, p, q, kern == KZ_KERNEL_SYNC_CLUSTER, pl);
         if (rc != KZ_OK && kern == KZ_KERNEL_SYNC_CLUSTER && p->kernel == KZ_KERNEL_AUTO)
             rc = plan_sync(s, p, q, false, pl);
+        // more workers than the column-sliced kernels take (q > 512): one CTA (or pair) per worker
+        // on the chain kernel, in waves
+        if (rc != KZ_OK && p->kernel == KZ_KERNEL_AUTO) rc = plan_chain(s, p, q, pl);
         KZ_TRY(rc);
     } else {
         return fail(KZ_EINVAL, "unknown kernel selector %d", kern);

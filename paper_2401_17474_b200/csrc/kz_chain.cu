@@ -159,7 +159,7 @@ __device__ __forceinline__ void grid_barrier_c(unsigned* counter, unsigned targe
     named_sync(1, T);
 }
 
-template <int EP, int R, int C, bool DELTA>
+template <int EP, int R, int C, bool DELTA, bool WIDE>
 __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kernel(SolveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
@@ -546,8 +546,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     // never runs on a pair with EP >= 8 (rows of < 1536 columns) and workers averaged (q > 1)
     // never run on 4- or 8-CTA clusters.  Compiling the unused driver out leaves the register
     // allocator one loop to fit (the EP = 16 pair kernel then keeps v and the row without spilling).
-    constexpr bool ONE_CHAIN = !(C == 2 && EP >= 8);
-    constexpr bool AVERAGED = C <= 2;
+    // (WIDE: averaged workers of 4 CTAs each, RKAB on rows beyond a pair's 20480 columns)
+    constexpr bool ONE_CHAIN = !(C == 2 && EP >= 8) && !WIDE;
+    constexpr bool AVERAGED = C <= 2 || WIDE;
     if (ONE_CHAIN && (q == 1 || !AVERAGED)) {
         // one chain: outer iteration k = rows [k*bs, (k+1)*bs); x = v after each
         while (d < total) {
@@ -654,8 +655,9 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     }
 }
 
-#define KZ_CHAIN(EP, R, C) template __global__ void chain_kernel<EP, R, C, false>(SolveArgs);
-#define KZ_CHAIN_DELTA(EP, R) template __global__ void chain_kernel<EP, R, 1, true>(SolveArgs);
+#define KZ_CHAIN(EP, R, C) template __global__ void chain_kernel<EP, R, C, false, false>(SolveArgs);
+#define KZ_CHAIN_DELTA(EP, R) template __global__ void chain_kernel<EP, R, 1, true, false>(SolveArgs);
+#define KZ_CHAIN_WIDE(EP, R) template __global__ void chain_kernel<EP, R, 4, false, true>(SolveArgs);
 KZ_CHAIN(1, 1, 1)
 KZ_CHAIN(1, 4, 1)
 KZ_CHAIN(2, 1, 1)
@@ -693,7 +695,12 @@ KZ_CHAIN_DELTA(4, 4)
 KZ_CHAIN_DELTA(8, 1)
 KZ_CHAIN_DELTA(8, 2)
 KZ_CHAIN_DELTA(16, 1)
+// averaged workers on clusters of 4 (RKAB with 20480 < n <= 40960)
+KZ_CHAIN_WIDE(8, 1)
+KZ_CHAIN_WIDE(8, 2)
+KZ_CHAIN_WIDE(16, 1)
 #undef KZ_CHAIN
 #undef KZ_CHAIN_DELTA
+#undef KZ_CHAIN_WIDE
 
 }  // namespace kz

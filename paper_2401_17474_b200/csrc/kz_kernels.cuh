@@ -78,7 +78,7 @@ enum {
 
 // chain kernel: worker-per-CTA (RK, RKAB).  EP = 16-byte pairs per thread,
 // R = rows resolved per CTA reduction (Gram-corrected block), C = CTAs per worker.
-template <int EP, int R, int C, bool DELTA = false>
+template <int EP, int R, int C, bool DELTA = false, bool WIDE = false>
 __global__ void chain_kernel(SolveArgs a);
 
 // one-warp RK / CK kernel for short rows (n <= 64 EPL); P rows prefetched in registers

@@ -68,3 +68,37 @@ def test_rka_on_chain_in_waves(gpu, oracle):
     assert rel_err(r.x, o["x"]) <= PARITY_TOL
     for j, ck in enumerate(o["checkpoints"]):
         assert rel_err(cap[j], ck) <= PARITY_TOL, j
+
+
+def test_rka_beyond_512_workers(gpu, oracle):
+    """RKA with q = 600: past the column-sliced kernels' 512 workers, the chain kernel in waves."""
+    from paper_2401_17474_b200 import DeviceSystem, GeneratorConfig, SolverConfig, generate_mother, solve_rka_seq
+
+    s = generate_mother(GeneratorConfig(m_max=8000, n_max=600, seed=6))
+    cfg = SolverConfig(variant="rka", q=600, base_seed=2, max_iterations=800)
+    with DeviceSystem(s) as ds:
+        r = solve_rka_seq(ds, cfg)
+    assert r.gpu["kernel"] == "chain", r.gpu
+    o = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=600, base_seed=2, max_iterations=800,
+                     nthreads=oracle.max_threads())
+    assert r.iterations == o["iterations"] and rel_err(r.x, o["x"]) <= PARITY_TOL
+
+
+def test_rkab_rows_beyond_a_pair(gpu, oracle):
+    """RKAB on n = 24000 (> 2 x 10240 columns): workers of 4 CTAs (chain_kernel<16, 1, 4, WIDE>),
+    16 workers -> 64 CTAs; q = 48 -> 192 CTAs in waves; a counter-keyed crop, every outer iteration."""
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, solve_rkab_seq
+
+    with DeviceSystem(m=24000, n=24000) as ds:
+        ds.generate_counter(0)
+        A, b, xr = ds.download()
+        for q in (16, 48):
+            cfg = SolverConfig(variant="rkab", q=q, block_size=30, base_seed=3, sampling_scheme="distributed")
+            cap = []
+            r = solve_rkab_seq(ds, cfg, budget=2, capture=cap)
+            assert r.gpu["plan"]["cluster"] == 4, r.gpu
+            assert (r.gpu["plan"]["waves"] > 1) == (q == 48), r.gpu
+            o = oracle.solve(A, b, xr, variant="rkab", q=q, block_size=30, base_seed=3, scheme="distributed",
+                             budget=2, ckpt_every=1, nthreads=oracle.max_threads())
+            for j, ck in enumerate(o["checkpoints"]):
+                assert rel_err(cap[j], ck) <= PARITY_TOL, (q, j)
