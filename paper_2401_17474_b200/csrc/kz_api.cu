@@ -861,6 +861,9 @@ void* chain_fn(int ep, int R, int C, bool delta = false, bool wide = false) {
             case 40801: return (void*)chain_kernel<8, 1, 4, false, true>;
             case 40802: return (void*)chain_kernel<8, 2, 4, false, true>;
             case 41601: return (void*)chain_kernel<16, 1, 4, false, true>;
+            case 80801: return (void*)chain_kernel<8, 1, 8, false, true>;
+            case 80802: return (void*)chain_kernel<8, 2, 8, false, true>;
+            case 81601: return (void*)chain_kernel<16, 1, 8, false, true>;
             default: return nullptr;
         }
     }
@@ -905,6 +908,9 @@ void* chain_fn(int ep, int R, int C, bool delta = false, bool wide = false) {
         case 41601: return (void*)chain_kernel<16, 1, 4>;
         case 80104: return (void*)chain_kernel<1, 4, 8>;
         case 80204: return (void*)chain_kernel<2, 4, 8>;
+        case 80801: return (void*)chain_kernel<8, 1, 8>;
+        case 80802: return (void*)chain_kernel<8, 2, 8>;
+        case 81601: return (void*)chain_kernel<16, 1, 8>;
         default: return nullptr;
     }
 }
@@ -923,7 +929,7 @@ constexpr int MAXG_CLUSTERS = 10;  // = MAXG in kz_sync.cu
 
 // Chain-kernel plan for a worker of C CTAs (a thread-block cluster of C column slices).
 static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan& pl) {
-    pl.wide = q > 1 && C == 4;
+    pl.wide = q > 1 && C >= 4;
     const int64_t pairs = s->ld / 2 / C;
     auto round32 = [](int64_t t) { return (int)std::max<int64_t>(32, (t + 31) / 32 * 32); };
     int ep = 0, T = 0;
@@ -963,7 +969,7 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
     void* fn = chain_fn(ep, R, C, pl.delta, pl.wide);
     // the instantiations carry one driver each for these shapes (kz_chain.cu ONE_CHAIN / AVERAGED)
-    if ((q == 1 && C == 2 && ep >= 8) || (q > 1 && C > 4))
+    if (q == 1 && C == 2 && ep >= 8)
         return fail(KZ_EINVAL, "no chain kernel drives q=%lld on %d-CTA workers with EP=%d", (long long)q, C, ep);
     if (!fn) return fail(KZ_EINVAL, "no chain kernel for EP=%d R=%d C=%d", ep, R, C);
     pl.kernel = KZ_KERNEL_CHAIN;
@@ -1019,6 +1025,7 @@ static int plan_chain(kz_system* s, const kz_params* p, int64_t q, Plan& pl) {
     for (int c = C; c >= 1; c /= 2) cand[nc++] = c;
     if (q > 1 && C < 2 && !pl.delta) cand[nc++] = 2;
     if (q > 1 && !pl.delta) cand[nc++] = 4;  // rows beyond a pair's reach: workers of 4 CTAs (in waves)
+    if (!pl.delta) cand[nc++] = 8;           // and of 8 CTAs (one chain, or averaged workers in waves)
     for (int i = 0; i < nc; ++i) {
         const int c = cand[i];
         if (c > 1 && (s->ld % (2 * c) != 0 || s->no_pairs)) continue;  // whole 16-byte pairs

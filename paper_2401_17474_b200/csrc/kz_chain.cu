@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     // never runs on a pair with EP >= 8 (rows of < 1536 columns) and workers averaged (q > 1)
     // never run on 4- or 8-CTA clusters.  Compiling the unused driver out leaves the register
     // allocator one loop to fit (the EP = 16 pair kernel then keeps v and the row without spilling).
-    // (WIDE: averaged workers of 4 CTAs each, RKAB on rows beyond a pair's 20480 columns)
+    // (WIDE: averaged workers of 4 or 8 CTAs each, RKAB on rows beyond a pair's 20480 columns)
     constexpr bool ONE_CHAIN = !(C == 2 && EP >= 8) && !WIDE;
     constexpr bool AVERAGED = C <= 2 || WIDE;
     if (ONE_CHAIN && (q == 1 || !AVERAGED)) {
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
 
 #define KZ_CHAIN(EP, R, C) template __global__ void chain_kernel<EP, R, C, false, false>(SolveArgs);
 #define KZ_CHAIN_DELTA(EP, R) template __global__ void chain_kernel<EP, R, 1, true, false>(SolveArgs);
-#define KZ_CHAIN_WIDE(EP, R) template __global__ void chain_kernel<EP, R, 4, false, true>(SolveArgs);
+#define KZ_CHAIN_WIDE(EP, R, C) template __global__ void chain_kernel<EP, R, C, false, true>(SolveArgs);
 KZ_CHAIN(1, 1, 1)
 KZ_CHAIN(1, 4, 1)
 KZ_CHAIN(2, 1, 1)
@@ -684,6 +684,9 @@ KZ_CHAIN(8, 2, 4)
 KZ_CHAIN(16, 1, 4)
 KZ_CHAIN(1, 4, 8)
 KZ_CHAIN(2, 4, 8)
+KZ_CHAIN(8, 1, 8)
+KZ_CHAIN(8, 2, 8)
+KZ_CHAIN(16, 1, 8)
 // the threaded engine's RKA (one CTA per worker)
 KZ_CHAIN_DELTA(1, 1)
 KZ_CHAIN_DELTA(1, 4)
@@ -695,10 +698,13 @@ KZ_CHAIN_DELTA(4, 4)
 KZ_CHAIN_DELTA(8, 1)
 KZ_CHAIN_DELTA(8, 2)
 KZ_CHAIN_DELTA(16, 1)
-// averaged workers on clusters of 4 (RKAB with 20480 < n <= 40960)
-KZ_CHAIN_WIDE(8, 1)
-KZ_CHAIN_WIDE(8, 2)
-KZ_CHAIN_WIDE(16, 1)
+// averaged workers on clusters of 4 or 8 (RKAB with 20480 < n <= 81920)
+KZ_CHAIN_WIDE(8, 1, 4)
+KZ_CHAIN_WIDE(8, 2, 4)
+KZ_CHAIN_WIDE(16, 1, 4)
+KZ_CHAIN_WIDE(8, 1, 8)
+KZ_CHAIN_WIDE(8, 2, 8)
+KZ_CHAIN_WIDE(16, 1, 8)
 #undef KZ_CHAIN
 #undef KZ_CHAIN_DELTA
 #undef KZ_CHAIN_WIDE

@@ -104,10 +104,12 @@ def test_chain_limits_are_errors_not_crashes(gpu):
     (KZ_EINVAL) instead of failing inside a launch."""
     from paper_2401_17474_b200 import DeviceSystem, SolverConfig, run_solver
 
-    with DeviceSystem(m=64, n=41000) as ds:
+    with DeviceSystem(m=64, n=82000) as ds:  # past one chain of 8 CTAs (81920 columns)
         ds.generate_counter(0)
         with pytest.raises(ValueError):
             run_solver(ds, SolverConfig(variant="rk"), budget=1)
+        with pytest.raises(ValueError):
+            run_solver(ds, SolverConfig(variant="rkab", q=4, block_size=2), budget=1)
 
 
 @pytest.fixture(scope="module")
@@ -145,3 +147,27 @@ def test_c4_horizon_iterates_match_oracle(gpu, oracle, c4_inconsistent, variant,
     h_gpu = float(np.linalg.norm(cap[-1] - x_ls))
     h_ora = float(np.linalg.norm(o["checkpoints"][-1] - x_ls))
     assert abs(h_gpu - h_ora) <= 1e-8 * h_ora
+
+
+def test_rows_beyond_40960_columns(gpu, oracle):
+    """n = 50000: RK on one chain of 8 CTAs (chain_kernel<16, 1, 8>) and RKAB on workers of 8 CTAs
+    (WIDE) against the oracle (a 4000-row crop of the counter-keyed generator: the loop does not
+    need m >= n)."""
+    from paper_2401_17474_b200 import SolverConfig, run_solver
+
+    ds, A, b, xr = _crop(4000, 50000)
+    with ds:
+        cap = []
+        r = run_solver(ds, SolverConfig(variant="rk", base_seed=4), budget=300, capture=cap)
+        assert r.gpu["plan"]["cluster"] == 8, r.gpu
+        o = oracle.solve(A, b, xr, variant="rk", base_seed=4, budget=300, ckpt_every=50)
+        for j, ck in enumerate(o["checkpoints"]):
+            assert rel_err(cap[50 * (j + 1) - 1], ck) <= PARITY_TOL, j
+        cap = []
+        cfg = SolverConfig(variant="rkab", q=6, block_size=20, base_seed=1, sampling_scheme="distributed")
+        r = run_solver(ds, cfg, budget=2, capture=cap)
+        assert r.gpu["plan"]["cluster"] == 8, r.gpu
+        o = oracle.solve(A, b, xr, variant="rkab", q=6, block_size=20, base_seed=1, scheme="distributed", budget=2,
+                         ckpt_every=1)
+        for j, ck in enumerate(o["checkpoints"]):
+            assert rel_err(cap[j], ck) <= PARITY_TOL, j
