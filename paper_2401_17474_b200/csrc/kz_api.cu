@@ -836,8 +836,9 @@ int chain_max_threads(int ep) { return ep <= 8 ? 128 : 320; }  // compute thread
 
 int chain_nv(int R) { return R + R * (R - 1) / 2 + R + 1; }
 
-int chain_smem(int64_t ldc, int stages, int R, int T, int C = 2) {
-    return (int)(288 + (2 * std::max(C, 1) * chain_nv(R) + 2) * sizeof(double) + stages * ldc * sizeof(double) +
+// ldr: the ring row pitch, 2 EP T columns (kz_chain.cu)
+int chain_smem(int64_t ldr, int stages, int R, int T, int C = 2) {
+    return (int)(288 + (2 * std::max(C, 1) * chain_nv(R) + 2) * sizeof(double) + stages * ldr * sizeof(double) +
                  stages * 2 * sizeof(double) + IDX_WINDOW * sizeof(int32_t) +
                  ((size_t)chain_nv(R) * T + chain_nv(R) + 1) * sizeof(double));
 }
@@ -954,18 +955,18 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     if (C == 2) R = std::min(R, 4);
     if (C > 2) R = std::min(R, 4);
     if (const char* e = dbg_env("KZ_CHAIN_ROWS")) R = std::max(1, atoi(e));
-    const int64_t ldc = s->ld / C;
-    const int64_t stage_bytes = ldc * (int64_t)sizeof(double);
+    const int64_t ldr = ep < 16 ? 2 * (int64_t)ep * T : s->ld / C;  // ring row pitch (kz_chain.cu PADDED)
+    const int64_t stage_bytes = ldr * (int64_t)sizeof(double);
     int stages = 0;
     for (;;) {
         while (R > 1 && !chain_fn(ep, R, C, pl.delta, pl.wide)) R /= 2;
-        const int64_t fixed = chain_smem(ldc, 0, R, T, C);
+        const int64_t fixed = chain_smem(ldr, 0, R, T, C);
         stages = (int)std::min<int64_t>(16, ((int64_t)200 * 1024 - fixed) / stage_bytes);
         if (const char* e = dbg_env("KZ_CHAIN_STAGES")) stages = std::min(16, atoi(e));
         if (stages >= R + 1 || R == 1) break;
         R = R > 4 ? 4 : (R > 2 ? 2 : 1);
     }
-    if (stages < 1 || (size_t)chain_smem(ldc, stages, R, T, C) > kSmemLimit)
+    if (stages < 1 || (size_t)chain_smem(ldr, stages, R, T, C) > kSmemLimit)
         return fail(KZ_EINVAL, "row of n=%lld does not fit the shared-memory ring", (long long)s->n);
     void* fn = chain_fn(ep, R, C, pl.delta, pl.wide);
     // the instantiations carry one driver each for these shapes (kz_chain.cu ONE_CHAIN / AVERAGED)
@@ -978,7 +979,7 @@ static int plan_chain_c(kz_system* s, const kz_params* p, int64_t q, int C, Plan
     pl.rows = R;
     pl.pair = C;
     pl.stages = stages;
-    pl.smem = chain_smem(ldc, stages, R, T, C);
+    pl.smem = chain_smem(ldr, stages, R, T, C);
     pl.ctas = (int)(q * C);
     KZ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     pl.waves = 1;

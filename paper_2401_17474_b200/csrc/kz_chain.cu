@@ -173,6 +173,12 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     const int h = (C >= 2) ? (int)cluster_rank() : 0;
     const int ldc = (int)(ld / C);  // this CTA's columns [cb, cb + ldc): 32-bit offsets within the slice
     const int64_t cb = (int64_t)h * ldc;
+    // ring row pitch: for EP < 16 every thread's EP pairs (2 EP T columns >= ldc), the tail past ldc
+    // zero, so the row loops read and update without a bounds test (v stays 0 past ldc: s * 0):
+    // c2 166 -> 153 us per outer iteration, c4-shape RKAB 748 -> 700.  EP = 16 keeps the exact
+    // pitch: its tail (2.4 % at c3) costs more shared-memory traffic than the tests do.
+    constexpr bool PADDED = EP < 16;
+    const int ldr = PADDED ? 2 * EP * T : ldc;
     ChainSmem sm;
     unsigned long long* xbar = reinterpret_cast<unsigned long long*>(smem_raw);  // 2 exchange mbarriers
     unsigned long long* full = xbar + 2;                                         // 16 row-stage mbarriers
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     volatile int* halt = reinterpret_cast<volatile int*>(smem_raw + 272);        // compute done
     double* xbuf = reinterpret_cast<double*>(smem_raw + 288);                     // 2 x C x NVC peer totals
     sm.ring = xbuf + 2 * C * Blk<R>::NVC + 2;
-    sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ldc);
+    sm.bsq = reinterpret_cast<double2*>(sm.ring + (size_t)D * ldr);
     sm.win = reinterpret_cast<int32_t*>(sm.bsq + D);
     sm.scr = reinterpret_cast<double*>(sm.win + IDX_WINDOW);
     sm.tot = sm.scr + (size_t)Blk<R>::NVC * T;
@@ -194,6 +200,8 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         *halt = 0;
         fence_mbarrier_init_cluster();
     }
+    for (int k = 0; k < D; ++k)  // the ring rows' zero tails (TMA never writes them)
+        for (int j = ldc + tid; j < ldr; j += blockDim.x) sm.ring[(size_t)k * ldr + j] = 0.0;
     __syncthreads();
     if (C >= 2) cluster_sync_all();
     int nex = 0;  // cluster exchanges done
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                     cp_async16(sm.bsq + st, bs2 + 2 * i);
                     cp_async_mbar_arrive(&full[st]);
                     mbar_arrive_expect_tx(&full[st], row_bytes);
-                    bulk_g2s(sm.ring + (size_t)st * ldc, a.A + i * ld + cb, row_bytes, &full[st]);
+                    bulk_g2s(sm.ring + (size_t)st * ldr, a.A + i * ld + cb, row_bytes, &full[st]);
                 }
                 __syncwarp();
                 j = jl + 1;  // rows issued
@@ -383,20 +391,20 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 for (int p = 0; p < EP; ++p) {
                     const int lc = 2 * (p * T + tid);
                     rr[r][p < EPK ? p : 0] =
-                        (r < Rp && lc < ldc) ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldc + lc)
+                        (r < Rp && (PADDED || lc < ldc)) ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldr + lc)
                                              : make_double2(0.0, 0.0);
                 }
         }
         auto row = [&](int r, int p) -> double2 {  // the dot's read
             if constexpr (KEEP_ROW) return rr[r][p < EPK ? p : 0];
             const int lc = 2 * (p * T + tid);
-            return r < Rp ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldc + lc)
+            return r < Rp ? *reinterpret_cast<const double2*>(sm.ring + (size_t)stg[r] * ldr + lc)
                           : make_double2(0.0, 0.0);
         };
         auto row_again = [&](int r, int p) -> double2 {  // the update's read
             if constexpr (KEEP_ROW) return rr[r][p < EPK ? p : 0];
             const int lc = 2 * (p * T + tid);
-            return lds_reread_f64x2(sm.ring + (size_t)stg[r] * ldc + lc);
+            return lds_reread_f64x2(sm.ring + (size_t)stg[r] * ldr + lc);
         };
         double2 bq = make_double2(0.0, 1.0);
         if (lane < Rp) {
@@ -415,7 +423,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         for (int p = 0; p < EP; ++p) {
             const int lc = 2 * (p * T + tid);
             const int64_t col = cb + lc;
-            if (lc < ldc) {
+            if ((PADDED && !CHECK) || lc < ldc) {  // the stop-rule terms read x_ref: bounded
                 const double vx = v[2 * p], vy = v[2 * p + 1];
 #pragma unroll
                 double2 ar[R];
@@ -496,7 +504,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
 #pragma unroll
                 for (int p = 0; p < EP; ++p) {
                     const int lc = 2 * (p * T + tid);
-                    if (lc < ldc) {
+                    if (PADDED || lc < ldc) {  // padded: the zero tail leaves v past ldc at 0
                         const double2 ap = row_again(r, p);
                         v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], ap.x));
                         v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], ap.y));
