@@ -210,7 +210,12 @@ typedef struct {
     int32_t pad;
 } kz_result;
 
-/* Full solve with host output x_host (n values, may be NULL). */
+/* Full solve with host output x_host (n values, may be NULL): the _drive protocol
+ * (solvers.py:182-263) of solve_rk / solve_rka_seq / solve_rkab_seq / solve_ck
+ * (solvers.py:271-371).  Any q: workers beyond the CTAs the GPU holds at once run
+ * in waves per outer iteration (kz_result.plan_waves), bit-identical to one launch;
+ * rows up to 81920 columns on the chain kernel (RK, CK, RKAB), any width for RKA.
+ * Trace mode needs the workers co-resident (KZ_EINVAL otherwise). */
 KZ_API int32_t kz_solve(kz_system* sys, const kz_params* params, kz_result* result, double* x_host, void* stream);
 /* The seeds of one RK configuration (seeds[S]) solved side by side in one launch per chunk:
  * one warp per seed on short rows (n <= 256), each with its own iterate, row draws
