@@ -641,6 +641,50 @@ def solve_rkab_parallel(system, cfg: SolverConfig, *, x_ref=None, budget=None, c
     return dataclasses.replace(r, barrier_events=2 * (r.iterations + 1)) if budget is None else r
 
 
+def solve_rk_block_sequential(system, cfg: SolverConfig, *, x_ref=None, budget=None, capture=None,
+                              checkpoint_every=None) -> RunReport:
+    """RK with the work of each iteration split over q workers (parallel.py:307-368): one sampling
+    stream, one row per iteration, partial inner products over column slices combined in a fixed
+    order -- the iterate sequence of solve_rk (bitwise at q = 1 in the reference, <= 1e-12
+    otherwise, test_parallel.py:7-24).  On the B200 every RK solve already splits each row over the
+    CTA's threads (or 4 / 8 CTAs) with a fixed reduction order, so this is solve_rk after the
+    reference's validation (q <= n)."""
+    cfg.validate()
+    n = system.n if isinstance(system, DeviceSystem) else system.A.shape[1]
+    if cfg.q > n:
+        raise ValueError(f"q={cfg.q} workers exceed n={n} columns")
+    return solve_rk(system, cfg.replace(q=1), x_ref=x_ref, budget=budget, capture=capture,
+                    checkpoint_every=checkpoint_every)
+
+
+@dataclass(frozen=True)
+class RowNormCache:
+    """Squared row norms and their total (linalg.py:64-78), computed on the device."""
+
+    sq_norms: np.ndarray
+    frobenius_sq: float
+
+    @property
+    def m(self) -> int:
+        return self.sq_norms.shape[0]
+
+
+def row_norm_cache(a) -> RowNormCache:
+    """linalg.py:80-88 on the device: np.einsum("ij,ij->i") order bit for bit (kz_row_norms),
+    DegenerateRowError on a zero row; ``a`` is a host matrix or a DeviceSystem."""
+    if isinstance(a, DeviceSystem):
+        sq = a.row_norms()
+    else:
+        A = np.ascontiguousarray(a, dtype=np.float64)
+        if A.ndim != 2:
+            raise DimensionMismatchError(f"expected a 2-D matrix, got ndim={A.ndim}")
+        with DeviceSystem(m=A.shape[0], n=A.shape[1]) as ds:
+            ds.upload(A, np.zeros(A.shape[0]))
+            sq = ds.row_norms()
+    sq.flags.writeable = False
+    return RowNormCache(sq_norms=sq, frobenius_sq=float(sq.sum()))
+
+
 def _run_cgls(system, cfg, x_ref):
     """harness._run_cgls (harness.py:72-95): CGLS on the device (kz_cgls)."""
     import time

@@ -104,3 +104,27 @@ def test_narrow_rows_every_variant(gpu, oracle, n):
                              variant=kw["variant"], max_iterations=200000)
             assert r.iterations == o["iterations"] and r.converged == o["converged"], (n, kw)
             assert rel_err(r.x, o["x"]) <= PARITY_TOL, (n, kw)
+
+
+def test_row_norm_cache_and_block_sequential(gpu, systems, oracle):
+    """row_norm_cache (linalg.py:80-88) on the device: numpy's einsum bit for bit, the total, the
+    zero-row error; solve_rk_block_sequential (parallel.py:307-368) is RK's iterate sequence and
+    rejects more workers than columns (test_parallel.py:7-30)."""
+    from paper_2401_17474_b200 import DegenerateRowError, SolverConfig, row_norm_cache, solve_rk
+    from paper_2401_17474_b200 import solve_rk_block_sequential
+
+    s = systems["s500"]
+    c = row_norm_cache(s.A)
+    assert np.array_equal(c.sq_norms, np.einsum("ij,ij->i", s.A, s.A)) and c.m == s.A.shape[0]
+    assert c.frobenius_sq == float(np.einsum("ij,ij->i", s.A, s.A).sum())
+    A0 = s.A.copy()
+    A0[7] = 0.0
+    with pytest.raises(DegenerateRowError) as exc:
+        row_norm_cache(A0)
+    assert exc.value.row == 7
+    rk = solve_rk(s, SolverConfig(variant="rk", base_seed=3))
+    for q in (1, 4):
+        par = solve_rk_block_sequential(s, SolverConfig(variant="rk", q=q, base_seed=3))
+        assert par.iterations == rk.iterations and np.array_equal(par.x, rk.x)
+    with pytest.raises(ValueError):
+        solve_rk_block_sequential(s, SolverConfig(variant="rk", q=s.n + 1, base_seed=0))
