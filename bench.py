@@ -471,6 +471,35 @@ def extra_workloads(device, peak, steps=3):
                                                        device=device), 400,
                     "c3: 160000x20000 counter-keyed, RKA q=64 (bs=1) distributed, 400 iterations per step")
 
+    def c3_sharded_protocol():
+        # the multi-GPU protocol at one rank: per outer iteration the local chain-kernel step, an
+        # in-place NCCL all-reduce (a one-rank communicator) and x = S / Q, against kz_solve's
+        # in-kernel average -- the per-iteration cost the N-GPU bench adds to the same local work
+        from paper_2401_17474_b200.multigpu import CudaShard, ShardComm, plan_shards, solve_sharded_native
+
+        plan = plan_shards(C3_M, 1, 0, C3_Q)
+        shard = CudaShard.counter(C3_M, C3_N, plan, C3_SEED, device)
+        comm = ShardComm(device, 1, 0)
+        try:
+            cfg = SolverConfig(variant="rkab", q=C3_Q, block_size=C3_BS, sampling_scheme="distributed",
+                               device=device)
+            budget = 100
+            solve_sharded_native(shard, cfg, budget=budget, comm=comm)  # warm-up
+            loop = [solve_sharded_native(shard, cfg.replace(base_seed=k), budget=budget, comm=comm) for k in range(2)]
+            solo = [solve_sharded_native(shard, cfg.replace(base_seed=k), budget=budget) for k in range(2)]
+            same = all(np.array_equal(a.x, b.x) for a, b in zip(loop, solo))
+            lms = float(np.mean([r.gpu["loop_ms"] for r in loop])) / budget
+            sms = float(np.mean([r.gpu["loop_ms"] for r in solo])) / budget
+            out.append({"workload": "c3_sharded_protocol_world1",
+                        "desc": "c3 RKAB q=64 bs=1000, 100-iteration replays: the row-sharded protocol at one rank "
+                                "(per iteration: chain step, NCCL all-reduce, average kernel) vs kz_solve's in-kernel "
+                                "average",
+                        "ms_per_iteration_protocol": lms, "ms_per_iteration_in_kernel": sms,
+                        "protocol_overhead": lms / sms - 1.0, "x_bitwise_equal": same})
+        finally:
+            shard.close()
+            comm.close()
+
     def c4():
         s4 = generate_mother(GeneratorConfig(m_max=80000, n_max=2000, seed=0))
         with DeviceSystem(s4, device=device) as ds:
@@ -568,7 +597,7 @@ def extra_workloads(device, peak, steps=3):
                         "ms_per_step": best[0].gpu["loop_ms"], "iterations": [r.iterations for r in best],
                         "converged": [r.converged for r in best], "kernel": "warp"})
 
-    for fn in (c3_rka, c4, c2, c1, c0):
+    for fn in (c3_rka, c3_sharded_protocol, c4, c2, c1, c0):
         guarded(fn)
     return out
 
