@@ -28,7 +28,9 @@
 //          DSMEM hops carrying q values each instead of an all-to-all of q x Pc.
 //          With G > 1 clusters the owners first exchange their cluster totals
 //          as tagged 64-bit words (value halves + iteration tag, single-copy
-//          atomic; no grid barrier, no fence) and add them in cluster order;
+//          atomic; no grid barrier, no fence; one 128-byte L2 line per slot),
+//          polled one word per lane (a thread's strong loads go out one after
+//          another), and add them in cluster order;
 //       4. stop rule on the broadcast error total;
 //       5. average: each warp sums fl(x + fl(s_t a_t)) over its block; the 8
 //          per-warp sums meet in shared memory behind one named barrier and
