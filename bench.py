@@ -524,9 +524,14 @@ def extra_workloads(device, peak, steps=3):
             for q, budget in ((1, 120000), (64, 60000), (512, 48000)):
                 cfg = SolverConfig(variant="rka" if q > 1 else "rk", q=q, device=device, max_iterations=budget)
                 cfgs = [cfg.replace(base_seed=k) for k in range(SEEDS)]
+                lanes = 1 if q > 64 else SEEDS
+                # warm-up (untimed): the lanes' system views, streams and samplers are built on first use
+                solve_concurrent(ds, [c.replace(max_iterations=2000) for c in cfgs], lanes=lanes, x_ref=x_ls,
+                                 trace_step=1000)
+                torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                rs = solve_concurrent(ds, cfgs, lanes=1 if q > 64 else SEEDS, x_ref=x_ls, trace_step=1000)
+                rs = solve_concurrent(ds, cfgs, lanes=lanes, x_ref=x_ls, trace_step=1000)
                 e1.record()
                 torch.cuda.synchronize()
                 wall_ms = e0.elapsed_time(e1)
