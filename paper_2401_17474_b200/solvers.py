@@ -434,7 +434,13 @@ class DeviceSystem:
 # allocator): every call still uploads A, b, x_ref and recomputes the row norms
 # and sampler, like the reference's per-call row_norm_cache (solvers.py:299).
 _POOL: dict[tuple[int, int, int], list[DeviceSystem]] = {}
-_POOL_MAX_BYTES = 8 << 30
+# the pool keeps at most one system per shape and this many bytes of matrices in total (the B200's
+# 180 GB hold a c3-size 25.6 GB system with room to spare); release_pool() frees them
+_POOL_MAX_BYTES = 64 << 30
+
+
+def _pool_bytes() -> int:
+    return sum(d.m * d.n * 8 for lst in _POOL.values() for d in lst)
 
 
 def _pool_acquire(system: LinearSystem, device: int) -> DeviceSystem:
@@ -454,7 +460,7 @@ def _pool_acquire(system: LinearSystem, device: int) -> DeviceSystem:
 
 def _pool_release(ds: DeviceSystem) -> None:
     ds.host = None
-    if ds.m * ds.n * 8 <= _POOL_MAX_BYTES and not _POOL.get((ds.m, ds.n, ds.device)):
+    if not _POOL.get((ds.m, ds.n, ds.device)) and _pool_bytes() + ds.m * ds.n * 8 <= _POOL_MAX_BYTES:
         _POOL.setdefault((ds.m, ds.n, ds.device), []).append(ds)
     else:
         ds.close()
