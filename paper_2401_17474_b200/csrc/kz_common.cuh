@@ -257,10 +257,9 @@ __device__ __noinline__ double ll_sum(const unsigned long long* p, int stride, i
 }
 
 // Lane-parallel twin of ll_sum: every lane polls ONE tagged word (act lanes; the others pass) until
-// all lanes of the warp hold theirs.  A thread's successive strong loads go out one after another
-// (B200, tools/mb_l2xchg.cu: 7 words polled by one lane ~5500 cycles per exchange round with 112
-// CTAs, one word per lane ~1650), so a sum over G clusters spreads its G polls over G lanes.
-// Warp-uniform call; the same spin bound and abort protocol as ll_sum.
+// all lanes of the warp hold theirs, so a sum over G clusters spreads its G polls over G lanes and
+// needs no per-lane word arrays (inlined: the __noinline__ ll_sum call cost the rka kernel its
+// spill-free register budget).  Warp-uniform call; the same spin bound and abort protocol as ll_sum.
 __device__ __forceinline__ double ll_poll_lane(const unsigned long long* p, bool act, unsigned tag, int* abort) {
     unsigned long long w0 = 0, w1 = 0;
     bool ok = !act;

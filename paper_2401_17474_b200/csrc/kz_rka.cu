@@ -29,8 +29,7 @@
 //          With G > 1 clusters the owners first exchange their cluster totals
 //          as tagged 64-bit words (value halves + iteration tag, single-copy
 //          atomic; no grid barrier, no fence; one 128-byte L2 line per slot),
-//          polled one word per lane (a thread's strong loads go out one after
-//          another), and add them in cluster order;
+//          polled one word per lane, and add them in cluster order;
 //       4. stop rule on the broadcast error total;
 //       5. average: each warp sums fl(x + fl(s_t a_t)) over its block; the 8
 //          per-warp sums meet in shared memory behind one named barrier and

@@ -21,9 +21,11 @@ __device__ __forceinline__ void ld2cg(const unsigned long long* p, unsigned long
     asm volatile("ld.global.cg.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-// MODE 0: one lane per worker polls the G groups in a loop (the rka kernel today); 1: lane (h, item)
-// polls one word, completion by ballot, the sum in group order by shuffles; 2: as 0 with
-// ld.volatile; 3: as 0 with ld.global.cg
+// MODE 0: one lane per worker polls the G groups in a loop over a runtime-indexed word array (local
+// memory: each load waits for the previous one's register -- the slow case); 1: lane (h, item) polls
+// one word, completion by ballot, the sum in group order by shuffles; 2: as 0 with ld.volatile;
+// 3: as 0 with ld.global.cg; 4: the 7 loads issued together into registers (G = 7); 5: volatile C++
+// loads
 template <int PAD, int MODE>
 __global__ void xchg(unsigned long long* words, int G, int rounds, long long* out) {
     const int c = blockIdx.x, g = c / 16, r = c % 16, lane = threadIdx.x;
@@ -51,7 +53,51 @@ __global__ void xchg(unsigned long long* words, int G, int rounds, long long* ou
             double v = mine ? (double)(w0 & 0xffffffffull) : 0.0;
             for (int o = 1; o < 8; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             acc += v;
-        } else if (lane < 4) {
+        } else if (MODE == 4 && lane < 4) {  // all 7 words in one asm statement (G == 7)
+            const int t = 4 * r + lane;
+            st2(base + ((size_t)g * Q1 + t) * PAD, (kk << 32) | 1u, (kk << 32) | 2u);
+            unsigned long long w[14];
+            for (;;) {
+                const unsigned long long* q0 = base + (size_t)t * PAD;
+                const size_t st = (size_t)Q1 * PAD;
+                asm volatile(
+                    "ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%14];\n"
+                    "ld.relaxed.gpu.global.v2.b64 {%2, %3}, [%15];\n"
+                    "ld.relaxed.gpu.global.v2.b64 {%4, %5}, [%16];\n"
+                    "ld.relaxed.gpu.global.v2.b64 {%6, %7}, [%17];\n"
+                    "ld.relaxed.gpu.global.v2.b64 {%8, %9}, [%18];\n"
+                    "ld.relaxed.gpu.global.v2.b64 {%10, %11}, [%19];\n"
+                    "ld.relaxed.gpu.global.v2.b64 {%12, %13}, [%20];\n"
+                    : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]), "=l"(w[4]), "=l"(w[5]), "=l"(w[6]),
+                      "=l"(w[7]), "=l"(w[8]), "=l"(w[9]), "=l"(w[10]), "=l"(w[11]), "=l"(w[12]), "=l"(w[13])
+                    : "l"(q0), "l"(q0 + st), "l"(q0 + 2 * st), "l"(q0 + 3 * st), "l"(q0 + 4 * st), "l"(q0 + 5 * st),
+                      "l"(q0 + 6 * st)
+                    : "memory");
+                bool all = true;
+                for (int h = 0; h < 14; ++h)
+                    if ((w[h] >> 32) != kk) all = false;
+                if (all) break;
+            }
+            for (int h = 0; h < 14; h += 2) acc += (double)(w[h] & 0xffffffffull);
+        } else if (MODE == 5 && lane < 4) {  // plain volatile C++ loads (compiler-scheduled)
+            const int t = 4 * r + lane;
+            st2(base + ((size_t)g * Q1 + t) * PAD, (kk << 32) | 1u, (kk << 32) | 2u);
+            volatile const unsigned long long* vb = base;
+            for (;;) {
+                unsigned long long w0[16], w1[16];
+                for (int h = 0; h < G; ++h) {
+                    w0[h] = vb[((size_t)h * Q1 + t) * PAD];
+                    w1[h] = vb[((size_t)h * Q1 + t) * PAD + 1];
+                }
+                bool all = true;
+                for (int h = 0; h < G; ++h)
+                    if ((w0[h] >> 32) != kk || (w1[h] >> 32) != kk) all = false;
+                if (all) {
+                    for (int h = 0; h < G; ++h) acc += (double)(w0[h] & 0xffffffffull);
+                    break;
+                }
+            }
+        } else if (MODE <= 3 && lane < 4) {
             const int t = 4 * r + lane;
             st2(base + ((size_t)g * Q1 + t) * PAD, (kk << 32) | 1u, (kk << 32) | 2u);
             unsigned long long w0[16], w1[16];
@@ -102,6 +148,8 @@ int main() {
         run<16, 1>(w, o, G);
         run<2, 2>(w, o, G);
         run<2, 3>(w, o, G);
+        run<16, 5>(w, o, G);
     }
+    run<16, 4>(w, o, 7);
     return 0;
 }
