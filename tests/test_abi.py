@@ -69,3 +69,27 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text and "kzo_" not in text, f
+
+
+def _header_struct_fields(name):
+    """Field names of a typedef'd struct in include/kz_b200.h, in order."""
+    src = open(os.path.join(ROOT, "include", "kz_b200.h")).read()
+    m = re.search(r"typedef struct\s*\{([^{}]*)\}\s*" + name + r"\s*;", src)
+    assert m, name
+    body = re.sub(r"/\*.*?\*/", "", m.group(1), flags=re.S)
+    return re.findall(r"\b(\w+)\s*;", body)
+
+
+def test_ctypes_structs_match_the_header():
+    """The ctypes mirrors of kz_params / kz_result (the package's _native and the stub a maintainer
+    copies from INTEGRATION.md) list the header's fields in order: kz_solve writes every field of
+    kz_result, so a shorter mirror would be written past."""
+    from paper_2401_17474_b200 import _native as N
+
+    for name, cls in (("kz_params", N.Params), ("kz_result", N.Result)):
+        assert [f[0] for f in cls._fields_] == _header_struct_fields(name), name
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    for name, cls in (("kz_params", "_Params"), ("kz_result", "_Result")):
+        m = re.search(r"class " + cls + r"\(C\.Structure\):.*?_fields_ = \[(.*?)\]\n", doc, flags=re.S)
+        assert m, cls
+        assert re.findall(r'\("(\w+)"', m.group(1)) == _header_struct_fields(name), name
