@@ -210,3 +210,48 @@ def test_fused_cross_rank_exchange_world1(gpu, oracle, n, budget):
     assert rf.iterations == o["iterations"] and rel_err(rf.x, o["x"]) <= PARITY_TOL
     o2 = oracle.solve(s.A, s.b, s.x_star, variant="rka", q=q, base_seed=7, scheme="distributed", budget=budget)
     assert rf2.iterations == o2["iterations"] and rel_err(rf2.x, o2["x"]) <= PARITY_TOL
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c3_width_world_emulation(gpu, oracle, world):
+    """The c3 configuration at N = 2 / 4 / 8 GPUs (64 workers per GPU, bs = 1000, distributed scheme)
+    as its one-GPU equivalent -- the sequential solver with q = 64 N, whose workers run in waves --
+    on a 64000 x 20000 leading crop of the counter-keyed system, against the oracle at every outer
+    iteration; and N emulated ranks (row shards, local steps summed in rank order) bit-identical
+    to it for the first two outer iterations (SURVEY 8(c) T5 / T6 at the c3 row width)."""
+    from paper_2401_17474_b200 import DeviceSystem, SolverConfig, solve_rkab_seq
+    from paper_2401_17474_b200.multigpu import CudaShard, plan_shards
+
+    Q, budget = 64 * world, 2
+    with DeviceSystem(m=64000, n=20000) as ds:
+        ds.generate_counter(0)
+        A, b, xr = ds.download()
+        cfg = SolverConfig(variant="rkab", q=Q, block_size=1000, base_seed=2, sampling_scheme="distributed")
+        cap = []
+        r = solve_rkab_seq(ds, cfg, budget=budget, capture=cap)
+    assert r.gpu["plan"]["waves"] >= 1 and len(cap) == budget
+    o = oracle.solve(A, b, xr, variant="rkab", q=Q, block_size=1000, base_seed=2, scheme="distributed",
+                     budget=budget, ckpt_every=1, nthreads=oracle.max_threads())
+    for j, ck in enumerate(o["checkpoints"]):
+        assert rel_err(cap[j], ck) <= PARITY_TOL, (world, j)
+    # the row-sharded protocol: rank g's shard and its 64 workers, the worker sums added in rank order
+    shards = [CudaShard(A[p.lo:p.hi + 1], b[p.lo:p.hi + 1], xr, p, device=0)
+              for p in (plan_shards(A.shape[0], world, g, 64) for g in range(world))]
+    try:
+        lcfg = cfg.replace(q=64)
+        for sh in shards:
+            sh.reset()
+        for k in range(budget):
+            S = [sh.step(lcfg, k) for sh in shards]
+            tot = S[0].clone()
+            for extra in S[1:]:
+                tot += extra
+            for sh in shards:
+                sh.finish(tot, Q)
+        xs = [sh.x() for sh in shards]
+    finally:
+        for sh in shards:
+            sh.close()
+    for x in xs[1:]:
+        assert np.array_equal(x, xs[0])
+    assert rel_err(xs[0], cap[-1]) <= PARITY_TOL
