@@ -54,7 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *os.environ.get("KZ_NVCC_EXTRA", "").split(), "-I", INCLUDE, "-c", src, "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     objs = []

@@ -439,6 +439,12 @@ __device__ __forceinline__ void tma_gather4(unsigned dst, const void* map, int c
         : "memory");
 }
 
+// L2 prefetch of `bytes` (a multiple of 16) from a 16-byte aligned global address: no shared memory,
+// no completion to wait for.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* gptr, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gptr), "r"(bytes) : "memory");
+}
+
 // Named barrier over the first `count` threads (the compute warps).
 __device__ __forceinline__ void named_sync(unsigned id, unsigned count) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");

@@ -54,6 +54,12 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                                                         const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB) {
     constexpr int NR = LG / 4;  // rows per lane group per round (8 rows per warp per round)
+    // rows whose shared-memory loads are issued together (RB x EPL 16-byte loads in flight per lane)
+#ifndef KZ_RKA_PF
+#define KZ_RKA_PF 2  // worker groups: L2 prefetch distance in iterations (0 = off)
+#endif
+    constexpr int RBW = EPL <= 1 ? NR : (EPL == 2 ? 4 : (EPL == 3 ? 2 : 1));
+    constexpr int RB = NR < RBW ? NR : RBW;
     static_assert(LG == 8 || LG == 16 || LG == 32, "lane group");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     if (a.halt != nullptr && *a.halt != 0) return;  // stopped earlier in the stream: uniform over the grid
@@ -168,6 +174,17 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                     tma_gather4(dst + rows_bytes + (unsigned)(g * 128), &tmB, 0, r[0], r[1], r[2], r[3], fb);
                 }
             }
+#if KZ_RKA_PF > 0
+            // worker groups: the row slices of iteration it + KZ_RKA_PF into L2, so the ring's refills
+            // (~q/G rows of every column box per CTA, two or three stages deep) hit L2 instead of HBM
+            // (c4 q = 512: 5.03 -> 4.75 us per iteration; the column-sliced plans do not gain and the
+            // one-cluster ones lose -- 64 more bulk instructions per 2 us iteration -- so they skip it)
+            if (wg && it + KZ_RKA_PF < a.count) {
+                const int32_t* ixp = a.idx + (it + KZ_RKA_PF) * qa + wlo;
+                for (int t = lane; t < q; t += 32)
+                    prefetch_l2_bulk(a.A + (size_t)__ldg(ixp + t) * (size_t)ld + c0, (unsigned)(wdt * 8));
+            }
+#endif
             if (++s == D) s = 0;
         }
         // drain: the last issued phase of every stage must land before exit
@@ -312,19 +329,47 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
             // SR (q <= 64): exactly one round of 8 rows per warp, row predicates precomputed
             for (int rb = wb, rofs = 0; SR ? rb == wb && wb < we : rb < we; rb += 8, rofs += rstep) {
                 double acc[NR];
+                if (SR ? rok == (1 << NR) - 1 : rb + grp * NR + NR <= we) {
+                    // all NR rows of the lane group exist: straight-line code, the loads of RB rows issued
+                    // together ahead of their FMA chains (per-row branches kept every load behind the
+                    // previous row's arithmetic: one exposed shared-memory latency per load)
 #pragma unroll
-                for (int r = 0; r < NR; ++r) {
-                    acc[r] = 0.0;
-                    const int t = rb + grp * NR + r;
-                    if (SR ? ((rok >> r) & 1) != 0 : t < we) {
-                        const double* row = rows + roff[r] + rofs;
+                    for (int r0 = 0; r0 < NR; r0 += RB) {
+                        double2 rv[RB][EPL];
 #pragma unroll
-                        for (int e = 0; e < EPL; ++e)
-                            if (vld[e]) {
-                                const double2 rv = *reinterpret_cast<const double2*>(row + 2 * LG * e);
-                                acc[r] = fma(rv.x, xv[e].x, acc[r]);
-                                acc[r] = fma(rv.y, xv[e].y, acc[r]);
-                            }
+                        for (int r = 0; r < RB; ++r)
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e)
+                                rv[r][e] = vld[e] ? *reinterpret_cast<const double2*>(rows + roff[r0 + r] + rofs +
+                                                                                       2 * LG * e)
+                                                  : make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int r = 0; r < RB; ++r) {
+                            double d = 0.0;
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e)
+                                if (vld[e]) {
+                                    d = fma(rv[r][e].x, xv[e].x, d);
+                                    d = fma(rv[r][e].y, xv[e].y, d);
+                                }
+                            acc[r0 + r] = d;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) {
+                        acc[r] = 0.0;
+                        const int t = rb + grp * NR + r;
+                        if (SR ? ((rok >> r) & 1) != 0 : t < we) {
+                            const double* row = rows + roff[r] + rofs;
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e)
+                                if (vld[e]) {
+                                    const double2 rv = *reinterpret_cast<const double2*>(row + 2 * LG * e);
+                                    acc[r] = fma(rv.x, xv[e].x, acc[r]);
+                                    acc[r] = fma(rv.y, xv[e].y, acc[r]);
+                                }
+                        }
                     }
                 }
 #pragma unroll
@@ -498,6 +543,37 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
 #pragma unroll
         for (int e = 0; e < EPL; ++e) acc[e] = make_double2(0.0, 0.0);
         for (int rb = wb; SR ? rb == wb && wb < we : rb < we; rb += 8) {
+            if (SR ? rok == (1 << NR) - 1 : rb + grp * NR + NR <= we) {
+                // all NR rows exist: the loads of RB rows (and their scales) ahead of the arithmetic,
+                // the sums in the same row order as below
+#pragma unroll
+                for (int r0 = 0; r0 < NR; r0 += RB) {
+                    double2 rv[RB][EPL];
+                    double sv[RB];
+#pragma unroll
+                    for (int r = 0; r < RB; ++r) {
+                        sv[r] = sc[rb + grp * NR + r0 + r];
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e)
+                            rv[r][e] = vld[e] ? *reinterpret_cast<const double2*>(rows + roff[r0 + r] +
+                                                                                   (rb - wb) * cwb + 2 * LG * e)
+                                              : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int r = 0; r < RB; ++r) {
+                        const bool first = (r0 + r == 0) && (rb == wb);
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e)
+                            if (vld[e]) {
+                                const double v0 = __dadd_rn(xv[e].x, __dmul_rn(sv[r], rv[r][e].x));
+                                const double v1 = __dadd_rn(xv[e].y, __dmul_rn(sv[r], rv[r][e].y));
+                                acc[e].x = first ? v0 : __dadd_rn(acc[e].x, v0);
+                                acc[e].y = first ? v1 : __dadd_rn(acc[e].y, v1);
+                            }
+                    }
+                }
+                continue;
+            }
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
                 const int t = rb + grp * NR + r;
