@@ -296,7 +296,11 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             st_async_f64(mapa_u32(smem_u32(xbuf + (xp * C + h) * Blk<R>::NVC + vi), peer), sm.tot[vi],
                          mapa_u32(smem_u32(&xbar[xp]), peer));
         }
-        mbar_wait_cluster(&xbar[xp], ph);
+        // the peers' totals arrive by st.async into THIS CTA's shared memory and complete xbar's
+        // bytes; a CTA-scope wait sees them (as in the rka kernel's exchanges) -- the cluster-scope
+        // acquire form compiles to an L1 invalidate (CCTL.IVALL) after every join, 5.6 % of the
+        // c4-shape RKAB kernel's stall samples, and evicts the row indices and (b, sq) lines
+        mbar_wait(&xbar[xp], ph);
         for (int i = 0; i < nv; ++i) {
             double acc = h == 0 ? vals[i] : xbuf[(xp * C) * Blk<R>::NVC + i];
             for (int c = 1; c < C; ++c) acc = __dadd_rn(acc, c == h ? vals[i] : xbuf[(xp * C + c) * Blk<R>::NVC + i]);
