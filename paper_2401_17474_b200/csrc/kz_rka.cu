@@ -153,6 +153,12 @@ __global__ void __launch_bounds__(RKA_NT, 1) rka_kernel(const __grid_constant__ 
                 if (!ok) break;
             }
             if (*halt) break;
+            if (TIMING && (a.ablate & 32) && it >= D) {  // ablation: no refills (stale rows), the stage completes at once
+                if (lane == 0) mbar_arrive(&full[s]);
+                __syncwarp();
+                if (++s == D) s = 0;
+                continue;
+            }
             const unsigned dst = ring_u + (unsigned)(s * stage_bytes);
             const int32_t* ix = a.idx + it * qa + wlo;
             if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
