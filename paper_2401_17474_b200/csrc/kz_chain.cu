@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         mbar_init(&xbar[1], 1);
         for (int k = 0; k < D; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], 1);
+            mbar_init(&empty[k], EP < 16 ? 1 : nw);  // EP = 16: one release per compute warp
         }
         *halt = 0;
         fence_mbarrier_init_cluster();
@@ -537,14 +537,28 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         }
         if (rec) a.dbg[nblk * 8 + 6] = clock64();
         ++nblk;
-        // the applied rows' stages go back to the producer (every thread read them before the
-        // reduction's barriers: rows live in registers, (b, sq) in lanes)
-        if (tid == 0)
-            for (int r = 0; r < Reff; ++r) {
-                int st = c_stage + r;
-                if (st >= D) st -= D;
-                mbar_arrive(&empty[st]);
-            }
+        // the applied rows' stages go back to the producer.  Rows kept in registers: every thread
+        // read them before the reduction's barriers, so one thread releases -- the last compute
+        // thread, not thread 0, whose warp also runs the reduction's cross-warp pass and the cluster
+        // join (RK n = 2000 0.382 -> 0.370 us per row, c2 146.9 -> 144.4 and c4-shape RKAB 664 ->
+        // 649 us per outer iteration).  Rows re-read from the ring by the update (EP = 16): every
+        // warp releases after its own re-reads (the stage barriers count the compute warps).
+        if constexpr (KEEP_ROW) {
+            if (tid == T - 1)
+                for (int r = 0; r < Reff; ++r) {
+                    int st = c_stage + r;
+                    if (st >= D) st -= D;
+                    mbar_arrive(&empty[st]);
+                }
+        } else {
+            __syncwarp();
+            if (lane == 0)
+                for (int r = 0; r < Reff; ++r) {
+                    int st = c_stage + r;
+                    if (st >= D) st -= D;
+                    mbar_arrive(&empty[st]);
+                }
+        }
         d += Reff;
         c_stage += Reff;
         if (c_stage >= D) {
