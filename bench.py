@@ -559,8 +559,30 @@ def extra_workloads(device, peak, steps=3):
     def c2():
         s2 = generate_mother(GeneratorConfig(m_max=80000, n_max=1000, seed=0))
         with DeviceSystem(s2, device=device) as ds:
-            measure("c2", ds, 1000, SolverConfig(variant="rkab", q=64, block_size=500, device=device), None,
-                    "c2: RKAB q=64 bs=500 80000x1000, solve to eps")
+            cfg = SolverConfig(variant="rkab", q=64, block_size=500, device=device)
+            measure("c2", ds, 1000, cfg, None, "c2: RKAB q=64 bs=500 80000x1000, solve to eps")
+            # BASELINE c2's 10 seeds, two solves side by side: one solve occupies 64 of the 148 SMs
+            # (64 workers, one CTA each), so a second lane runs on the others
+            cfgs = [cfg.replace(base_seed=k) for k in range(SEEDS)]
+            solve_concurrent(ds, cfgs, lanes=2)
+            best = None
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                rs = solve_concurrent(ds, cfgs, lanes=2)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1)
+                best = (ms, rs) if best is None or ms < best[0] else best
+            ms, rs = best
+            rows = sum(r.gpu["rows_projected"] for r in rs)
+            gbs = rows * 8 * 1000 / (ms / 1e3) / 1e9
+            out.append({"workload": "c2_ten_seeds", "desc": "c2: RKAB q=64 bs=500 80000x1000, the 10 seed-solves to "
+                        "eps two at a time (solve_concurrent, lanes=2)", "rows_per_s": rows / (ms / 1e3),
+                        "ms_per_step": ms, "iterations": [r.iterations for r in rs],
+                        "converged": [r.converged for r in rs], "kernel": rs[0].gpu["kernel"],
+                        "roofline": {"achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
+                                     "note": "aggregate over the two lanes"}})
 
     def c1():
         # c1's 10 seed-solves side by side (solve_concurrent: 10 lanes, one 16-CTA cluster each)
