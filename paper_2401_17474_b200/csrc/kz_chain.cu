@@ -93,8 +93,9 @@ __device__ __forceinline__ void warp_transpose32(const double* v, double* dst, i
     if (lane < NV32) dst[lane] = w[0];
 }
 
-template <int NV>
-__device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double* tot, int tid, int T, int nw) {
+template <int NV, typename OnTotal>
+__device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double* tot, int tid, int T, int nw,
+                                           OnTotal on_total) {
     constexpr int NP = NV <= 32 ? 32 : 64;
     static_assert(NV <= 64, "cta_reduce: at most 64 values");
     const int lane = tid & 31, warp = tid >> 5;
@@ -122,6 +123,7 @@ __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double*
 #pragma unroll
             for (int k = 0; k + hh < 16; k += 2 * hh) a[k] = __dadd_rn(a[k], a[k + hh]);
         tot[u] = a[0];
+        on_total(u, a[0]);  // the cluster join's push leaves from the thread that formed the total
     }
     named_sync(1, T);
 #pragma unroll
@@ -282,20 +284,26 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
     // join the C slices of a reduction: every CTA sends its totals to every peer (slot
     // [parity][sender][value]) and adds the C totals in CTA order, so all hold the same bits
     // (for a pair the order is immaterial: IEEE addition is commutative)
+    // total u of the current reduction -> slot [parity][this CTA][u] of every peer, by the thread
+    // that formed it (before the reduction's second barrier: the peers' waits end that much sooner)
+    auto push_total = [&](int u, double val) {
+        if (C < 2) return;
+        const int xp = nex & 1;
+        const int u_o = opaque_i32(u);  // slot arithmetic formed here, not hoisted out of the row loop
+#pragma unroll
+        for (int pk = 0; pk < C - 1; ++pk) {
+            const unsigned peer = (unsigned)(pk < h ? pk : pk + 1);
+            st_async_f64(mapa_u32(smem_u32(xbuf + (xp * C + h) * Blk<R>::NVC + u_o), peer), val,
+                         mapa_u32(smem_u32(&xbar[xp]), peer));
+        }
+    };
     auto pair_join = [&](double* vals, int nv) {
         if (C < 2) return;
         const int xp = nex & 1;
         const unsigned ph = (unsigned)((nex >> 1) & 1);
         ++nex;
         if (tid == 0) mbar_arrive_expect_tx(&xbar[xp], (unsigned)((C - 1) * nv * sizeof(double)));
-        // tid through an opaque move: the slot arithmetic below is formed here, not hoisted out
-        // of the row loop into registers the EP = 16 kernels would spill
-        for (int i = opaque_i32(tid); i < (C - 1) * nv; i += T) {
-            const int vi = i % nv, pk = i / nv;
-            const unsigned peer = (unsigned)(pk < h ? pk : pk + 1);
-            st_async_f64(mapa_u32(smem_u32(xbuf + (xp * C + h) * Blk<R>::NVC + vi), peer), sm.tot[vi],
-                         mapa_u32(smem_u32(&xbar[xp]), peer));
-        }
+        // (the totals were pushed to the peers by push_total, from inside the reduction)
         // the peers' totals arrive by st.async into THIS CTA's shared memory and complete xbar's
         // bytes; a CTA-scope wait sees them (as in the rka kernel's exchanges) -- the cluster-scope
         // acquire form compiles to an L1 invalidate (CCTL.IVALL) after every join, 5.6 % of the
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 e[0] = fma(d1, d1, e[0]);
             }
         }
-        cta_reduce<1>(e, sm.scr, sm.tot, tid, T, nw);
+        cta_reduce<1>(e, sm.scr, sm.tot, tid, T, nw, push_total);
         pair_join(e, 1);
         return e[0];
     };
@@ -451,7 +459,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             }
         }
         if (rec) a.dbg[nblk * 8 + 3] = clock64();
-        cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw);
+        cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw, push_total);
         pair_join(vals, NV);
         if (rec) a.dbg[nblk * 8 + 4] = clock64();
         // every row's (b, sq, 1/sq) to all lanes up front: the shuffles leave the sequential chain
