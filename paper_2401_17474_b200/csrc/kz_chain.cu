@@ -473,13 +473,27 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         double s[R];
         int Reff = Rp;
         double e = CHECK ? vals[NV - 1] : 0.0;
+        // s_r = alpha (b_r - <a_r, v> - sum_{l<r} s_l <a_r, a_l>) / sq_r as c_r - sum_l s_l g_rl with
+        // c_r = (b_r - <a_r, v>) (alpha / sq_r) and g_rl = <a_r, a_l> (alpha / sq_r) formed up front,
+        // independent of the scales: the sequential chain s_0 -> s_1 -> ... is one FMA per row
+        // instead of FMA, subtraction and two multiplications
+        double cs[R], gs[Blk<R>::NG > 0 ? Blk<R>::NG : 1];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double ai = __dmul_rn(alpha, invrs[r]);
+            cs[r] = __dmul_rn(__dsub_rn(brs[r], vals[r]), ai);
+#pragma unroll
+            for (int l = 0; l < r; ++l) gs[gidx(r, l)] = __dmul_rn(vals[R + gidx(r, l)], ai);
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             if (r < Reff) {
-                const double br = brs[r], sqr = sqrs[r], invr = invrs[r];
+                const double sqr = sqrs[r];
                 double dr = vals[r];
+                if (CHECK) {  // <a_r, v_r> itself: the error update below (off the scales' chain)
 #pragma unroll
-                for (int l = 0; l < r; ++l) dr = fma(s[l], vals[R + gidx(r, l)], dr);
+                    for (int l = 0; l < r; ++l) dr = fma(s[l], vals[R + gidx(r, l)], dr);
+                }
                 if (CHECK && d + r == next_check) {
                     if (r == 0) {
                         ++checks;
@@ -497,7 +511,10 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                 }
                 if (r < Reff) {
                     if (CHECK && d + r == next_check) next_check += bs;
-                    s[r] = __dmul_rn(__dmul_rn(alpha, __dsub_rn(br, dr)), invr);
+                    double sr = cs[r];
+#pragma unroll
+                    for (int l = 0; l < r; ++l) sr = fma(-s[l], gs[gidx(r, l)], sr);
+                    s[r] = sr;
                     if (CHECK) e = fma(s[r] * s[r], sqr, fma(2.0 * s[r], dr - vals[Blk<R>::NVN + r], e));
                 }
             }
