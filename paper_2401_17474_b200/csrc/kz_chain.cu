@@ -419,7 +419,11 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             return lds_reread_f64x2(sm.ring + (size_t)stg[r] * ldr + lc);
         };
         double2 bq = make_double2(0.0, 1.0);
-        if (lane < Rp) {
+        if constexpr (R == 1) {
+            // one row per reduction: every lane reads the (b, sq) pair and divides for itself (in the
+            // shadow of the dot's shared-memory reads); no shuffle between the join and the scale
+            if (Rp > 0) bq = sm.bsq[c_stage];
+        } else if (lane < Rp) {
             int sl = c_stage + lane;
             if (sl >= D) sl -= D;
             bq = sm.bsq[sl];
@@ -459,17 +463,20 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             }
         }
         if (rec) a.dbg[nblk * 8 + 3] = clock64();
-        cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw, push_total);
-        pair_join(vals, NV);
-        if (rec) a.dbg[nblk * 8 + 4] = clock64();
-        // every row's (b, sq, 1/sq) to all lanes up front: the shuffles leave the sequential chain
+        // every row's (b, sq) to all lanes before the reduction (they need no division), alpha / sq
+        // after it (the division in lane r overlaps the reduction): two of the three shuffle rounds
+        // leave the path between the join and the scales
         double brs[R], sqrs[R], invrs[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            brs[r] = __shfl_sync(0xffffffffu, bq.x, r);
-            sqrs[r] = __shfl_sync(0xffffffffu, bq.y, r);
-            invrs[r] = __shfl_sync(0xffffffffu, inv_l, r);
+            brs[r] = R == 1 ? bq.x : __shfl_sync(0xffffffffu, bq.x, r);
+            sqrs[r] = R == 1 ? bq.y : __shfl_sync(0xffffffffu, bq.y, r);
         }
+        cta_reduce<NV>(vals, sm.scr, sm.tot, tid, T, nw, push_total);
+        pair_join(vals, NV);
+        if (rec) a.dbg[nblk * 8 + 4] = clock64();
+#pragma unroll
+        for (int r = 0; r < R; ++r) invrs[r] = R == 1 ? inv_l : __shfl_sync(0xffffffffu, inv_l, r);
         double s[R];
         int Reff = Rp;
         double e = CHECK ? vals[NV - 1] : 0.0;
