@@ -412,7 +412,9 @@ def run_b200(args, rank, world, local_rank):
                      "algorithmic_bytes": "8*n = 160000 bytes per row projection; one outer iteration = "
                                           f"{C3_Q} workers x {C3_BS} rows = 10.24 GB per GPU",
                      "note": "achieved = rows x 8n / summed device time of the solve-kernel launches (CUDA events "
-                             "on the launching stream, rank 0)"},
+                             "on the launching stream, rank 0); the peak is a COPY bandwidth (read + write), the "
+                             "kernel a read-only stream (6.98 TB/s of DRAM reads in the ncu capture), so frac can "
+                             "pass 1"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "api": "solve_rkab_seq(LinearSystem(host arrays), cfg)" if world == 1
