@@ -93,6 +93,29 @@ __device__ __forceinline__ void warp_transpose32(const double* v, double* dst, i
     if (lane < NV32) dst[lane] = w[0];
 }
 
+// The same for at most 16 values in half the shuffles: the values are halved across lanes at xor
+// offsets 16, 8, 4, 2 (8 + 4 + 2 + 1 shuffles), which leaves lane l with value (l >> 1) summed over
+// the 16 lanes of its parity, and one butterfly step at xor 1 completes the warp sum (both lanes of
+// a pair hold the same bits; the even one stores).
+template <int NV16>
+__device__ __forceinline__ void warp_transpose16(const double* v, double* dst, int lane) {
+    double w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = i < NV16 ? v[i] : 0.0;
+#pragma unroll
+    for (int h = 8, o = 16; o >= 2; h >>= 1, o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = up ? w[i] : w[i + h];
+            const double keep = up ? w[i + h] : w[i];
+            w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    const double tot = w[0] + __shfl_xor_sync(0xffffffffu, w[0], 1);
+    if ((lane & 1) == 0 && (lane >> 1) < NV16) dst[lane >> 1] = tot;
+}
+
 template <int NV, typename OnTotal>
 __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double* tot, int tid, int T, int nw,
                                            OnTotal on_total) {
@@ -107,6 +130,8 @@ __device__ __forceinline__ void cta_reduce(double (&v)[NV], double* scr, double*
             for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
             if (lane == i) scr[warp * NP + i] = x;
         }
+    } else if (NV <= 12) {  // (the stop-rule blocks' 15 values measured faster on the 32-wide form)
+        warp_transpose16<NV>(v, scr + warp * NP, lane);
     } else if (NV <= 32) {
         warp_transpose32<NV>(v, scr + warp * NP, lane);
     } else {  // two passes of 32: the padded 64-value transpose would hold 128 registers at once
@@ -381,12 +406,17 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
         // rows d .. d + Rp - 1 landed: the R barrier probes go out together (one ~90-cycle
         // round trip instead of R); only stragglers are re-polled
         {
-            bool okr[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) okr[r] = r >= Rp || mbar_test(&full[stg[r]], prs[r]);
+            unsigned okm;
+            if constexpr (R == 4)
+                okm = mbar_test4(&full[stg[0]], prs[0], &full[stg[1]], prs[1], &full[stg[2]], prs[2], &full[stg[3]],
+                                 prs[3]);
+            else if constexpr (R == 2)
+                okm = mbar_test2(&full[stg[0]], prs[0], &full[stg[1]], prs[1]);
+            else
+                okm = mbar_test(&full[stg[0]], prs[0]) ? 1u : 0u;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (!okr[r]) mbar_wait(&full[stg[r]], prs[r]);
+                if (r < Rp && !((okm >> r) & 1u)) mbar_wait(&full[stg[r]], prs[r]);
         }
         if (rec) a.dbg[nblk * 8 + 2] = clock64();
         // rows -> registers (kept for the update), (b, sq) -> lane r.  EP = 16 (168 registers per

@@ -514,6 +514,43 @@ __device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned pari
     return done != 0;
 }
 
+// Two / four barrier probes issued back to back (one asm block: a warp issues in order, and a probe
+// followed by the selp that reads its predicate holds the next probe back for the full latency --
+// four separate probes cost ~300 cycles in the chain kernel's block prologue).  Bit r of the result:
+// phase p_r of barrier b_r complete.
+__device__ __forceinline__ unsigned mbar_test2(unsigned long long* b0, unsigned p0, unsigned long long* b1,
+                                               unsigned p1) {
+    unsigned m;
+    asm volatile(
+        "{\n .reg .pred q0, q1;\n .reg .u32 t0, t1;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %3;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 q1, [%2], %4;\n"
+        " selp.u32 t0, 1, 0, q0;\n selp.u32 t1, 2, 0, q1;\n"
+        " or.b32 %0, t0, t1;\n}\n"
+        : "=r"(m)
+        : "r"(smem_u32(b0)), "r"(smem_u32(b1)), "r"(p0), "r"(p1)
+        : "memory");
+    return m;
+}
+__device__ __forceinline__ unsigned mbar_test4(unsigned long long* b0, unsigned p0, unsigned long long* b1,
+                                               unsigned p1, unsigned long long* b2, unsigned p2,
+                                               unsigned long long* b3, unsigned p3) {
+    unsigned m;
+    asm volatile(
+        "{\n .reg .pred q0, q1, q2, q3;\n .reg .u32 t0, t1, t2, t3;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 q0, [%1], %5;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 q1, [%2], %6;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 q2, [%3], %7;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 q3, [%4], %8;\n"
+        " selp.u32 t0, 1, 0, q0;\n selp.u32 t1, 2, 0, q1;\n selp.u32 t2, 4, 0, q2;\n selp.u32 t3, 8, 0, q3;\n"
+        " or.b32 t0, t0, t1;\n or.b32 t2, t2, t3;\n or.b32 %0, t0, t2;\n}\n"
+        : "=r"(m)
+        : "r"(smem_u32(b0)), "r"(smem_u32(b1)), "r"(smem_u32(b2)), "r"(smem_u32(b3)), "r"(p0), "r"(p1), "r"(p2),
+          "r"(p3)
+        : "memory");
+    return m;
+}
+
 }  // namespace kz
 
 
