@@ -21,10 +21,11 @@
 //     d_r = <a_r, v>   and   G_rl = <a_r, a_l> (l < r),
 // then resolves the chain exactly as the reference orders it:
 //     <a_r, v_{r-1}> = d_r + sum_{l<r} s_l G_rl,  s_r = alpha (b_r - <a_r, v_{r-1}>) / sq_r,
-// and applies v += s_r a_r row by row with the reference's rounding
-// (__dmul_rn then __dadd_rn).  The dot products are therefore rebracketed
-// (tolerance parity, like any change of summation order); the updates and
-// the averaging are the reference's.  1/sq_r replaces the division.
+// and applies v += s_r a_r row by row: with the reference's rounding
+// (__dmul_rn then __dadd_rn) when R = 1, as one FMA per element in blocks of
+// R > 1 rows, whose scales are already rebracketed.  The dot products are
+// rebracketed (tolerance parity, like any change of summation order); the
+// averaging is the reference's.  1/sq_r replaces the division.
 //
 // The stop rule (RK and RKAB with q = 1 check between rows) rides along:
 // the same reduction carries ||v - x_ref||^2 and <a_r, x_ref>, and
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
             }
         }
         if (rec) a.dbg[nblk * 8 + 5] = clock64();
-        // apply the Reff projections in order with the reference's rounding.  The threaded RKA
+        // apply the Reff projections in order (R = 1: the reference's multiply-then-add rounding).  The threaded RKA
         // publishes the increment itself: v restarts from 0 (0 + fl(s a) is exact; v is reloaded
         // from x after the combine), so the row loop below is the same for every engine
         if (rka_delta) {
@@ -572,8 +573,16 @@ __global__ void __launch_bounds__(ChainMaxThreads<EP>::value + 32, 1) chain_kern
                     const int lc = 2 * (p * T + tid);
                     if (PADDED || lc < ldc) {  // padded: the zero tail leaves v past ldc at 0
                         const double2 ap = row_again(r, p);
-                        v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], ap.x));
-                        v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], ap.y));
+                        if constexpr (R > 1) {
+                            // Gram-corrected blocks already round differently from the reference's
+                            // row-by-row arithmetic (within the 1e-10 parity bar): their update is one
+                            // FMA per element, half the FP64 instructions of the block's apply phase
+                            v[2 * p] = fma(s[r], ap.x, v[2 * p]);
+                            v[2 * p + 1] = fma(s[r], ap.y, v[2 * p + 1]);
+                        } else {
+                            v[2 * p] = __dadd_rn(v[2 * p], __dmul_rn(s[r], ap.x));
+                            v[2 * p + 1] = __dadd_rn(v[2 * p + 1], __dmul_rn(s[r], ap.y));
+                        }
                     }
                 }
                 if (q == 1 && d + r + 1 == outer_end) {  // outer iteration kdone completes here
